@@ -1,0 +1,238 @@
+/* semwarm_b200 — C-ABI of the B200-native SoundWeaver warm-start path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch types. Every entry
+ * point names the reference interface it replaces (file:line under /root/reference/proj).
+ * The reference has no FFI of its own; its boundary is the C++ class API of
+ * include/semwarm/{index,selector,gater,cache}.hpp called by Pipeline (pipeline.cpp:91-297).
+ * The C++ shim in paper_2603_07865_b200/csrc/host/semwarm_b200.hpp re-exposes those C++
+ * signatures on top of this ABI; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns int: SW_OK (0), a negative error, or a positive soft warning
+ *    (the reference's warn()-and-no-op cases). No exception crosses the ABI.
+ *  - sw_last_error() returns a thread-local message for the last failing call.
+ *  - "d_" arguments are device pointers; calls taking a `stream` are stream-ordered and
+ *    asynchronous. "_host" variants take host pointers and return synchronously.
+ *  - Readers (search/plan/align) may run concurrently; arena mutations are exclusive and
+ *    synchronous, mirroring the shared/unique locks of pipeline.cpp:216,264,282.
+ */
+#ifndef SEMWARM_B200_H
+#define SEMWARM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW_OK 0
+#define SW_EINVAL (-1)        /* std::invalid_argument in the reference */
+#define SW_ERUNTIME (-2)      /* std::runtime_error */
+#define SW_ECUDA (-3)         /* CUDA / driver failure */
+#define SW_ENOMEM (-4)        /* arena or device memory exhausted */
+#define SW_WARN_UNKNOWN_ID 1  /* warn("... unknown entry id") + no-op (index.cpp:243-245) */
+
+/* sw_config.flags */
+#define SW_FLAG_EXACT_ONLY 0x1u   /* never use the tcgen05 pre-filter: fp64 brute force only */
+#define SW_FLAG_TC_ALWAYS 0x2u    /* use the tcgen05 pre-filter even for tiny caches (tests) */
+
+/* sw_choice.flags */
+#define SW_CHOICE_AMBIGUOUS_DRAW 0x1u  /* |acc - target| within exp() ulp slack (H3) */
+#define SW_CHOICE_NONFINITE_PHI 0x2u   /* non-finite features -> arm 0 (gater.cpp:71-76) */
+#define SW_CHOICE_INCOMPLETE 0x4u      /* candidate buffer overflow: search not certified */
+#define SW_CHOICE_AMBIGUOUS_ARM 0x8u   /* explore-mode softplus within ulp slack of a tie */
+
+typedef struct sw_ctx sw_ctx;
+
+/* Arena geometry. One context = one device-resident cache shard. */
+typedef struct sw_config {
+    int32_t dim;             /* embedding dimension D (EmbeddingVector::dim, core.hpp:15-24) */
+    int32_t rows_per_entry;  /* max pyramid rows per entry (7 at delta=1/4, index.cpp:12-31) */
+    int64_t max_entries;     /* entry capacity (CacheConfig::capacity, cache.hpp:33) */
+    int32_t latent_c;        /* latent slot shape [C][T_max][F], fp32 (8 x 256 x 16) */
+    int32_t latent_t_max;
+    int32_t latent_f;
+    int32_t max_batch;       /* largest B any batched call will pass */
+    int64_t latent_slots;    /* 0 -> max_entries; fewer -> slot = entry_slot % latent_slots */
+    double latent_fps;       /* latent frame rate (25 frames/s = 256 frames per 10.24 s) */
+    uint32_t flags;          /* SW_FLAG_* */
+    int32_t reserved;
+} sw_config;
+
+/* PyramidDescriptor (index.hpp:13-17) */
+typedef struct sw_segment {
+    int32_t level;
+    int32_t reserved;
+    double start_s;
+    double length_s;
+} sw_segment;
+
+/* SearchHit (index.hpp:25-29) */
+typedef struct sw_hit {
+    uint64_t entry_id;
+    sw_segment segment;
+    double similarity;
+} sw_hit;
+
+/* SelectorConfig (selector.hpp:25-33); the negative embedding is set with sw_set_negative */
+typedef struct sw_selector_config {
+    int32_t top_k;
+    int32_t reserved;
+    double temperature;
+    double quality_threshold;
+} sw_selector_config;
+
+/* SkipPolicy + its parameters (pipeline.hpp:17-22, 37-41) */
+#define SW_POLICY_EXPLOIT 0
+#define SW_POLICY_EXPLORE 1
+#define SW_POLICY_RULE 2
+#define SW_POLICY_FIXED 3
+typedef struct sw_policy {
+    int32_t kind;
+    int32_t fixed_arm;
+    double rule_similarity_threshold;
+    double rule_skip_fraction;
+} sw_policy;
+
+/* GenerationRequest (core.hpp:45-51) minus the prompt, which travels as a B x D fp32 matrix */
+typedef struct sw_request {
+    uint64_t id;
+    double duration_s;
+    int32_t total_steps;
+    int32_t reserved;
+} sw_request;
+
+/* Result of plan_request + pick_arm + t* (pipeline.cpp:91-202, simgen.cpp:70): the
+ * ServeOutcome fields cache_hit, entry_id, arm_index, steps_skipped, reference_similarity
+ * (core.hpp:54-67) plus the chosen segment and where its latent lives. */
+typedef struct sw_choice {
+    int32_t hit;
+    int32_t arm;
+    int32_t steps_skipped;
+    int32_t n_hits;
+    uint64_t entry_id;
+    sw_segment segment;
+    double similarity;
+    double skip_fraction;
+    int32_t pick;    /* index of the chosen candidate in the top-k list, -1 on a miss */
+    uint32_t flags;  /* SW_CHOICE_* */
+    int32_t t_out;   /* aligned latent frames written by sw_align_noise (0 on a miss) */
+    int32_t owner;   /* shard rank that owns the chosen entry */
+    int64_t slot;    /* arena slot of the chosen entry on its owner shard */
+} sw_choice;
+
+/* Per-shard top-k record exchanged by the multi-GPU all-gather (128 bytes). */
+#define SW_HIT_RECORD_BYTES 128
+
+/* ---------------------------------------------------------------- context */
+int sw_ctx_create(const sw_config* cfg, int device, sw_ctx** out);
+int sw_ctx_destroy(sw_ctx* ctx);
+const char* sw_last_error(void);
+int sw_version(void);
+
+/* SelectorConfig::negative_embedding (selector.hpp:31, make_negative_embedding selector.cpp:16-20).
+ * Host pointer, D floats. Recomputes every stored row's s_neg. */
+int sw_set_negative(sw_ctx* ctx, const float* neg);
+/* BanditModel theta/psi/beta (gater.hpp:35-52), host pointers, 14 x feature_dim fp32 each. */
+int sw_set_gater(sw_ctx* ctx, const float* theta, const float* psi, int32_t feature_dim,
+                 double beta);
+/* Forward-noising schedule abar[0..n-1] (fp64, abar[0] = 1). Default: scaled-linear
+ * 0.00085..0.012 over 1000 DDPM steps. Index used: llround((T - t*) * (n-1) / T). */
+int sw_set_schedule(sw_ctx* ctx, const double* abar, int32_t n);
+
+/* ---------------------------------------------------------------- arena (Cache Manager data plane)
+ * IvfIndex::insert (index.cpp:226-239) + the latent payload CacheManager::admit stores
+ * (cache.cpp:30-52). rows: n_rows x D fp32 in pyramid order (level 0 first); segs: n_rows;
+ * latent: C x t_src x F fp32 or NULL. Host pointers. Inserting an id that already exists
+ * appends its rows (IvfIndex keeps per-entry counts, index.cpp:234-235). */
+int sw_arena_insert(sw_ctx* ctx, uint64_t entry_id, int32_t n_rows, const float* rows,
+                    const sw_segment* segs, const float* latent, int32_t t_src);
+/* Bulk insert of n entries; entry e owns rows [row_off[e], row_off[e+1]). If src_on_device,
+ * rows/segs/latents are device pointers (latents: n x C x t_src[e] x F packed at lat_off[e]). */
+int sw_arena_insert_batch(sw_ctx* ctx, int64_t n, const uint64_t* ids, const int64_t* row_off,
+                          const float* rows, const sw_segment* segs, const float* latents,
+                          const int64_t* lat_off, const int32_t* t_src, int32_t src_on_device);
+/* IvfIndex::remove (index.cpp:241-255): SW_WARN_UNKNOWN_ID for an unknown id. */
+int sw_arena_remove(sw_ctx* ctx, uint64_t entry_id);
+/* CacheManager::refine's re-index (cache.cpp:129-139): replace rows/latent of an entry in place. */
+int sw_arena_replace(sw_ctx* ctx, uint64_t entry_id, int32_t n_rows, const float* rows,
+                     const sw_segment* segs, const float* latent, int32_t t_src);
+int64_t sw_arena_entry_count(const sw_ctx* ctx);  /* IvfIndex::entry_count (index.hpp:74) */
+int sw_arena_contains(const sw_ctx* ctx, uint64_t entry_id); /* index.hpp:75 */
+/* Benchmark fill: n entries with ids first_id.. of seeded iid unit rows generated on the
+ * device (Philox normals, fp64 normalise, fp32 round), durations U[4,12] s, pyramid rows per
+ * the context's rows_per_entry, latents N(0,1). Deterministic in seed. */
+int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t seed,
+                            double delta);
+/* Copy stored fp32 rows of an entry back to host (n_rows_cap x D); returns rows copied. */
+int sw_arena_read_rows(sw_ctx* ctx, uint64_t entry_id, float* rows, int32_t n_rows_cap);
+
+/* ---------------------------------------------------------------- batched hot path
+ * IvfIndex::search (index.cpp:289-326) in exhaustive mode for B queries: exact fp64 cosine,
+ * best segment per entry, (sim desc, id asc), truncated to k. d_out: B x k, d_n: B. */
+int sw_search(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, sw_hit* d_out,
+              int32_t* d_n, void* stream);
+int sw_search_host(sw_ctx* ctx, const float* queries, int32_t B, int32_t k, sw_hit* out,
+                   int32_t* n);
+
+/* Pipeline::plan_request + pick_arm + t* (pipeline.cpp:91-202, simgen.cpp:70) for B requests:
+ * search -> score_candidates -> select (Rng(derive_seed(seed, id, 2)), pipeline.cpp:211) ->
+ * context_features -> choose_arm / rule / fixed -> steps_skipped = llround(0.05 arm T). */
+int sw_plan(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, int32_t B,
+            uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+            sw_choice* d_out, void* stream);
+
+/* Temporal alignment of the chosen cached latent to the request (crop / tile cyclically along
+ * T, slice_clip frame math simgen.cpp:113-128) fused with forward noising
+ * x_t = sqrt(abar)*x0 + sqrt(1-abar)*eps. d_eps: B x C x t_out_max x F, or NULL for Philox
+ * noise keyed by (philox_seed, request id). d_out: B x C x t_out_max x F. Misses untouched. */
+int sw_align_noise(sw_ctx* ctx, const sw_choice* d_choices, const sw_request* d_reqs,
+                   int32_t B, const float* d_eps, uint64_t philox_seed, float* d_out,
+                   int32_t t_out_max, void* stream);
+
+/* plan + align_noise in one stream-ordered call (the whole warm-start path). */
+int sw_warmstart(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, int32_t B,
+                 uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                 const float* d_eps, uint64_t philox_seed, sw_choice* d_choices, float* d_out,
+                 int32_t t_out_max, void* stream);
+/* End-to-end from host buffers (pinned or pageable): H2D prompts+requests, warm start,
+ * D2H choices; the noised latents stay on the device in d_out. Synchronous. */
+int sw_warmstart_host(sw_ctx* ctx, const float* queries, const sw_request* reqs, int32_t B,
+                      uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                      uint64_t philox_seed, sw_choice* choices, float* d_out,
+                      int32_t t_out_max, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU (entry-sharded)
+ * Per-shard top-k records for the all-gather: B x k records of SW_HIT_RECORD_BYTES plus a
+ * count per query. `rank` is stamped into each record. */
+int sw_local_topk(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, int32_t rank,
+                  void* d_records, int32_t* d_n, void* stream);
+/* Deterministic merge of world x (B x k) gathered records (sim desc, id asc) followed by
+ * score_candidates / select / gater / t* (replicated on every rank; no broadcast needed). */
+int sw_merge_select(sw_ctx* ctx, const void* d_gathered, const int32_t* d_gathered_n,
+                    int32_t world, const float* d_queries, const sw_request* d_reqs, int32_t B,
+                    int32_t k, uint64_t seed, const sw_selector_config* sel,
+                    const sw_policy* pol, sw_choice* d_out, void* stream);
+/* Owner-computes alignment: only requests whose chosen entry has owner == rank are written. */
+int sw_align_noise_owned(sw_ctx* ctx, const sw_choice* d_choices, const sw_request* d_reqs,
+                         int32_t B, int32_t rank, const float* d_eps, uint64_t philox_seed,
+                         float* d_out, int32_t t_out_max, void* stream);
+
+/* ---------------------------------------------------------------- component entry points
+ * score_candidates + select (selector.cpp:24-85) on one explicit candidate set, evaluated by
+ * the same device code the batched path uses. Outputs n x {s_pos,s_neg,a,b,q} and the pick. */
+int sw_score_select_host(sw_ctx* ctx, int32_t n, const double* sims, const double* s_neg,
+                         const double* durations, double L, const sw_selector_config* sel,
+                         uint64_t rng_seed, double* scores_out, int32_t* pick);
+/* context_features + choose_arm (gater.cpp:13-92) for B (prompt, segment) pairs. */
+int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const int32_t* T,
+                  int32_t B, int32_t explore, double* phi_out, int32_t* arm_out);
+/* Launch statistics of the last sw_plan/sw_search on this context (kernels launched, mode). */
+int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
+                        int32_t* candidates_max);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEMWARM_B200_H */

@@ -1,0 +1,372 @@
+"""TEST INFRASTRUCTURE ONLY — CPU checkers for the warm-start path.
+
+Two checkers live here:
+
+* ``Ref``    — the UNMODIFIED reference (``/root/reference/proj/src``) compiled in place by
+               ``oracle/Makefile`` into ``oracle/_ref/libsemwarm_ref.so`` (+ ``ref_harness.cpp``).
+* ``Oracle`` — our plain-C restatement (``oracle/semwarm_oracle.c``), pinned against ``Ref`` and
+               the committed golden vectors in ``tests/golden``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu-baseline / reference legs
+may import this package. The product path (``paper_2603_07865_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libsemwarm_ref.so")
+ORACLE_SO = os.path.join(HERE, "_build", "libsemwarm_oracle.so")
+
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+
+# RefPlanOut / so_plan (identical layouts)
+PLAN_DTYPE = np.dtype(
+    [("hit", "<i4"), ("arm", "<i4"), ("steps_skipped", "<i4"), ("n_hits", "<i4"),
+     ("entry_id", "<u8"), ("level", "<i4"), ("pick", "<i4"), ("start_s", "<f8"),
+     ("length_s", "<f8"), ("similarity", "<f8")])
+HIT_DTYPE = np.dtype(
+    [("entry_id", "<u8"), ("level", "<i4"), ("row", "<i4"), ("start_s", "<f8"),
+     ("length_s", "<f8"), ("similarity", "<f8")])
+
+POLICY = {"exploit": 0, "explore": 1, "rule": 2, "fixed": 3}
+
+
+def build(force: bool = False) -> None:
+    """Compile both checkers (needs /root/reference for the ``ref`` target)."""
+    import subprocess
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj/src"):
+        targets.append("ref")
+    subprocess.check_call(["make", "-s", "-C", HERE] + (["-B"] if force else []) + targets)
+
+
+def _load(path: str) -> C.CDLL:
+    if not os.path.exists(path):
+        raise RuntimeError(f"oracle library missing: {path} (run `make -C oracle`)")
+    return C.CDLL(path)
+
+
+class Arena:
+    """Flat cache view shared by both checkers: entry e owns rows [off[e], off[e+1])."""
+
+    def __init__(self, ids, off, rows, levels, starts, lengths):
+        self.ids = np.ascontiguousarray(ids, np.uint64)
+        self.off = np.ascontiguousarray(off, np.int64)
+        self.rows = np.ascontiguousarray(rows, np.float32)
+        self.levels = np.ascontiguousarray(levels, np.int32)
+        self.starts = np.ascontiguousarray(starts, np.float64)
+        self.lengths = np.ascontiguousarray(lengths, np.float64)
+        self.dim = int(self.rows.shape[1])
+        self.n_entries = int(self.ids.shape[0])
+
+
+class _SoArena(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_entries", C.c_int), ("ids", C.c_void_p),
+                ("off", C.c_void_p), ("rows", C.c_void_p), ("levels", C.c_void_p),
+                ("starts", C.c_void_p), ("lengths", C.c_void_p)]
+
+
+class Oracle:
+    """ctypes view of oracle/semwarm_oracle.c."""
+
+    def __init__(self):
+        L = self.lib = _load(ORACLE_SO)
+        L.so_derive_seed.restype = C.c_uint64
+        L.so_derive_seed.argtypes = [C.c_uint64] * 4
+        L.so_mt64_first.restype = C.c_uint64
+        L.so_mt64_first.argtypes = [C.c_uint64]
+        L.so_uniform_first.restype = C.c_double
+        L.so_uniform_first.argtypes = [C.c_uint64]
+        L.so_cosine.restype = C.c_double
+        L.so_cosine.argtypes = [f32p, f32p, C.c_int]
+        L.so_search.restype = C.c_int
+        L.so_plan_batch.restype = C.c_int
+        L.so_align_noise.restype = C.c_int
+        L.so_align_noise.argtypes = [f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                     C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_uint64,
+                                     C.c_uint64, f32p]
+        L.so_philox_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, f32p]
+        L.so_abar_table.argtypes = [f64p]
+        L.so_abar_index.restype = C.c_int
+        L.so_abar_index.argtypes = [C.c_int, C.c_int]
+        L.so_context_features.argtypes = [f32p, f32p, C.c_int, C.c_int, f64p]
+        L.so_choose_arm.restype = C.c_int
+        L.so_choose_arm.argtypes = [f32p, f32p, C.c_int, C.c_double, f64p, C.c_int]
+        L.so_score_select.restype = C.c_int
+        L.so_score_select.argtypes = [C.c_int, f64p, f64p, f32p, C.c_int, f32p, C.c_double,
+                                      C.c_double, C.c_double, C.c_uint64, f64p, f64p, f64p,
+                                      f64p, f64p]
+
+    def _arena(self, ar: Arena) -> _SoArena:
+        return _SoArena(ar.dim, ar.n_entries, ar.ids.ctypes.data, ar.off.ctypes.data,
+                        ar.rows.ctypes.data, ar.levels.ctypes.data, ar.starts.ctypes.data,
+                        ar.lengths.ctypes.data)
+
+    def derive_seed(self, base, a, b=0, c=0) -> int:
+        return self.lib.so_derive_seed(base, a, b, c)
+
+    def mt64_first(self, seed) -> int:
+        return self.lib.so_mt64_first(seed)
+
+    def uniform_first(self, seed) -> float:
+        return self.lib.so_uniform_first(seed)
+
+    def search(self, ar: Arena, q: np.ndarray, k: int) -> np.ndarray:
+        out = np.zeros(k, HIT_DTYPE)
+        sa = self._arena(ar)
+        q = np.ascontiguousarray(q, np.float32)
+        n = self.lib.so_search(C.byref(sa), q.ctypes.data_as(C.c_void_p), C.c_int(k),
+                               out.ctypes.data_as(C.c_void_p))
+        return out[:n]
+
+    def plan_batch(self, ar: Arena, neg, queries, L, req_ids, T, *, seed=1, top_k=8, temp=0.05,
+                   thr=0.6, policy="exploit", theta=None, psi=None, beta=1.0, rule_thr=0.35,
+                   rule_arm=11, fixed_arm=0, nthreads=1):
+        B = queries.shape[0]
+        out = np.zeros(B, PLAN_DTYPE)
+        hits = np.zeros(B * top_k, HIT_DTYPE)
+        theta = np.zeros(14 * 11, np.float32) if theta is None else np.ascontiguousarray(theta, np.float32)
+        psi = np.zeros(14 * 11, np.float32) if psi is None else np.ascontiguousarray(psi, np.float32)
+        sa = self._arena(ar)
+        queries = np.ascontiguousarray(queries, np.float32)
+        neg = np.ascontiguousarray(neg, np.float32)
+        L = np.ascontiguousarray(L, np.float64)
+        req_ids = np.ascontiguousarray(req_ids, np.uint64)
+        T = np.ascontiguousarray(T, np.int32)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        rc = self.lib.so_plan_batch(
+            C.byref(sa), vp(neg), C.c_int(B), vp(queries), vp(L), vp(req_ids), vp(T),
+            C.c_uint64(seed), C.c_int(top_k), C.c_double(temp), C.c_double(thr),
+            C.c_int(POLICY[policy]), vp(theta), vp(psi), C.c_int(11), C.c_double(beta),
+            C.c_double(rule_thr), C.c_int(rule_arm), C.c_int(fixed_arm), C.c_int(nthreads),
+            vp(out), vp(hits))
+        if rc != 0:
+            raise ValueError("so_plan_batch failed")
+        return out, hits.reshape(B, top_k)
+
+    def align_noise(self, latent, start_s, length_s, L, fps, abar, eps=None, seed=0, rid=0):
+        latent = np.ascontiguousarray(latent, np.float32)
+        C_, t_src, F = latent.shape
+        t_out = int(np.round(L * fps)) + 2
+        out = np.zeros(C_ * t_out * F, np.float32)
+        ep = None
+        if eps is not None:
+            eps = np.ascontiguousarray(eps, np.float32)
+            ep = eps.ctypes.data
+        n = self.lib.so_align_noise(latent, C_, t_src, F, start_s, length_s, L, fps, abar, ep,
+                                    seed, rid, out)
+        return out[: C_ * n * F].reshape(C_, n, F)
+
+    def philox_normals(self, seed, rid, n):
+        out = np.zeros(n, np.float32)
+        self.lib.so_philox_normals(seed, rid, n, out)
+        return out
+
+    def abar_table(self):
+        t = np.zeros(1001, np.float64)
+        self.lib.so_abar_table(t)
+        return t
+
+    def abar_index(self, T, S):
+        return self.lib.so_abar_index(T, S)
+
+    def context_features(self, p, c, T):
+        phi = np.zeros(11, np.float64)
+        p = np.ascontiguousarray(p, np.float32)
+        c = np.ascontiguousarray(c, np.float32)
+        self.lib.so_context_features(p, c, p.shape[0], T, phi)
+        return phi
+
+    def choose_arm(self, theta, psi, beta, phi, explore=False):
+        return self.lib.so_choose_arm(np.ascontiguousarray(theta, np.float32),
+                                      np.ascontiguousarray(psi, np.float32), 11, beta,
+                                      np.ascontiguousarray(phi, np.float64), int(explore))
+
+
+class Ref:
+    """ctypes view of the compiled reference (oracle/_ref/libsemwarm_ref.so)."""
+
+    def __init__(self):
+        L = self.lib = _load(REF_SO)
+        L.ref_derive_seed.restype = C.c_uint64
+        L.ref_derive_seed.argtypes = [C.c_uint64] * 4
+        L.ref_rng_first_u64.restype = C.c_uint64
+        L.ref_rng_first_u64.argtypes = [C.c_uint64]
+        L.ref_rng_first_uniform.restype = C.c_double
+        L.ref_rng_first_uniform.argtypes = [C.c_uint64]
+        L.ref_cosine.restype = C.c_double
+        L.ref_cosine.argtypes = [f32p, f32p, C.c_int]
+        L.ref_random_unit_vector.argtypes = [C.c_uint64, C.c_int, f32p]
+        L.ref_random_unit_vectors.argtypes = [C.c_uint64, C.c_int, C.c_int, f32p]
+        L.ref_perturb.argtypes = [f32p, C.c_int, C.c_double, C.c_uint64, f32p]
+        L.ref_make_negative.argtypes = [C.c_int, f32p]
+        L.ref_pyramid_segments.restype = C.c_int
+        L.ref_pyramid_segments.argtypes = [C.c_double, C.c_double, i32p, f64p, f64p, C.c_int]
+        L.ref_build_entry_vectors.restype = C.c_int
+        L.ref_build_entry_vectors.argtypes = [C.c_uint64, f32p, C.c_int, C.c_double, C.c_double,
+                                              C.c_uint64, f32p, i32p, f64p, f64p, C.c_int]
+        L.ref_index_new.restype = C.c_void_p
+        L.ref_index_new.argtypes = [C.c_int]
+        L.ref_index_free.argtypes = [C.c_void_p]
+        L.ref_index_insert_many.restype = C.c_int
+        L.ref_index_insert_many.argtypes = [C.c_void_p, C.c_int, u64p, i64p, f32p, i32p, f64p, f64p]
+        L.ref_index_remove.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_index_search.restype = C.c_int
+        L.ref_index_search.argtypes = [C.c_void_p, f32p, C.c_int, u64p, i32p, f64p, f64p, f64p]
+        L.ref_plan_batch.restype = C.c_int
+        L.ref_context_features.argtypes = [f32p, f32p, C.c_int, C.c_int, f64p]
+        L.ref_choose_arm.restype = C.c_int
+        L.ref_choose_arm.argtypes = [f32p, f32p, C.c_int, C.c_double, f64p, C.c_int]
+        L.ref_score_select.restype = C.c_int
+        L.ref_score_select.argtypes = [C.c_int, u64p, i32p, f64p, f64p, f64p, f32p, C.c_int,
+                                       f32p, f32p, C.c_double, C.c_int, C.c_double, C.c_double,
+                                       C.c_uint64, f64p, f64p, f64p, f64p, f64p]
+        L.ref_expected_quality.restype = C.c_double
+        L.ref_expected_quality.argtypes = [C.c_double, C.c_double]
+        L.ref_arm_skip_fraction.restype = C.c_double
+        L.ref_arm_skip_fraction.argtypes = [C.c_int]
+        # cache manager
+        L.ref_cache_new.restype = C.c_void_p
+        L.ref_cache_new.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double,
+                                    C.c_uint64]
+        L.ref_cache_free.argtypes = [C.c_void_p]
+        L.ref_cache_admit.restype = C.c_int64
+        L.ref_cache_admit.argtypes = [C.c_void_p, f32p, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.ref_cache_record_reuse.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_double,
+                                             C.c_double, C.c_double]
+        L.ref_cache_evict.restype = C.c_int
+        L.ref_cache_evict.argtypes = [C.c_void_p, C.c_double, u64p, C.c_int]
+        L.ref_cache_importance.restype = C.c_double
+        L.ref_cache_importance.argtypes = [C.c_void_p, C.c_uint64, C.c_double]
+        L.ref_cache_size.restype = C.c_int
+        L.ref_cache_size.argtypes = [C.c_void_p]
+        L.ref_cache_ids.restype = C.c_int
+        L.ref_cache_ids.argtypes = [C.c_void_p, u64p, C.c_int]
+        L.ref_cache_refinement_candidates.restype = C.c_int
+        L.ref_cache_refinement_candidates.argtypes = [C.c_void_p, u64p, C.c_int]
+        L.ref_cache_refine.restype = C.c_int
+        L.ref_cache_refine.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, f64p, f32p, C.c_int,
+                                       C.c_int, u64p]
+        L.ref_cache_search.restype = C.c_int
+        L.ref_cache_search.argtypes = [C.c_void_p, f32p, C.c_int, C.c_int, u64p, i32p, f64p,
+                                       f64p, f64p]
+        L.ref_cache_entry_rows.restype = C.c_int
+        L.ref_cache_entry_rows.argtypes = [C.c_void_p, C.c_uint64, f32p, C.c_int]
+
+    # -- helpers
+    def derive_seed(self, base, a, b=0, c=0):
+        return self.lib.ref_derive_seed(base, a, b, c)
+
+    def random_unit_vectors(self, seed, n, dim):
+        out = np.zeros((n, dim), np.float32)
+        self.lib.ref_random_unit_vectors(seed, n, dim, out)
+        return out
+
+    def perturb(self, v, scale, seed):
+        v = np.ascontiguousarray(v, np.float32)
+        out = np.zeros_like(v)
+        self.lib.ref_perturb(v, v.shape[0], scale, seed, out)
+        return out
+
+    def negative(self, dim):
+        out = np.zeros(dim, np.float32)
+        self.lib.ref_make_negative(dim, out)
+        return out
+
+    def pyramid(self, duration, delta):
+        lv = np.zeros(64, np.int32)
+        st = np.zeros(64, np.float64)
+        ln = np.zeros(64, np.float64)
+        n = self.lib.ref_pyramid_segments(duration, delta, lv, st, ln, 64)
+        return lv[:n], st[:n], ln[:n]
+
+    def build_entry_vectors(self, eid, full, duration, delta, seed_base):
+        full = np.ascontiguousarray(full, np.float32)
+        dim = full.shape[0]
+        rows = np.zeros((64, dim), np.float32)
+        lv = np.zeros(64, np.int32)
+        st = np.zeros(64, np.float64)
+        ln = np.zeros(64, np.float64)
+        n = self.lib.ref_build_entry_vectors(eid, full, dim, duration, delta, seed_base, rows,
+                                             lv, st, ln, 64)
+        return rows[:n].copy(), lv[:n].copy(), st[:n].copy(), ln[:n].copy()
+
+    # -- index
+    def index(self, ar: Arena):
+        return RefIndex(self, ar)
+
+    def context_features(self, p, c, T):
+        phi = np.zeros(11, np.float64)
+        p = np.ascontiguousarray(p, np.float32)
+        c = np.ascontiguousarray(c, np.float32)
+        self.lib.ref_context_features(p, c, p.shape[0], T, phi)
+        return phi
+
+    def choose_arm(self, theta, psi, beta, phi, explore=False):
+        return self.lib.ref_choose_arm(np.ascontiguousarray(theta, np.float32),
+                                       np.ascontiguousarray(psi, np.float32), 11, beta,
+                                       np.ascontiguousarray(phi, np.float64), int(explore))
+
+
+class RefIndex:
+    """Reference IvfIndex in exhaustive parity mode over an Arena (kept alive here)."""
+
+    def __init__(self, ref: Ref, ar: Arena):
+        self.ref, self.ar = ref, ar
+        self.h = ref.lib.ref_index_new(ar.dim)
+        rc = ref.lib.ref_index_insert_many(self.h, ar.n_entries, ar.ids, ar.off, ar.rows,
+                                           ar.levels, ar.starts, ar.lengths)
+        if rc != 0:
+            raise RuntimeError("reference insert failed")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_index_free(self.h)
+            self.h = None
+
+    def remove(self, eid):
+        self.ref.lib.ref_index_remove(self.h, eid)
+
+    def search(self, q, k):
+        ids = np.zeros(k, np.uint64)
+        lv = np.zeros(k, np.int32)
+        st = np.zeros(k, np.float64)
+        ln = np.zeros(k, np.float64)
+        sm = np.zeros(k, np.float64)
+        n = self.ref.lib.ref_index_search(self.h, np.ascontiguousarray(q, np.float32), k, ids, lv,
+                                          st, ln, sm)
+        return ids[:n], lv[:n], st[:n], ln[:n], sm[:n]
+
+    def plan_batch(self, neg, queries, L, req_ids, T, *, seed=1, top_k=8, temp=0.05, thr=0.6,
+                   policy="exploit", theta=None, psi=None, beta=1.0, rule_thr=0.35,
+                   rule_skip=0.55, fixed_arm=0, nthreads=1):
+        B = queries.shape[0]
+        out = np.zeros(B, PLAN_DTYPE)
+        hit_ids = np.zeros(B * top_k, np.uint64)
+        hit_sims = np.zeros(B * top_k, np.float64)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        queries = np.ascontiguousarray(queries, np.float32)
+        neg = np.ascontiguousarray(neg, np.float32)
+        L = np.ascontiguousarray(L, np.float64)
+        req_ids = np.ascontiguousarray(req_ids, np.uint64)
+        T = np.ascontiguousarray(T, np.int32)
+        theta = None if theta is None else np.ascontiguousarray(theta, np.float32)
+        psi = None if psi is None else np.ascontiguousarray(psi, np.float32)
+        rc = self.ref.lib.ref_plan_batch(
+            C.c_void_p(self.h), vp(neg), C.c_int(B), vp(queries), vp(L), vp(req_ids), vp(T),
+            C.c_uint64(seed), C.c_int(top_k), C.c_double(temp), C.c_double(thr),
+            C.c_int(POLICY[policy]), None if theta is None else vp(theta),
+            None if psi is None else vp(psi), C.c_int(11), C.c_double(beta),
+            C.c_double(rule_thr), C.c_double(rule_skip), C.c_int(fixed_arm), C.c_int(nthreads),
+            vp(out), vp(hit_ids), vp(hit_sims))
+        if rc != 0:
+            raise RuntimeError("ref_plan_batch failed")
+        return out, hit_ids.reshape(B, top_k), hit_sims.reshape(B, top_k)

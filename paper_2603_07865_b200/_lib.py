@@ -1,0 +1,154 @@
+"""ctypes binding of the C-ABI in include/semwarm_b200.h (libsemwarm_b200.so, built in-tree).
+
+There is no fallback: if the shared library is missing or fails to load, every entry point
+raises. The structures below mirror the header field-for-field.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsemwarm_b200.so")
+
+SW_OK = 0
+SW_EINVAL = -1
+SW_ERUNTIME = -2
+SW_ECUDA = -3
+SW_ENOMEM = -4
+SW_WARN_UNKNOWN_ID = 1
+
+SW_FLAG_EXACT_ONLY = 0x1
+SW_FLAG_TC_ALWAYS = 0x2
+
+SW_CHOICE_AMBIGUOUS_DRAW = 0x1
+SW_CHOICE_NONFINITE_PHI = 0x2
+SW_CHOICE_INCOMPLETE = 0x4
+SW_CHOICE_AMBIGUOUS_ARM = 0x8
+
+POLICY = {"exploit": 0, "explore": 1, "rule": 2, "fixed": 3}
+HIT_RECORD_BYTES = 128
+
+
+class SwConfig(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("rows_per_entry", C.c_int32), ("max_entries", C.c_int64),
+                ("latent_c", C.c_int32), ("latent_t_max", C.c_int32), ("latent_f", C.c_int32),
+                ("max_batch", C.c_int32), ("latent_slots", C.c_int64), ("latent_fps", C.c_double),
+                ("flags", C.c_uint32), ("reserved", C.c_int32)]
+
+
+class SwSelectorConfig(C.Structure):
+    _fields_ = [("top_k", C.c_int32), ("reserved", C.c_int32), ("temperature", C.c_double),
+                ("quality_threshold", C.c_double)]
+
+
+class SwPolicy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("fixed_arm", C.c_int32),
+                ("rule_similarity_threshold", C.c_double), ("rule_skip_fraction", C.c_double)]
+
+
+# numpy mirrors of the array-of-struct types
+SEGMENT_DTYPE = np.dtype([("level", "<i4"), ("reserved", "<i4"), ("start_s", "<f8"),
+                          ("length_s", "<f8")])
+HIT_DTYPE = np.dtype([("entry_id", "<u8"), ("level", "<i4"), ("reserved", "<i4"),
+                      ("start_s", "<f8"), ("length_s", "<f8"), ("similarity", "<f8")])
+REQUEST_DTYPE = np.dtype([("id", "<u8"), ("duration_s", "<f8"), ("total_steps", "<i4"),
+                          ("reserved", "<i4")])
+CHOICE_DTYPE = np.dtype([("hit", "<i4"), ("arm", "<i4"), ("steps_skipped", "<i4"),
+                         ("n_hits", "<i4"), ("entry_id", "<u8"), ("level", "<i4"),
+                         ("seg_reserved", "<i4"), ("start_s", "<f8"), ("length_s", "<f8"),
+                         ("similarity", "<f8"), ("skip_fraction", "<f8"), ("pick", "<i4"),
+                         ("flags", "<u4"), ("t_out", "<i4"), ("owner", "<i4"), ("slot", "<i8")])
+assert SEGMENT_DTYPE.itemsize == 24 and HIT_DTYPE.itemsize == 40
+assert REQUEST_DTYPE.itemsize == 24 and CHOICE_DTYPE.itemsize == 88
+
+_lib = None
+
+
+class SemwarmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def lib() -> C.CDLL:
+    """Load libsemwarm_b200.so (raises if it was not built — there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} not found: the CUDA extension is not built (run __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+    sig = {
+        "sw_version": ([], C.c_int),
+        "sw_last_error": ([], C.c_char_p),
+        "sw_ctx_create": ([C.POINTER(SwConfig), C.c_int, C.POINTER(vp)], C.c_int),
+        "sw_ctx_destroy": ([vp], C.c_int),
+        "sw_set_negative": ([vp, vp], C.c_int),
+        "sw_set_gater": ([vp, vp, vp, i32, f64], C.c_int),
+        "sw_set_schedule": ([vp, vp, i32], C.c_int),
+        "sw_arena_insert": ([vp, u64, i32, vp, vp, vp, i32], C.c_int),
+        "sw_arena_insert_batch": ([vp, i64, vp, vp, vp, vp, vp, vp, vp, i32], C.c_int),
+        "sw_arena_remove": ([vp, u64], C.c_int),
+        "sw_arena_replace": ([vp, u64, i32, vp, vp, vp, i32], C.c_int),
+        "sw_arena_entry_count": ([vp], i64),
+        "sw_arena_contains": ([vp, u64], C.c_int),
+        "sw_arena_fill_synthetic": ([vp, i64, u64, u64, f64], C.c_int),
+        "sw_arena_read_rows": ([vp, u64, vp, i32], C.c_int),
+        "sw_search": ([vp, vp, i32, i32, vp, vp, vp], C.c_int),
+        "sw_search_host": ([vp, vp, i32, i32, vp, vp], C.c_int),
+        "sw_plan": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy),
+                     vp, vp], C.c_int),
+        "sw_align_noise": ([vp, vp, vp, i32, vp, u64, vp, i32, vp], C.c_int),
+        "sw_warmstart": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
+                          C.POINTER(SwPolicy), vp, u64, vp, vp, i32, vp], C.c_int),
+        "sw_warmstart_host": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
+                               C.POINTER(SwPolicy), u64, vp, vp, i32, vp], C.c_int),
+        "sw_local_topk": ([vp, vp, i32, i32, i32, vp, vp, vp], C.c_int),
+        "sw_merge_select": ([vp, vp, vp, i32, vp, vp, i32, i32, u64,
+                             C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy), vp, vp], C.c_int),
+        "sw_align_noise_owned": ([vp, vp, vp, i32, i32, vp, u64, vp, i32, vp], C.c_int),
+        "sw_score_select_host": ([vp, i32, vp, vp, vp, f64, C.POINTER(SwSelectorConfig), u64,
+                                  vp, vp], C.c_int),
+        "sw_gater_host": ([vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
+        "sw_last_launch_info": ([vp, vp, vp, vp], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = [
+    "sw_version", "sw_last_error", "sw_ctx_create", "sw_ctx_destroy", "sw_set_negative",
+    "sw_set_gater", "sw_set_schedule", "sw_arena_insert", "sw_arena_insert_batch",
+    "sw_arena_remove", "sw_arena_replace", "sw_arena_entry_count", "sw_arena_contains",
+    "sw_arena_fill_synthetic", "sw_arena_read_rows", "sw_search", "sw_search_host", "sw_plan",
+    "sw_align_noise", "sw_warmstart", "sw_warmstart_host", "sw_local_topk", "sw_merge_select",
+    "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
+]
+
+
+def check(rc: int, what: str = "") -> int:
+    if rc < 0:
+        msg = lib().sw_last_error().decode(errors="replace")
+        if rc == SW_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        raise SemwarmError(rc, f"{what}: {msg}")
+    return rc
+
+
+def ptr(a) -> int:
+    """Raw pointer of a numpy array or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    return a.data_ptr()  # torch.Tensor

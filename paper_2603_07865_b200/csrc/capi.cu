@@ -1,0 +1,768 @@
+// The C-ABI (include/semwarm_b200.h): context lifetime, arena mutations (synchronous, exclusive)
+// and the stream-ordered batched hot path. No exception crosses this boundary.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "sw_internal.cuh"
+
+struct sw_ctx {
+    sw::Ctx c;
+};
+
+namespace sw {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return SW_ENOMEM;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SW_ERUNTIME;
+    }
+}
+
+static int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <class T>
+static void dalloc(T** p, size_t n) {
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(SW_ENOMEM, std::string("cudaMalloc of ") + std::to_string(sizeof(T) * n) +
+                                   " bytes failed: " + cudaGetErrorString(e));
+    }
+}
+
+static void default_schedule(std::vector<double>& abar) {
+    // scaled-linear DDPM betas 0.00085..0.012 over 1000 steps (the LDM/AudioLDM default)
+    abar.assign(1001, 1.0);
+    const double b0 = std::sqrt(0.00085), b1 = std::sqrt(0.012);
+    for (int t = 1; t <= 1000; ++t) {
+        double s = b0 + (b1 - b0) * (double)(t - 1) / 999.0;
+        abar[t] = abar[t - 1] * (1.0 - s * s);
+    }
+}
+
+static void free_ctx(Ctx& c) {
+    void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.tsrc,
+                    c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
+                    c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
+                    c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c.h_pinned) cudaFreeHost(c.h_pinned);
+    if (c.mstream) cudaStreamDestroy(c.mstream);
+}
+
+static void create(Ctx& c, const sw_config& cfg, int device) {
+    SW_REQUIRE(cfg.dim >= 1, "dim must be >= 1");
+    SW_REQUIRE(cfg.rows_per_entry >= 1 && cfg.rows_per_entry <= kMaxRowsPad,
+               "rows_per_entry must be in [1, 32]");
+    SW_REQUIRE(cfg.max_entries >= 1, "cache capacity must be >= 1");  // cache.cpp:16
+    SW_REQUIRE(cfg.max_batch >= 1, "max_batch must be >= 1");
+    c.cfg = cfg;
+    if (c.cfg.latent_fps <= 0.0) c.cfg.latent_fps = 25.0;
+    c.device = device;
+    SW_CUDA(cudaSetDevice(device));
+    c.D = cfg.dim;
+    c.Dp = (cfg.dim + 63) / 64 * 64;
+    c.Df = (cfg.dim + 3) / 4 * 4;
+    c.R = cfg.rows_per_entry;
+    c.Rp = next_pow2(cfg.rows_per_entry);
+    c.logRp = 0;
+    while ((1 << c.logRp) < c.Rp) ++c.logRp;
+    // round capacity up to whole 256-row tiles so TMA boxes never straddle the allocation
+    const int64_t per_tile = std::max(1, 256 / c.Rp);
+    c.S = (cfg.max_entries + per_tile - 1) / per_tile * per_tile;
+    c.C = cfg.latent_c;
+    c.Tmax = cfg.latent_t_max;
+    c.F = cfg.latent_f;
+    c.Lslots = cfg.latent_slots > 0 ? std::min<int64_t>(cfg.latent_slots, c.S) : c.S;
+    c.Bmax = cfg.max_batch;
+    c.BmaxPad = (cfg.max_batch + 127) / 128 * 128;
+    const int64_t nrow = c.S * c.Rp;
+    dalloc(&c.rows, (size_t)nrow * c.Df);
+    dalloc(&c.rows_bf, (size_t)nrow * c.Dp);
+    dalloc(&c.sneg, (size_t)nrow);
+    dalloc(&c.segs, (size_t)nrow);
+    dalloc(&c.ids, (size_t)c.S);
+    dalloc(&c.nrows, (size_t)c.S);
+    dalloc(&c.valid, (size_t)c.S);
+    dalloc(&c.tsrc, (size_t)c.S);
+    if (c.C > 0 && c.Tmax > 0 && c.F > 0)
+        dalloc(&c.latent, (size_t)c.Lslots * c.C * c.Tmax * c.F);
+    dalloc(&c.maxnorm, 1);
+    dalloc(&c.neg, (size_t)c.Df);
+    dalloc(&c.theta, kNumArms * kFeatureDim);
+    dalloc(&c.psi, kNumArms * kFeatureDim);
+    dalloc(&c.q_bf, (size_t)c.BmaxPad * c.Dp);
+    dalloc(&c.q_norm, (size_t)c.Bmax);
+    dalloc(&c.thr, (size_t)c.Bmax);
+    dalloc(&c.cand_n, (size_t)3 * c.Bmax);
+    dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
+    dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);
+    dalloc(&c.cand_exact, (size_t)c.Bmax * kCandCap);
+    dalloc(&c.cand_row, (size_t)c.Bmax * kCandCap);
+    dalloc(&c.cand_list, (size_t)c.Bmax * kCandCap);
+    dalloc(&c.hits, (size_t)c.Bmax * kMaxTopK);
+    dalloc(&c.nhits, (size_t)c.Bmax);
+    dalloc(&c.d_q_stage, (size_t)c.Bmax * c.D);
+    dalloc(&c.d_req_stage, (size_t)c.Bmax);
+    dalloc(&c.d_choice_stage, (size_t)c.Bmax);
+    SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
+    SW_CUDA(cudaMemsetAsync(c.valid, 0, (size_t)c.S, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.nrows, 0, sizeof(int32_t) * (size_t)c.S, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.tsrc, 0, sizeof(int32_t) * (size_t)c.S, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.rows_bf, 0, sizeof(__nv_bfloat16) * (size_t)nrow * c.Dp, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.q_bf, 0, sizeof(__nv_bfloat16) * (size_t)c.BmaxPad * c.Dp, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.neg, 0, sizeof(float) * c.Df, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.theta, 0, sizeof(float) * kNumArms * kFeatureDim, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.psi, 0, sizeof(float) * kNumArms * kFeatureDim, c.mstream));
+    const uint32_t zero_norm = f2ord(0.0f);
+    SW_CUDA(cudaMemcpyAsync(c.maxnorm, &zero_norm, 4, cudaMemcpyHostToDevice, c.mstream));
+    std::vector<double> ab;
+    default_schedule(ab);
+    dalloc(&c.abar, ab.size());
+    c.n_abar = (int)ab.size();
+    SW_CUDA(cudaMemcpyAsync(c.abar, ab.data(), sizeof(double) * ab.size(), cudaMemcpyHostToDevice,
+                            c.mstream));
+    c.h_pinned_bytes = (size_t)c.Bmax * (sizeof(float) * c.D + sizeof(sw_request) + sizeof(sw_choice));
+    SW_CUDA(cudaMallocHost(&c.h_pinned, c.h_pinned_bytes));
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+    c.h_nrows.assign((size_t)c.S, 0);
+    int major = 0, minor = 0;
+    SW_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    SW_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    SW_CUDA(cudaDeviceGetAttribute(&c.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    c.tc_ok = major == 10 && minor == 0 && encode_tensor_maps(c);
+}
+
+// Reserve slots for n new entries (lowest free slot first) and update host bookkeeping.
+static int64_t take_slot(Ctx& c) {
+    if (!c.free_slots.empty()) {
+        int64_t s = *c.free_slots.begin();
+        c.free_slots.erase(c.free_slots.begin());
+        return s;
+    }
+    if (c.high_water >= c.S) throw Error(SW_ENOMEM, "arena full (max_entries reached)");
+    return c.high_water++;
+}
+
+struct InsertPlan {
+    std::vector<int64_t> slot;
+    std::vector<int32_t> base;
+};
+
+// Stage host inputs and run the insert kernels on the mutation stream (synchronously).
+static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row_off,
+                      const float* rows, const sw_segment* segs, const float* latents,
+                      const int64_t* lat_off, const int32_t* t_src, bool on_device) {
+    InsertPlan pl;
+    pl.slot.resize((size_t)n);
+    pl.base.resize((size_t)n);
+    std::vector<uint64_t> h_ids((size_t)n);
+    std::vector<int64_t> h_off((size_t)n + 1);
+    if (on_device) {
+        SW_CUDA(cudaMemcpy(h_ids.data(), ids, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+        SW_CUDA(cudaMemcpy(h_off.data(), row_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    } else {
+        std::memcpy(h_ids.data(), ids, sizeof(uint64_t) * n);
+        std::memcpy(h_off.data(), row_off, sizeof(int64_t) * (n + 1));
+    }
+    // validate everything before mutating any state
+    std::unordered_map<uint64_t, int32_t> pending;
+    for (int64_t e = 0; e < n; ++e) {
+        const int64_t nr = h_off[e + 1] - h_off[e];
+        SW_REQUIRE(nr >= 0, "row offsets must be non-decreasing");
+        auto it = c.slot_of.find(h_ids[e]);
+        int32_t have = it == c.slot_of.end() ? 0 : c.h_nrows[(size_t)it->second];
+        have += pending[h_ids[e]];
+        SW_REQUIRE(have + nr <= c.Rp && have + nr <= kMaxRowsPad,
+                   "entry has more rows than the arena's rows_per_entry");
+        pending[h_ids[e]] += (int32_t)nr;
+    }
+    for (int64_t e = 0; e < n; ++e) {
+        const int64_t nr = h_off[e + 1] - h_off[e];
+        auto it = c.slot_of.find(h_ids[e]);
+        if (it == c.slot_of.end()) {
+            const int64_t s = take_slot(c);
+            c.slot_of[h_ids[e]] = s;
+            pl.slot[e] = s;
+            pl.base[e] = 0;
+        } else {
+            pl.slot[e] = it->second;
+            pl.base[e] = c.h_nrows[(size_t)it->second];
+        }
+        c.h_nrows[(size_t)pl.slot[e]] = pl.base[e] + (int32_t)nr;
+    }
+    cudaStream_t st = c.mstream;
+    const int64_t total_rows = h_off[n] - h_off[0];
+    int64_t *d_slot = nullptr, *d_off = nullptr, *d_latoff = nullptr;
+    int32_t *d_base = nullptr, *d_tsrc = nullptr;
+    uint64_t* d_ids = nullptr;
+    float *d_rows = nullptr, *d_lat = nullptr;
+    sw_segment* d_segs = nullptr;
+    dalloc(&d_slot, (size_t)n);
+    dalloc(&d_base, (size_t)n);
+    SW_CUDA(cudaMemcpyAsync(d_slot, pl.slot.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+    SW_CUDA(cudaMemcpyAsync(d_base, pl.base.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    if (on_device) {
+        d_ids = const_cast<uint64_t*>(ids);
+        d_off = const_cast<int64_t*>(row_off);
+        d_rows = const_cast<float*>(rows);
+        d_segs = const_cast<sw_segment*>(segs);
+    } else {
+        dalloc(&d_ids, (size_t)n);
+        dalloc(&d_off, (size_t)n + 1);
+        dalloc(&d_rows, (size_t)std::max<int64_t>(1, h_off[n]) * c.D);
+        dalloc(&d_segs, (size_t)std::max<int64_t>(1, h_off[n]));
+        SW_CUDA(cudaMemcpyAsync(d_ids, ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_off, row_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+        if (total_rows > 0) {
+            SW_CUDA(cudaMemcpyAsync(d_rows, rows, sizeof(float) * h_off[n] * c.D,
+                                    cudaMemcpyHostToDevice, st));
+            SW_CUDA(cudaMemcpyAsync(d_segs, segs, sizeof(sw_segment) * h_off[n],
+                                    cudaMemcpyHostToDevice, st));
+        }
+    }
+    launch_insert_rows_full(c, n, d_slot, d_base, d_off, d_ids, d_rows, d_segs, st);
+    if (latents && c.latent) {
+        if (on_device) {
+            d_lat = const_cast<float*>(latents);
+            d_latoff = const_cast<int64_t*>(lat_off);
+            d_tsrc = const_cast<int32_t*>(t_src);
+        } else {
+            int64_t tot = 0;
+            for (int64_t e = 0; e < n; ++e)
+                tot = std::max<int64_t>(tot, lat_off[e] + (int64_t)c.C * t_src[e] * c.F);
+            dalloc(&d_lat, (size_t)std::max<int64_t>(tot, 1));
+            dalloc(&d_latoff, (size_t)n);
+            dalloc(&d_tsrc, (size_t)n);
+            SW_CUDA(cudaMemcpyAsync(d_lat, latents, sizeof(float) * tot, cudaMemcpyHostToDevice, st));
+            SW_CUDA(cudaMemcpyAsync(d_latoff, lat_off, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+            SW_CUDA(cudaMemcpyAsync(d_tsrc, t_src, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        }
+        launch_copy_latents(c, n, d_slot, d_lat, d_latoff, d_tsrc, st);
+    }
+    SW_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_slot);
+    cudaFree(d_base);
+    if (!on_device) {
+        cudaFree(d_ids);
+        cudaFree(d_off);
+        cudaFree(d_rows);
+        cudaFree(d_segs);
+        if (latents && c.latent) {
+            cudaFree(d_lat);
+            cudaFree(d_latoff);
+            cudaFree(d_tsrc);
+        }
+    }
+}
+
+static void do_remove(Ctx& c, uint64_t id, bool* found) {
+    auto it = c.slot_of.find(id);
+    if (it == c.slot_of.end()) {
+        *found = false;
+        return;
+    }
+    *found = true;
+    const int64_t s = it->second;
+    c.slot_of.erase(it);
+    c.h_nrows[(size_t)s] = 0;
+    const uint8_t z = 0;
+    const int32_t zi = 0;
+    SW_CUDA(cudaMemcpyAsync(c.valid + s, &z, 1, cudaMemcpyHostToDevice, c.mstream));
+    SW_CUDA(cudaMemcpyAsync(c.nrows + s, &zi, 4, cudaMemcpyHostToDevice, c.mstream));
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+    if (s == c.high_water - 1) {
+        --c.high_water;
+        // trim trailing free slots so the scan range stays tight
+        while (c.high_water > 0 && c.free_slots.count(c.high_water - 1)) {
+            c.free_slots.erase(c.high_water - 1);
+            --c.high_water;
+        }
+    } else {
+        c.free_slots.insert(s);
+    }
+}
+
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace sw
+
+using namespace sw;
+
+extern "C" {
+
+int sw_version(void) { return 1; }
+
+const char* sw_last_error(void) { return g_last_error.c_str(); }
+
+int sw_ctx_create(const sw_config* cfg, int device, sw_ctx** out) {
+    return guarded([&] {
+        SW_REQUIRE(cfg && out, "null argument");
+        auto* h = new sw_ctx;
+        try {
+            create(h->c, *cfg, device);
+        } catch (...) {
+            free_ctx(h->c);
+            delete h;
+            throw;
+        }
+        *out = h;
+        return SW_OK;
+    });
+}
+
+int sw_ctx_destroy(sw_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return SW_OK;
+        cudaSetDevice(ctx->c.device);
+        cudaDeviceSynchronize();
+        free_ctx(ctx->c);
+        delete ctx;
+        return SW_OK;
+    });
+}
+
+int sw_set_negative(sw_ctx* ctx, const float* neg) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && neg, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        SW_CUDA(cudaMemcpyAsync(c.neg, neg, sizeof(float) * c.D, cudaMemcpyHostToDevice, c.mstream));
+        c.have_neg = true;
+        launch_recompute_sneg(c, c.mstream);
+        SW_CUDA(cudaStreamSynchronize(c.mstream));
+        return SW_OK;
+    });
+}
+
+int sw_set_gater(sw_ctx* ctx, const float* theta, const float* psi, int32_t fd, double beta) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && theta && psi, "null argument");
+        SW_REQUIRE(fd == kFeatureDim, "feature dim mismatch");  // gater.cpp:62
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        SW_CUDA(cudaMemcpyAsync(c.theta, theta, sizeof(float) * kNumArms * fd, cudaMemcpyHostToDevice, c.mstream));
+        SW_CUDA(cudaMemcpyAsync(c.psi, psi, sizeof(float) * kNumArms * fd, cudaMemcpyHostToDevice, c.mstream));
+        SW_CUDA(cudaStreamSynchronize(c.mstream));
+        c.beta = beta;
+        c.fd = fd;
+        return SW_OK;
+    });
+}
+
+int sw_set_schedule(sw_ctx* ctx, const double* abar, int32_t n) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && abar && n >= 2, "schedule needs >= 2 entries");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        if (n != c.n_abar) {
+            cudaFree(c.abar);
+            c.abar = nullptr;
+            dalloc(&c.abar, (size_t)n);
+            c.n_abar = n;
+        }
+        SW_CUDA(cudaMemcpy(c.abar, abar, sizeof(double) * n, cudaMemcpyHostToDevice));
+        return SW_OK;
+    });
+}
+
+int sw_arena_insert(sw_ctx* ctx, uint64_t id, int32_t n_rows, const float* rows,
+                    const sw_segment* segs, const float* latent, int32_t t_src) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (n_rows == 0 || (rows && segs)), "null argument");
+        SW_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
+        if (n_rows == 0) return SW_OK;  // IvfIndex::insert of nothing (index.cpp:227)
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        int64_t off[2] = {0, n_rows};
+        int64_t loff = 0;
+        do_insert(c, 1, &id, off, rows, segs, latent, &loff, &t_src, false);
+        return SW_OK;
+    });
+}
+
+int sw_arena_insert_batch(sw_ctx* ctx, int64_t n, const uint64_t* ids, const int64_t* row_off,
+                          const float* rows, const sw_segment* segs, const float* latents,
+                          const int64_t* lat_off, const int32_t* t_src, int32_t on_device) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && ids && row_off, "null argument");
+        if (n <= 0) return SW_OK;
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        do_insert(c, n, ids, row_off, rows, segs, latents, lat_off, t_src, on_device != 0);
+        return SW_OK;
+    });
+}
+
+int sw_arena_remove(sw_ctx* ctx, uint64_t id) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        bool found = false;
+        do_remove(c, id, &found);
+        if (!found) {
+            set_last_error("remove of unknown entry id " + std::to_string(id));
+            return SW_WARN_UNKNOWN_ID;
+        }
+        return SW_OK;
+    });
+}
+
+int sw_arena_replace(sw_ctx* ctx, uint64_t id, int32_t n_rows, const float* rows,
+                     const sw_segment* segs, const float* latent, int32_t t_src) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && rows && segs && n_rows >= 1, "bad argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        auto it = c.slot_of.find(id);
+        if (it == c.slot_of.end()) {
+            set_last_error("replace of unknown entry id " + std::to_string(id));
+            return SW_WARN_UNKNOWN_ID;
+        }
+        SW_REQUIRE(n_rows <= c.Rp, "entry has more rows than the arena's rows_per_entry");
+        // in place: same slot, rows rewritten from row 0 (CacheManager::refine, cache.cpp:129-139)
+        c.h_nrows[(size_t)it->second] = 0;
+        int64_t off[2] = {0, n_rows};
+        int64_t loff = 0;
+        do_insert(c, 1, &id, off, rows, segs, latent, &loff, &t_src, false);
+        return SW_OK;
+    });
+}
+
+int64_t sw_arena_entry_count(const sw_ctx* ctx) {
+    if (!ctx) return 0;
+    std::shared_lock lk(ctx->c.mu);
+    return (int64_t)ctx->c.slot_of.size();
+}
+
+int sw_arena_contains(const sw_ctx* ctx, uint64_t id) {
+    if (!ctx) return 0;
+    std::shared_lock lk(ctx->c.mu);
+    return ctx->c.slot_of.count(id) ? 1 : 0;
+}
+
+int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t seed, double delta) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && n >= 0, "bad argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        SW_REQUIRE(c.free_slots.empty(), "synthetic fill needs a compact arena");
+        SW_REQUIRE(c.high_water + n <= c.S, "arena full (max_entries reached)");
+        for (int64_t i = 0; i < n; ++i)
+            SW_REQUIRE(!c.slot_of.count(first_id + (uint64_t)i), "synthetic id collides");
+        const int64_t slot0 = c.high_water;
+        launch_fill_synthetic(c, slot0, n, first_id, seed, delta, c.mstream);
+        SW_CUDA(cudaStreamSynchronize(c.mstream));
+        for (int64_t i = 0; i < n; ++i) {
+            c.slot_of[first_id + (uint64_t)i] = slot0 + i;
+            c.h_nrows[(size_t)(slot0 + i)] = c.R;
+        }
+        c.high_water += n;
+        return SW_OK;
+    });
+}
+
+int sw_arena_read_rows(sw_ctx* ctx, uint64_t id, float* rows, int32_t cap) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && rows, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        auto it = c.slot_of.find(id);
+        if (it == c.slot_of.end()) return -1;
+        const int n = std::min(cap, c.h_nrows[(size_t)it->second]);
+        SW_CUDA(cudaMemcpy2D(rows, sizeof(float) * c.D, c.rows + it->second * c.Rp * c.Df,
+                             sizeof(float) * c.Df, sizeof(float) * c.D, n, cudaMemcpyDeviceToHost));
+        return n;
+    });
+}
+
+int sw_search(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, sw_hit* d_out, int32_t* d_n,
+              void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_out && d_n)), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t st = as_stream(stream);
+        int kn = launch_search(c, d_q, B, k, 0, st);
+        launch_hits_to_public(c, B, k, d_out, d_n, st);
+        c.last_kernels = kn + 1;
+        return SW_OK;
+    });
+}
+
+int sw_search_host(sw_ctx* ctx, const float* q, int32_t B, int32_t k, sw_hit* out, int32_t* n) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (q && out && n)), "null argument");
+        Ctx& c = ctx->c;
+        SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
+        SW_CUDA(cudaSetDevice(c.device));
+        sw_hit* d_out = nullptr;
+        int32_t* d_n = nullptr;
+        dalloc(&d_out, (size_t)std::max(1, B * k));
+        dalloc(&d_n, (size_t)std::max(1, B));
+        cudaStream_t st = nullptr;
+        SW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        int rc;
+        {
+            std::shared_lock lk(c.mu);
+            SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
+                                    cudaMemcpyHostToDevice, st));
+            int kn = launch_search(c, c.d_q_stage, B, k, 0, st);
+            launch_hits_to_public(c, B, k, d_out, d_n, st);
+            c.last_kernels = kn + 1;
+            SW_CUDA(cudaMemcpyAsync(out, d_out, sizeof(sw_hit) * (size_t)B * k, cudaMemcpyDeviceToHost, st));
+            SW_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+            SW_CUDA(cudaStreamSynchronize(st));
+            rc = SW_OK;
+        }
+        cudaStreamDestroy(st);
+        cudaFree(d_out);
+        cudaFree(d_n);
+        return rc;
+    });
+}
+
+static void check_sel(const sw_selector_config* sel, const sw_policy* pol) {
+    SW_REQUIRE(sel && pol, "null selector config or policy");
+    SW_REQUIRE(sel->top_k >= 1, "selector top_k must be >= 1");               // selector.cpp:9
+    SW_REQUIRE(sel->top_k <= kMaxTopK, "selector top_k above 32 is not supported");
+    SW_REQUIRE(sel->temperature > 0.0, "selector temperature must be > 0");   // selector.cpp:10
+    SW_REQUIRE(sel->quality_threshold >= 0.0 && sel->quality_threshold <= 1.0,
+               "selector quality threshold must be in [0, 1]");            // selector.cpp:11-13
+    SW_REQUIRE(pol->kind >= 0 && pol->kind <= 3, "unknown gater policy");
+    SW_REQUIRE(pol->kind != SW_POLICY_FIXED || (pol->fixed_arm >= 0 && pol->fixed_arm < kNumArms),
+               "arm index out of range");                                  // gater.hpp:17
+}
+
+static int plan_impl(Ctx& c, const float* d_q, const sw_request* d_req, int B, uint64_t seed,
+                     const sw_selector_config* sel, const sw_policy* pol, sw_choice* d_out,
+                     cudaStream_t st) {
+    check_sel(sel, pol);
+    int kn = launch_search(c, d_q, B, sel->top_k, 0, st);
+    launch_select(c, c.hits, c.nhits, kMaxTopK, d_q, d_req, B, seed, *sel, *pol, d_out, 0, st);
+    return kn + 1;
+}
+
+int sw_plan(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, uint64_t seed,
+            const sw_selector_config* sel, const sw_policy* pol, sw_choice* d_out, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_req && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        c.last_kernels = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_out, as_stream(stream));
+        return SW_OK;
+    });
+}
+
+int sw_align_noise(sw_ctx* ctx, const sw_choice* d_ch, const sw_request* d_req, int32_t B,
+                   const float* d_eps, uint64_t philox_seed, float* d_out, int32_t t_out_max,
+                   void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_ch && d_req && d_out)), "null argument");
+        SW_REQUIRE(t_out_max >= 1, "t_out_max must be >= 1");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max,
+                           as_stream(stream));
+        return SW_OK;
+    });
+}
+
+int sw_align_noise_owned(sw_ctx* ctx, const sw_choice* d_ch, const sw_request* d_req, int32_t B,
+                         int32_t rank, const float* d_eps, uint64_t philox_seed, float* d_out,
+                         int32_t t_out_max, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_ch && d_req && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        launch_align_noise(c, d_ch, d_req, B, rank, d_eps, philox_seed, d_out, t_out_max,
+                           as_stream(stream));
+        return SW_OK;
+    });
+}
+
+int sw_warmstart(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, uint64_t seed,
+                 const sw_selector_config* sel, const sw_policy* pol, const float* d_eps,
+                 uint64_t philox_seed, sw_choice* d_ch, float* d_out, int32_t t_out_max,
+                 void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_req && d_ch && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t st = as_stream(stream);
+        int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, st);
+        launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, st);
+        c.last_kernels = kn + 1;
+        return SW_OK;
+    });
+}
+
+int sw_warmstart_host(sw_ctx* ctx, const float* q, const sw_request* reqs, int32_t B,
+                      uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                      uint64_t philox_seed, sw_choice* choices, float* d_out, int32_t t_out_max,
+                      void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (q && reqs && choices && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t st = as_stream(stream);
+        SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
+                                cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(c.d_req_stage, reqs, sizeof(sw_request) * (size_t)B,
+                                cudaMemcpyHostToDevice, st));
+        int kn = plan_impl(c, c.d_q_stage, c.d_req_stage, B, seed, sel, pol, c.d_choice_stage, st);
+        launch_align_noise(c, c.d_choice_stage, c.d_req_stage, B, -1, nullptr, philox_seed, d_out,
+                           t_out_max, st);
+        SW_CUDA(cudaMemcpyAsync(choices, c.d_choice_stage, sizeof(sw_choice) * (size_t)B,
+                                cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaStreamSynchronize(st));
+        c.last_kernels = kn + 1;
+        return SW_OK;
+    });
+}
+
+int sw_local_topk(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, int32_t rank,
+                  void* d_records, int32_t* d_n, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_records && d_n)), "null argument");
+        SW_REQUIRE(k >= 1 && k <= kMaxTopK, "k must be in [1, 32]");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t st = as_stream(stream);
+        int kn = launch_search(c, d_q, B, k, rank, st);
+        // compact [B][32] records to [B][k]
+        SW_CUDA(cudaMemcpy2DAsync(d_records, sizeof(HitRec) * k, c.hits, sizeof(HitRec) * kMaxTopK,
+                                  sizeof(HitRec) * k, B, cudaMemcpyDeviceToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_n, c.nhits, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+        c.last_kernels = kn;
+        return SW_OK;
+    });
+}
+
+int sw_merge_select(sw_ctx* ctx, const void* d_gathered, const int32_t* d_gn, int32_t world,
+                    const float* d_q, const sw_request* d_req, int32_t B, int32_t k,
+                    uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                    sw_choice* d_out, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_gathered && d_gn && d_req && d_out)), "null argument");
+        check_sel(sel, pol);
+        SW_REQUIRE(k == sel->top_k, "merge k must equal the selector top_k");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t st = as_stream(stream);
+        launch_merge(c, reinterpret_cast<const HitRec*>(d_gathered), d_gn, world, B, k, st);
+        launch_select(c, c.hits, c.nhits, kMaxTopK, d_q, d_req, B, seed, *sel, *pol, d_out, 0, st);
+        c.last_kernels = 2;
+        return SW_OK;
+    });
+}
+
+int sw_score_select_host(sw_ctx* ctx, int32_t n, const double* sims, const double* s_neg,
+                         const double* durations, double L, const sw_selector_config* sel,
+                         uint64_t rng_seed, double* scores_out, int32_t* pick) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && sel && sims && s_neg && durations && scores_out && pick, "null argument");
+        SW_REQUIRE(n >= 1, "score_candidates: empty candidate list");  // selector.cpp:28
+        SW_REQUIRE(n <= kMaxTopK, "at most 32 candidates");
+        SW_REQUIRE(L > 0.0, "requested duration must be positive");    // selector.cpp:29-31
+        SW_REQUIRE(sel->temperature > 0.0, "selector temperature must be > 0");
+        SW_REQUIRE(sel->quality_threshold >= 0.0 && sel->quality_threshold <= 1.0,
+                   "selector quality threshold must be in [0, 1]");
+        Ctx& c = ctx->c;
+        SW_CUDA(cudaSetDevice(c.device));
+        double *d_in = nullptr, *d_sc = nullptr;
+        int32_t* d_pick = nullptr;
+        dalloc(&d_in, (size_t)3 * n);
+        dalloc(&d_sc, (size_t)5 * n);
+        dalloc(&d_pick, 2);
+        SW_CUDA(cudaMemcpy(d_in, sims, sizeof(double) * n, cudaMemcpyHostToDevice));
+        SW_CUDA(cudaMemcpy(d_in + n, s_neg, sizeof(double) * n, cudaMemcpyHostToDevice));
+        SW_CUDA(cudaMemcpy(d_in + 2 * n, durations, sizeof(double) * n, cudaMemcpyHostToDevice));
+        launch_score_select_one(c, n, d_in, d_in + n, d_in + 2 * n, L, *sel, rng_seed, d_sc,
+                                d_pick, nullptr);
+        SW_CUDA(cudaMemcpy(scores_out, d_sc, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost));
+        SW_CUDA(cudaMemcpy(pick, d_pick, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost));
+        cudaFree(d_in);
+        cudaFree(d_sc);
+        cudaFree(d_pick);
+        return SW_OK;
+    });
+}
+
+int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const int32_t* T,
+                  int32_t B, int32_t explore, double* phi_out, int32_t* arm_out) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && prompts && segs && T && phi_out && arm_out, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        float *d_p = nullptr, *d_s = nullptr;
+        int32_t *d_T = nullptr, *d_arm = nullptr;
+        double* d_phi = nullptr;
+        dalloc(&d_p, (size_t)B * c.D);
+        dalloc(&d_s, (size_t)B * c.D);
+        dalloc(&d_T, (size_t)B);
+        dalloc(&d_arm, (size_t)B);
+        dalloc(&d_phi, (size_t)B * kFeatureDim);
+        SW_CUDA(cudaMemcpy(d_p, prompts, sizeof(float) * B * c.D, cudaMemcpyHostToDevice));
+        SW_CUDA(cudaMemcpy(d_s, segs, sizeof(float) * B * c.D, cudaMemcpyHostToDevice));
+        SW_CUDA(cudaMemcpy(d_T, T, sizeof(int32_t) * B, cudaMemcpyHostToDevice));
+        launch_gater(c, d_p, d_s, d_T, B, explore, d_phi, d_arm, nullptr);
+        SW_CUDA(cudaMemcpy(phi_out, d_phi, sizeof(double) * B * kFeatureDim, cudaMemcpyDeviceToHost));
+        SW_CUDA(cudaMemcpy(arm_out, d_arm, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
+        cudaFree(d_p);
+        cudaFree(d_s);
+        cudaFree(d_T);
+        cudaFree(d_arm);
+        cudaFree(d_phi);
+        return SW_OK;
+    });
+}
+
+int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tc, int32_t* cand_max) {
+    if (!ctx) return SW_EINVAL;
+    if (kernels) *kernels = ctx->c.last_kernels;
+    if (used_tc) *used_tc = ctx->c.last_tc;
+    if (cand_max) *cand_max = ctx->c.last_cand_max;
+    return SW_OK;
+}
+
+}  // extern "C"

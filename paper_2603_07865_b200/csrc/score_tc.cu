@@ -1,0 +1,337 @@
+// K1 — tensor-core pre-filter for IvfIndex::search (index.cpp:289-326, hot loop :306-315).
+//
+// One CTA owns 128 queries (UMMA M) and streams a contiguous range of 256-row cache tiles
+// (UMMA N) through a TMA -> smem -> tcgen05.mma -> TMEM pipeline:
+//   warp 0      TMA producer: the CTA's 128 bf16 queries once (resident, K-major SW128), then
+//               one 256x64 bf16 cache chunk per pipeline stage
+//   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=256, K=16 per instruction),
+//               double-buffered fp32 accumulators (2 x 256 TMEM columns)
+//   warps 2-5   epilogue: TMEM lane == query, so each thread walks ITS query's 256 scores with
+//               tcgen05.ld, takes the per-entry max over the entry's Rp pyramid rows, and keeps
+//               a running 32-deep top list in registers.
+//
+// The 1M x 1024 score matrix is never written. Instead the epilogue emits a CERTIFIED candidate
+// set: with eps_q >= |bf16 score - exact score| (bf16 rounding of both operands, 2u + u^2 with
+// u = 2^-8, plus fp32 accumulation slack, times |q| * max|row|), an entry can be in the exact
+// top-k only if its approximate score >= T_a - 2 eps_q, where T_a is the k-th best approximate
+// entry score. Every CTA's running k-th best is a lower bound of T_a, and CTAs share it through
+// an atomicMax per query, so the emission threshold tightens as the scan proceeds. The exact
+// fp64 rescoring (exact.cu) then decides ties and order bit-exactly.
+#include "ptx.cuh"
+#include "sw_internal.cuh"
+
+namespace sw {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int A_CHUNK = BM * 128;  // bytes: 128 rows x 64 bf16
+constexpr int B_STAGE = BN * 128;  // bytes: 256 rows x 64 bf16
+constexpr int THREADS = 192;
+constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
+
+struct TcParams {
+    int B;
+    int kch;        // Dp / 64
+    int n_stages;
+    int k;          // top-k
+    int64_t n_tiles;
+    int64_t tiles_per_cta;
+    int64_t n_slots;  // high-water slot count
+    const uint8_t* valid;
+    const float* q_norm;
+    const uint32_t* maxnorm;
+    uint32_t* thr;
+    int32_t* cand_n;
+    int32_t* cand_slot;
+    float* cand_score;
+    float eps_rel;
+};
+
+template <int RP>
+__device__ __forceinline__ void rare_path(const float (&v)[32], int c, int64_t tile, float& theta,
+                                          float (&list)[32], float& kth, float eps2, int q,
+                                          const TcParams& p) {
+    constexpr int E = 32 / RP;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        float m = v[e * RP];
+#pragma unroll
+        for (int j = 1; j < RP; ++j) m = fmaxf(m, v[e * RP + j]);
+        m = fminf(1.0f, fmaxf(-1.0f, m));  // clamped like cosine_similarity (core.cpp:35-36)
+        if (m >= theta) {
+            const int64_t slot = (tile * BN + c * 32 + e * RP) / RP;
+            if (slot < p.n_slots && p.valid[slot]) {
+                int idx = atomicAdd(&p.cand_n[q], 1);
+                if (idx < kCandCap) {
+                    p.cand_slot[(int64_t)q * kCandCap + idx] = (int32_t)slot;
+                    p.cand_score[(int64_t)q * kCandCap + idx] = m;
+                }
+                // sorted insertion into the running list (descending)
+                float x = m;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    float hi = fmaxf(list[i], x);
+                    x = fminf(list[i], x);
+                    list[i] = hi;
+                }
+                float kk = list[0];
+#pragma unroll
+                for (int i = 1; i < 32; ++i)
+                    if (i == p.k - 1) kk = list[i];
+                kth = kk;
+                theta = fmaxf(theta, kth - eps2);
+            }
+        }
+    }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_score_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmE,
+               const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + p.kch * A_CHUNK;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * B_STAGE);
+    const int S = p.n_stages;
+    // full[S] | empty[S] | a_full | tfull[2] | tempty[2]
+    auto bar = [&](int i) { return ptx::smem_u32(&bars[i]); };
+    const int FULL = 0, EMPTY = S, AFULL = 2 * S, TFULL = 2 * S + 1, TEMPTY = 2 * S + 3;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 5]);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int qblock = blockIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
+    const int64_t t1 = min(p.n_tiles, t0 + p.tiles_per_cta);
+    if (t0 >= t1) return;  // uniform for the whole CTA
+    const int ntiles = (int)(t1 - t0);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(bar(FULL + i), 1);
+            ptx::mbar_init(bar(EMPTY + i), 1);
+        }
+        ptx::mbar_init(bar(AFULL), 1);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(bar(TFULL + i), 1);
+            ptx::mbar_init(bar(TEMPTY + i), 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmQ);
+        ptx::tma_prefetch_desc(&tmE);
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
+            for (int kc = 0; kc < p.kch; ++kc)
+                ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
+                                 qblock * BM);
+            uint32_t it = 0;
+            for (int lt = 0; lt < ntiles; ++lt) {
+                const int64_t tile = t0 + lt;
+                for (int kc = 0; kc < p.kch; ++kc, ++it) {
+                    const int s = (int)(it % S);
+                    const uint32_t ph = (it / S) & 1u;
+                    ptx::mbar_wait(bar(EMPTY + s), ph ^ 1u);
+                    ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
+                    ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
+                                     kc * 64, (int32_t)(tile * BN));
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (one thread issues for the whole CTA)
+            ptx::mbar_wait(bar(AFULL), 0);
+            ptx::tc_fence_after();
+            uint32_t it = 0;
+            for (int lt = 0; lt < ntiles; ++lt) {
+                const int acc = lt & 1;
+                const uint32_t aph = (lt >> 1) & 1u;
+                ptx::mbar_wait(bar(TEMPTY + acc), aph ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kc = 0; kc < p.kch; ++kc, ++it) {
+                    const int s = (int)(it % S);
+                    const uint32_t ph = (it / S) & 1u;
+                    ptx::mbar_wait(bar(FULL + s), ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + kc * A_CHUNK);
+                    const uint32_t b0 = ptx::smem_u32(sB + s * B_STAGE);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(a0 + k * 32),
+                                      ptx::umma_desc_sw128(b0 + k * 32), IDESC,
+                                      (kc | k) != 0 ? 1u : 0u);
+                    ptx::mma_commit(bar(EMPTY + s));  // frees the smem stage when MMAs finish
+                }
+                ptx::mma_commit(bar(TFULL + acc));  // accumulator ready for the epilogue
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: TMEM lane == query
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
+        const int q = qblock * BM + quarter * 32 + lane;
+        const bool qvalid = q < p.B;
+        float eps2 = 0.0f;
+        if (qvalid) eps2 = 2.0f * p.eps_rel * p.q_norm[q] * ord2f(*p.maxnorm);
+        float theta = -INFINITY, kth = -INFINITY, published = -INFINITY;
+        float list[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) list[i] = -INFINITY;
+        const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+
+        for (int lt = 0; lt < ntiles; ++lt) {
+            const int acc = lt & 1;
+            const uint32_t aph = (lt >> 1) & 1u;
+            const int64_t tile = t0 + lt;
+            if (qvalid) {
+                float g = ord2f(__ldcg(&p.thr[q]));
+                theta = fmaxf(theta, g - eps2);
+            }
+            ptx::mbar_wait(bar(TFULL + acc), aph);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
+                ptx::tmem_ld_wait();
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                float m = v[0];
+#pragma unroll
+                for (int j = 1; j < 32; ++j) m = fmaxf(m, v[j]);
+                if (qvalid && fminf(1.0f, m) >= theta)
+                    rare_path<RP>(v, c, tile, theta, list, kth, eps2, q, p);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(TEMPTY + acc));
+            if (qvalid && kth > published) {
+                atomicMax(&p.thr[q], f2ord(kth));
+                published = kth;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encoder() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+    PFN_encodeTiled enc = get_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {inner * sizeof(__nv_bfloat16)};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int RP>
+void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        SW_CUDA(cudaFuncSetAttribute(k_score_tc<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     c.smem_optin));
+        attr_set = true;
+    }
+    k_score_tc<RP><<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+}
+
+}  // namespace
+
+bool encode_tensor_maps(Ctx& c) {
+    if (c.Dp > 512) return false;
+    bool ok = encode_2d(&c.tm_rows, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN);
+    ok = ok && encode_2d(&c.tm_q, c.q_bf, (uint64_t)c.Dp, (uint64_t)c.BmaxPad, BM);
+    return ok;
+}
+
+// Returns the number of kernels launched (1).
+int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
+    TcParams p{};
+    p.B = B;
+    p.kch = c.Dp / 64;
+    const int budget = c.smem_optin - 1024 - 256;
+    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_STAGE);
+    SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
+    p.k = k;
+    const int64_t rows_hw = c.high_water * c.Rp;
+    p.n_tiles = (rows_hw + BN - 1) / BN;
+    const int qblocks = (B + BM - 1) / BM;
+    int64_t chunks = std::max<int64_t>(1, 148 / qblocks);
+    chunks = std::min<int64_t>(chunks, p.n_tiles);
+    p.tiles_per_cta = (p.n_tiles + chunks - 1) / chunks;
+    chunks = (p.n_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
+    p.n_slots = c.high_water;
+    p.valid = c.valid;
+    p.q_norm = c.q_norm;
+    p.maxnorm = c.maxnorm;
+    p.thr = c.thr;
+    p.cand_n = c.cand_n;
+    p.cand_slot = c.cand_slot;
+    p.cand_score = c.cand_score;
+    // |bf16 dot - exact| <= (2u + u^2) |q||e| + fp32 accumulation slack; u = 2^-8
+    p.eps_rel = 0.0081f;
+    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;
+    dim3 grid((unsigned)qblocks, (unsigned)chunks);
+    switch (c.Rp) {
+        case 1: launch_tc_rp<1>(c, p, grid, smem, st); break;
+        case 2: launch_tc_rp<2>(c, p, grid, smem, st); break;
+        case 4: launch_tc_rp<4>(c, p, grid, smem, st); break;
+        case 8: launch_tc_rp<8>(c, p, grid, smem, st); break;
+        case 16: launch_tc_rp<16>(c, p, grid, smem, st); break;
+        case 32: launch_tc_rp<32>(c, p, grid, smem, st); break;
+        default: throw Error(SW_EINVAL, "rows per entry pad must be a power of two <= 32");
+    }
+    SW_CUDA(cudaGetLastError());
+    return 1;
+}
+
+}  // namespace sw

@@ -1,0 +1,352 @@
+// K3 — duration/quality gate, stochastic select and Skip Gater, one thread per request.
+//
+// Restates, in the same fp64 operation order, score_candidates + select (selector.cpp:24-85),
+// the selector RNG draw Rng(derive_seed(seed, id, 2)).uniform() (pipeline.cpp:211,
+// core.hpp:83), context_features (gater.cpp:13-30), choose_arm (gater.cpp:52-92, double x double
+// products WITHOUT fma), the rule / fixed policies (pipeline.cpp:180-202) and
+// t* = llround(0.05 * arm * T) (gater.hpp:16-19, simgen.cpp:70).
+// The only non-IEEE-exact step is exp() in the softmax (and log1p/exp in explore mode): CUDA's
+// double exp is within 1 ulp of glibc's, so a draw whose cumulative sum lands within that slack
+// of the target is flagged SW_CHOICE_AMBIGUOUS_DRAW instead of being silently trusted (H3).
+#include "sw_internal.cuh"
+
+namespace sw {
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // core.cpp:58-63
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b,
+                                                uint64_t c) {  // core.cpp:65-71
+    uint64_t s = splitmix64(base ^ 0x53454d5741524dULL);
+    s = splitmix64(s ^ a);
+    s = splitmix64(s ^ b);
+    return splitmix64(s ^ c);
+}
+// First output of std::mt19937_64(seed): only state words 0, 1 and 156 feed the first refill.
+__device__ __forceinline__ uint64_t mt64_first(uint64_t seed) {
+    const uint64_t f = 6364136223846793005ULL;
+    uint64_t x = seed, x1 = 0;
+#pragma unroll 4
+    for (uint64_t i = 1; i <= 156; ++i) {
+        x = f * (x ^ (x >> 62)) + i;
+        if (i == 1) x1 = x;
+    }
+    const uint64_t y = (seed & 0xFFFFFFFF80000000ULL) | (x1 & 0x7FFFFFFFULL);
+    uint64_t z = x ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+__device__ __forceinline__ double clamp01(double v) { return fmin(1.0, fmax(0.0, v)); }
+
+__device__ __forceinline__ double softplus(double x) {  // gater.cpp:32-36
+    if (x > 30.0) return x;
+    if (x < -30.0) return exp(x);
+    return log1p(exp(x));
+}
+
+struct GateOut {
+    int pick;
+    uint32_t flags;
+};
+
+// score_candidates + select over n records; scores optionally written (n x 5).
+__device__ GateOut gate_select(int n, const double* sims, const double* snegs,
+                               const double* durs, double L, double temp, double thr,
+                               uint64_t rng_seed, double* scores) {
+    double s_pos[kMaxTopK], a[kMaxTopK], b[kMaxTopK], q[kMaxTopK];
+    double max_pos = 0.0, max_neg_dis = 0.0;
+    for (int i = 0; i < n; ++i) {
+        s_pos[i] = clamp01(sims[i]);
+        max_pos = fmax(max_pos, s_pos[i]);
+        max_neg_dis = fmax(max_neg_dis, 1.0 - snegs[i]);
+    }
+    const double lo = 0.5 * L, hi = 1.5 * L;
+    for (int i = 0; i < n; ++i) {
+        a[i] = max_pos > 0.0 ? __ddiv_rn(s_pos[i], max_pos) : 0.0;
+        b[i] = max_neg_dis > 0.0 ? __ddiv_rn(1.0 - snegs[i], max_neg_dis) : 0.0;
+        const bool ok = durs[i] >= lo && durs[i] <= hi;
+        q[i] = ok ? fmin(a[i], b[i]) : 0.0;
+        if (scores) {
+            scores[i * 5 + 0] = s_pos[i];
+            scores[i * 5 + 1] = snegs[i];
+            scores[i * 5 + 2] = a[i];
+            scores[i * 5 + 3] = b[i];
+            scores[i * 5 + 4] = q[i];
+        }
+    }
+    GateOut g{-1, 0u};
+    int surv[kMaxTopK], ns = 0;
+    for (int i = 0; i < n; ++i)
+        if (q[i] >= thr) surv[ns++] = i;
+    if (ns == 0) return g;  // no survivor: miss, and no RNG draw (selector.cpp:67)
+    double max_s = s_pos[surv[0]];
+    for (int j = 0; j < ns; ++j) max_s = fmax(max_s, s_pos[surv[j]]);
+    double w[kMaxTopK], total = 0.0;
+    for (int j = 0; j < ns; ++j) {
+        w[j] = exp(__ddiv_rn(s_pos[surv[j]] - max_s, temp));
+        total = __dadd_rn(total, w[j]);
+    }
+    const double u = (double)(mt64_first(rng_seed) >> 11) * 0x1.0p-53;
+    const double target = __dmul_rn(u, total);
+    const double slack = 1e-13 * total;
+    double acc = 0.0;
+    g.pick = surv[ns - 1];
+    for (int j = 0; j < ns; ++j) {
+        acc = __dadd_rn(acc, w[j]);
+        if (fabs(acc - target) <= slack) g.flags |= SW_CHOICE_AMBIGUOUS_DRAW;
+        if (acc >= target) {
+            g.pick = surv[j];
+            break;
+        }
+    }
+    return g;
+}
+
+// choose_arm (gater.cpp:70-92): products and sums strictly unfused.
+__device__ int choose_arm(const float* __restrict__ theta, const float* __restrict__ psi, int fd,
+                          double beta, const double* phi, int explore, uint32_t* flags) {
+    for (int i = 0; i < fd; ++i)
+        if (!isfinite(phi[i])) {
+            *flags |= SW_CHOICE_NONFINITE_PHI;
+            return 0;
+        }
+    int best = 0;
+    double best_score = -INFINITY, second = -INFINITY;
+    for (int a = 0; a < kNumArms; ++a) {
+        double s = 0.0;
+        for (int i = 0; i < fd; ++i) s = __dadd_rn(s, __dmul_rn((double)theta[a * fd + i], phi[i]));
+        if (explore) {
+            double u = 0.0;
+            for (int i = 0; i < fd; ++i) u = __dadd_rn(u, __dmul_rn((double)psi[a * fd + i], phi[i]));
+            s = __dadd_rn(s, __dmul_rn(beta, softplus(u)));
+        }
+        if (s >= best_score) {  // ties to the larger skip fraction
+            second = best_score;
+            best_score = s;
+            best = a;
+        } else if (s > second) {
+            second = s;
+        }
+    }
+    if (explore && fabs(best_score - second) <= 1e-13 * fmax(1.0, fabs(best_score)))
+        *flags |= SW_CHOICE_AMBIGUOUS_ARM;
+    return best;
+}
+
+struct SelParams {
+    uint64_t seed;
+    int top_k;
+    double temp, thr;
+    int policy, fixed_arm, rule_arm;
+    double rule_thr;
+    double fps;
+    const float* theta;
+    const float* psi;
+    int fd;
+    double beta;
+};
+
+__global__ void k_select(int B, const HitRec* __restrict__ hits, const int32_t* __restrict__ nh_in,
+                         int ld, const sw_request* __restrict__ reqs, SelParams p,
+                         sw_choice* __restrict__ out) {
+    const int bq = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bq >= B) return;
+    const sw_request rq = reqs[bq];
+    int nh = nh_in[bq];
+    uint32_t flags = 0;
+    if (nh < 0) {
+        nh = -nh - 1;
+        flags |= SW_CHOICE_INCOMPLETE;
+    }
+    nh = min(nh, p.top_k);
+    const HitRec* h = hits + (int64_t)bq * ld;
+    sw_choice c;
+    memset(&c, 0, sizeof(c));
+    c.pick = -1;
+    c.n_hits = nh;
+    int hit = 0;
+    double phi[kFeatureDim];
+    if (nh > 0) {
+        double sims[kMaxTopK], sn[kMaxTopK], du[kMaxTopK];
+        for (int i = 0; i < nh; ++i) {
+            sims[i] = h[i].sim;
+            sn[i] = h[i].s_neg;
+            du[i] = h[i].length_s;  // matched segment duration (pipeline.cpp:122)
+        }
+        GateOut g = gate_select(nh, sims, sn, du, rq.duration_s, p.temp, p.thr,
+                                derive_seed(p.seed, rq.id, 2, 0), nullptr);
+        flags |= g.flags;
+        if (g.pick >= 0) {
+            const HitRec& ch = h[g.pick];
+            hit = 1;
+            c.pick = g.pick;
+            c.entry_id = ch.entry_id;
+            c.segment.level = ch.level;
+            c.segment.start_s = ch.start_s;
+            c.segment.length_s = ch.length_s;
+            c.similarity = ch.sim;  // cos(prompt, seg_emb) (pipeline.cpp:173)
+            c.owner = ch.owner;
+            c.slot = ch.slot;
+            phi[0] = ch.sim;
+            for (int j = 0; j < 8; ++j) phi[1 + j] = ch.phi[j];
+            phi[9] = (double)rq.total_steps / 200.0;
+            phi[10] = 1.0;
+        }
+    }
+    int arm = 0;
+    if (hit) {
+        if (p.policy == SW_POLICY_EXPLOIT || p.policy == SW_POLICY_EXPLORE)
+            arm = choose_arm(p.theta, p.psi, p.fd, p.beta, phi, p.policy == SW_POLICY_EXPLORE,
+                             &flags);
+        else if (p.policy == SW_POLICY_RULE)
+            arm = c.similarity >= p.rule_thr ? p.rule_arm : 0;
+        else
+            arm = p.fixed_arm;
+    } else if (p.policy == SW_POLICY_FIXED) {
+        arm = p.fixed_arm;  // latency held constant even on a miss (pipeline.cpp:229-231)
+    }
+    const double skip = 0.05 * (double)arm;
+    c.hit = hit;
+    c.arm = arm;
+    c.skip_fraction = skip;
+    c.steps_skipped = (int32_t)llround(skip * (double)rq.total_steps);
+    c.t_out = hit ? (int32_t)llround(rq.duration_s * p.fps) : 0;
+    c.flags = flags;
+    out[bq] = c;
+}
+
+// Deterministic merge of world sorted top-k lists (sim desc, id asc) into c.hits.
+__global__ void k_merge(int B, int k, int world, const HitRec* __restrict__ g,
+                        const int32_t* __restrict__ gn, HitRec* __restrict__ out,
+                        int32_t* __restrict__ out_n) {
+    const int bq = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bq >= B) return;
+    int head[16];
+    int lim[16];
+    bool incomplete = false;
+    for (int r = 0; r < world; ++r) {
+        head[r] = 0;
+        int n = gn[(int64_t)r * B + bq];
+        if (n < 0) {
+            n = -n - 1;
+            incomplete = true;
+        }
+        lim[r] = n;
+    }
+    int m = 0;
+    for (; m < k; ++m) {
+        int br = -1;
+        for (int r = 0; r < world; ++r) {
+            if (head[r] >= lim[r]) continue;
+            const HitRec& x = g[((int64_t)r * B + bq) * k + head[r]];
+            if (br < 0) {
+                br = r;
+                continue;
+            }
+            const HitRec& y = g[((int64_t)br * B + bq) * k + head[br]];
+            if (x.sim > y.sim || (x.sim == y.sim && x.entry_id < y.entry_id)) br = r;
+        }
+        if (br < 0) break;
+        out[(int64_t)bq * kMaxTopK + m] = g[((int64_t)br * B + bq) * k + head[br]];
+        head[br]++;
+    }
+    out_n[bq] = incomplete ? -m - 1 : m;
+}
+
+__global__ void k_score_select_one(int n, const double* sims, const double* sneg,
+                                   const double* durs, double L, double temp, double thr,
+                                   uint64_t rng_seed, double* scores, int32_t* pick) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        GateOut g = gate_select(n, sims, sneg, durs, L, temp, thr, rng_seed, scores);
+        pick[0] = g.pick;
+        pick[1] = (int32_t)g.flags;
+    }
+}
+
+__global__ void k_gater(const float* __restrict__ P, const float* __restrict__ Sg,
+                        const int32_t* __restrict__ T, int B, int D, const float* theta,
+                        const float* psi, int fd, double beta, int explore, double* phi_out,
+                        int32_t* arm_out) {
+    const int bq = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bq >= B) return;
+    const float* p = P + (int64_t)bq * D;
+    const float* c = Sg + (int64_t)bq * D;
+    double phi[kFeatureDim];
+    double s = 0.0;
+    for (int i = 0; i < D; ++i) s = fma((double)p[i], (double)c[i], s);
+    phi[0] = fmin(1.0, fmax(-1.0, s));
+    for (int j = 0; j < 8; ++j) {
+        const size_t lo = (size_t)j * D / 8, hi = (size_t)(j + 1) * D / 8;
+        double t = 0.0;
+        for (size_t i = lo; i < hi; ++i) t = fma((double)p[i], (double)c[i], t);
+        phi[1 + j] = t;
+    }
+    phi[9] = (double)T[bq] / 200.0;
+    phi[10] = 1.0;
+    uint32_t flags = 0;
+    arm_out[bq] = choose_arm(theta, psi, fd, beta, phi, explore, &flags);
+    for (int i = 0; i < kFeatureDim; ++i) phi_out[(int64_t)bq * kFeatureDim + i] = phi[i];
+}
+
+}  // namespace
+
+void launch_select(Ctx& c, const HitRec* d_hits, const int32_t* d_nh, int ld, const float* d_q,
+                   const sw_request* d_req, int B, uint64_t seed, const sw_selector_config& sel,
+                   const sw_policy& pol, sw_choice* d_out, uint32_t extra_flags_mask,
+                   cudaStream_t st) {
+    (void)d_q;
+    (void)extra_flags_mask;
+    if (B == 0) return;
+    SelParams p;
+    p.seed = seed;
+    p.top_k = sel.top_k;
+    p.temp = sel.temperature;
+    p.thr = sel.quality_threshold;
+    p.policy = pol.kind;
+    p.fixed_arm = pol.fixed_arm;
+    p.rule_arm = (int)llround(pol.rule_skip_fraction / 0.05);  // pipeline.cpp:193
+    p.rule_thr = pol.rule_similarity_threshold;
+    p.fps = c.cfg.latent_fps;
+    p.theta = c.theta;
+    p.psi = c.psi;
+    p.fd = c.fd;
+    p.beta = c.beta;
+    k_select<<<(B + 63) / 64, 64, 0, st>>>(B, d_hits, d_nh, ld, d_req, p, d_out);
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_merge(Ctx& c, const HitRec* d_gathered, const int32_t* d_gn, int world, int B, int k,
+                  cudaStream_t st) {
+    SW_REQUIRE(world >= 1 && world <= 16, "world size must be in [1, 16]");
+    if (B == 0) return;
+    k_merge<<<(B + 127) / 128, 128, 0, st>>>(B, k, world, d_gathered, d_gn, c.hits, c.nhits);
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_score_select_one(Ctx& c, int n, const double* d_sims, const double* d_sneg,
+                             const double* d_dur, double L, const sw_selector_config& sel,
+                             uint64_t rng_seed, double* d_scores, int32_t* d_pick,
+                             cudaStream_t st) {
+    (void)c;
+    k_score_select_one<<<1, 32, 0, st>>>(n, d_sims, d_sneg, d_dur, L, sel.temperature,
+                                         sel.quality_threshold, rng_seed, d_scores, d_pick);
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_gater(Ctx& c, const float* d_p, const float* d_s, const int32_t* d_T, int B,
+                  int explore, double* d_phi, int32_t* d_arm, cudaStream_t st) {
+    if (B == 0) return;
+    k_gater<<<(B + 63) / 64, 64, 0, st>>>(d_p, d_s, d_T, B, c.D, c.theta, c.psi, c.fd, c.beta,
+                                         explore, d_phi, d_arm);
+    SW_CUDA(cudaGetLastError());
+}
+
+}  // namespace sw

@@ -1,0 +1,179 @@
+// Internal definitions shared by the semwarm_b200 translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <set>
+#include <shared_mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "semwarm_b200.h"
+
+namespace sw {
+
+// --------------------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string& msg);
+
+#define SW_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            throw ::sw::Error(SW_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define SW_REQUIRE(cond, msg)                                      \
+    do {                                                           \
+        if (!(cond)) throw ::sw::Error(SW_EINVAL, std::string(msg)); \
+    } while (0)
+
+// --------------------------------------------------------------------------- constants
+constexpr int kNumArms = 14;          // gater.hpp:13
+constexpr int kFeatureDim = 11;       // gater.hpp:28
+constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep running list
+constexpr int kCandCap = 8192;        // certified candidates per query
+constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
+
+// Per-shard top-k record (SW_HIT_RECORD_BYTES = 128): everything the replicated select /
+// gater stage needs, so the all-gather carries no embeddings.
+struct __align__(16) HitRec {
+    double sim;        // exact clamped fp64 cosine of the winning segment (core.cpp:33-38)
+    uint64_t entry_id;
+    int32_t level;
+    int32_t slot;      // arena slot on the owner shard
+    double start_s;
+    double length_s;
+    double s_neg;      // clamp01(cos(segment row, negative)) (selector.cpp:41-42)
+    double phi[8];     // block sums of the gater features (gater.cpp:18-26)
+    int32_t row;       // pyramid row index within the entry
+    int32_t owner;     // shard rank
+};
+static_assert(sizeof(HitRec) == SW_HIT_RECORD_BYTES, "hit record must stay 128 bytes");
+
+// --------------------------------------------------------------------------- order helpers
+// float/double -> unsigned key preserving order (for atomicMax and packed comparisons)
+__host__ __device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float ord2f(uint32_t u) {
+    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+__host__ __device__ __forceinline__ uint64_t d2ord(double d) {
+    uint64_t u;
+    memcpy(&u, &d, 8);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// --------------------------------------------------------------------------- context
+struct Ctx {
+    sw_config cfg{};
+    int device = 0;
+    int D = 0, Dp = 0, Df = 0;   // dim, bf16 row stride (mult of 64), fp32 row stride (mult of 4)
+    int R = 0, Rp = 0, logRp = 0;
+    int64_t S = 0;               // entry slots
+    int64_t Lslots = 0;          // latent slots
+    int C = 0, Tmax = 0, F = 0;
+    int Bmax = 0, BmaxPad = 0;
+
+    // device arena (Cache Manager data plane)
+    float* rows = nullptr;            // [S*Rp][Df] fp32 master rows
+    __nv_bfloat16* rows_bf = nullptr; // [S*Rp][Dp] bf16 shadow (pad rows = copy of row 0)
+    double* sneg = nullptr;           // [S*Rp]
+    sw_segment* segs = nullptr;       // [S*Rp]
+    uint64_t* ids = nullptr;          // [S]
+    int32_t* nrows = nullptr;         // [S]
+    uint8_t* valid = nullptr;         // [S]
+    int32_t* tsrc = nullptr;          // [S]
+    float* latent = nullptr;          // [Lslots][C][Tmax][F]
+    uint32_t* maxnorm = nullptr;      // ordered float bits, max row L2 norm
+    float* neg = nullptr;             // [Df]
+    float* theta = nullptr;           // [14*11]
+    float* psi = nullptr;
+    double* abar = nullptr;
+    int n_abar = 0;
+    double beta = 1.0;
+    int fd = kFeatureDim;
+    bool have_neg = false;
+
+    // batch scratch
+    __nv_bfloat16* q_bf = nullptr;  // [BmaxPad][Dp]
+    float* q_norm = nullptr;        // [Bmax]
+    uint32_t* thr = nullptr;        // [Bmax] shared running k-th best (ordered)
+    int32_t* cand_n = nullptr;      // [3][Bmax]: raw count | compacted count | overflow flag
+    int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
+    float* cand_score = nullptr;    // [Bmax][kCandCap]
+    double* cand_exact = nullptr;   // [Bmax][kCandCap]
+    int32_t* cand_row = nullptr;    // [Bmax][kCandCap]
+    int32_t* cand_list = nullptr;   // [Bmax][kCandCap] compacted certified candidates
+    HitRec* hits = nullptr;         // [Bmax][kMaxTopK]
+    int32_t* nhits = nullptr;       // [Bmax]
+    float* d_q_stage = nullptr;     // [Bmax][D] (host e2e staging)
+    sw_request* d_req_stage = nullptr;
+    sw_choice* d_choice_stage = nullptr;
+    void* h_pinned = nullptr;       // pinned host staging
+    size_t h_pinned_bytes = 0;
+
+    // TMA descriptors (encoded once at creation; cover the full capacity)
+    CUtensorMap tm_rows{};
+    CUtensorMap tm_q{};
+    bool tc_ok = false;
+    int smem_optin = 0;
+
+    // host bookkeeping (mirrors the reference's entry_vector_counts_, index.hpp:92)
+    std::unordered_map<uint64_t, int64_t> slot_of;
+    std::vector<int32_t> h_nrows;
+    std::set<int64_t> free_slots;
+    int64_t high_water = 0;
+    mutable std::shared_mutex mu;
+
+    cudaStream_t mstream = nullptr;   // mutation stream
+    // last launch info
+    int last_kernels = 0, last_tc = 0, last_cand_max = 0;
+};
+
+// kernel-side launchers (implemented in the .cu files)
+void launch_insert_rows_full(Ctx& c, int64_t n, const int64_t* d_slot, const int32_t* d_base,
+                             const int64_t* d_row_off, const uint64_t* d_ids, const float* d_rows,
+                             const sw_segment* d_segs, cudaStream_t st);
+void launch_copy_latents(Ctx& c, int64_t n, const int64_t* d_slot, const float* d_lat,
+                         const int64_t* d_lat_off, const int32_t* d_tsrc, cudaStream_t st);
+void launch_recompute_sneg(Ctx& c, cudaStream_t st);
+void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, uint64_t seed,
+                           double delta, cudaStream_t st);
+
+int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t st);
+void launch_hits_to_public(Ctx& c, int B, int k, sw_hit* d_out, int32_t* d_n, cudaStream_t st);
+void launch_select(Ctx& c, const HitRec* d_hits, const int32_t* d_nh, int ld, const float* d_q,
+                   const sw_request* d_req, int B, uint64_t seed, const sw_selector_config& sel,
+                   const sw_policy& pol, sw_choice* d_out, uint32_t extra_flags_mask,
+                   cudaStream_t st);
+void launch_merge(Ctx& c, const HitRec* d_gathered, const int32_t* d_gn, int world, int B,
+                  int k, cudaStream_t st);
+void launch_align_noise(Ctx& c, const sw_choice* d_ch, const sw_request* d_req, int B,
+                        int rank, const float* d_eps, uint64_t seed, float* d_out, int t_out_max,
+                        cudaStream_t st);
+void launch_score_select_one(Ctx& c, int n, const double* d_sims, const double* d_sneg,
+                             const double* d_dur, double L, const sw_selector_config& sel,
+                             uint64_t rng_seed, double* d_scores, int32_t* d_pick,
+                             cudaStream_t st);
+void launch_gater(Ctx& c, const float* d_p, const float* d_s, const int32_t* d_T, int B,
+                  int explore, double* d_phi, int32_t* d_arm, cudaStream_t st);
+
+bool encode_tensor_maps(Ctx& c);
+
+}  // namespace sw

@@ -1,0 +1,276 @@
+"""Python host layer over the C-ABI, mirroring the reference's C++ API for the warm-start path.
+
+Reference interface                                   here
+IvfIndex::insert / remove / search (index.hpp:59-67)  WarmStartCache.insert / remove / search
+score_candidates + select (selector.hpp:50-58)         score_select
+context_features + choose_arm (gater.hpp:30,56-57)     gater
+Pipeline::plan_request + pick_arm (pipeline.cpp:91-202) WarmStartCache.plan
+slice_clip + (new) forward noising                     WarmStartCache.align_noise / warmstart
+
+Errors follow the reference: invalid arguments raise ValueError (std::invalid_argument), an
+unknown id on remove warns and is a no-op (index.cpp:243-245), a miss is an empty result.
+Device buffers come from torch (plumbing only); the compute is libsemwarm_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import (CHOICE_DTYPE, HIT_DTYPE, POLICY, REQUEST_DTYPE, SEGMENT_DTYPE, SwConfig,
+                   SwPolicy, SwSelectorConfig, check, ptr)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class SelectorConfig:
+    """SelectorConfig (selector.hpp:25-33) — negative embedding set on the cache."""
+    top_k: int = 8
+    temperature: float = 0.05
+    quality_threshold: float = 0.6
+
+    def c(self) -> SwSelectorConfig:
+        return SwSelectorConfig(int(self.top_k), 0, float(self.temperature),
+                                float(self.quality_threshold))
+
+
+@dataclass
+class Policy:
+    """SkipPolicy + parameters (pipeline.hpp:17-22, 37-41)."""
+    kind: str = "exploit"
+    fixed_arm: int = 0
+    rule_similarity_threshold: float = 0.35
+    rule_skip_fraction: float = 0.55
+
+    def c(self) -> SwPolicy:
+        return SwPolicy(POLICY[self.kind], int(self.fixed_arm),
+                        float(self.rule_similarity_threshold), float(self.rule_skip_fraction))
+
+
+def segments(levels, starts, lengths) -> np.ndarray:
+    s = np.zeros(len(levels), SEGMENT_DTYPE)
+    s["level"], s["start_s"], s["length_s"] = levels, starts, lengths
+    return s
+
+
+def requests(ids, durations, total_steps) -> np.ndarray:
+    r = np.zeros(len(ids), REQUEST_DTYPE)
+    r["id"], r["duration_s"], r["total_steps"] = ids, durations, total_steps
+    return r
+
+
+class WarmStartCache:
+    """One device-resident cache shard: arena + batched warm-start path."""
+
+    def __init__(self, dim: int, rows_per_entry: int = 7, max_entries: int = 1024,
+                 latent_shape=(8, 256, 16), max_batch: int = 1024, latent_slots: int = 0,
+                 fps: float = 25.0, exact_only: bool = False, tc_always: bool = False,
+                 device: int = 0):
+        L = _lib.lib()
+        cfg = SwConfig()
+        cfg.dim = dim
+        cfg.rows_per_entry = rows_per_entry
+        cfg.max_entries = max_entries
+        cfg.latent_c, cfg.latent_t_max, cfg.latent_f = latent_shape if latent_shape else (0, 0, 0)
+        cfg.max_batch = max_batch
+        cfg.latent_slots = latent_slots
+        cfg.latent_fps = fps
+        cfg.flags = (_lib.SW_FLAG_EXACT_ONLY if exact_only else 0) | (
+            _lib.SW_FLAG_TC_ALWAYS if tc_always else 0)
+        h = C.c_void_p()
+        check(L.sw_ctx_create(C.byref(cfg), device, C.byref(h)), "sw_ctx_create")
+        self._h = h
+        self.dim = dim
+        self.device = device
+        self.latent_shape = tuple(latent_shape) if latent_shape else None
+        self.max_batch = max_batch
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().sw_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ configuration
+    def set_negative(self, neg: np.ndarray):
+        neg = np.ascontiguousarray(neg, np.float32)
+        check(_lib.lib().sw_set_negative(self._h, ptr(neg)), "sw_set_negative")
+
+    def set_gater(self, theta, psi, beta: float = 1.0):
+        theta = np.ascontiguousarray(theta, np.float32).reshape(-1)
+        psi = np.ascontiguousarray(psi, np.float32).reshape(-1)
+        check(_lib.lib().sw_set_gater(self._h, ptr(theta), ptr(psi), 11, beta), "sw_set_gater")
+
+    def set_schedule(self, abar):
+        abar = np.ascontiguousarray(abar, np.float64)
+        check(_lib.lib().sw_set_schedule(self._h, ptr(abar), len(abar)), "sw_set_schedule")
+
+    # ------------------------------------------------------------------ arena (K5)
+    def insert(self, entry_id: int, rows, levels, starts, lengths, latent=None):
+        rows = np.ascontiguousarray(rows, np.float32).reshape(-1, self.dim)
+        sg = segments(levels, starts, lengths)
+        lat = None if latent is None else np.ascontiguousarray(latent, np.float32)
+        t_src = 0 if lat is None else lat.shape[1]
+        check(_lib.lib().sw_arena_insert(self._h, entry_id, rows.shape[0], ptr(rows), ptr(sg),
+                                         ptr(lat), t_src), "sw_arena_insert")
+
+    def insert_batch(self, ids, row_off, rows, levels, starts, lengths, latents=None,
+                     lat_off=None, t_src=None):
+        ids = np.ascontiguousarray(ids, np.uint64)
+        row_off = np.ascontiguousarray(row_off, np.int64)
+        rows = np.ascontiguousarray(rows, np.float32)
+        sg = segments(levels, starts, lengths)
+        lp = lo = ts = None
+        if latents is not None:
+            lp = np.ascontiguousarray(latents, np.float32)
+            lo = np.ascontiguousarray(lat_off, np.int64)
+            ts = np.ascontiguousarray(t_src, np.int32)
+        check(_lib.lib().sw_arena_insert_batch(self._h, len(ids), ptr(ids), ptr(row_off),
+                                               ptr(rows), ptr(sg), ptr(lp), ptr(lo), ptr(ts), 0),
+              "sw_arena_insert_batch")
+
+    def remove(self, entry_id: int) -> bool:
+        rc = check(_lib.lib().sw_arena_remove(self._h, entry_id), "sw_arena_remove")
+        if rc == _lib.SW_WARN_UNKNOWN_ID:
+            warnings.warn(f"remove of unknown entry id {entry_id}")
+            return False
+        return True
+
+    def replace(self, entry_id: int, rows, levels, starts, lengths, latent=None) -> bool:
+        rows = np.ascontiguousarray(rows, np.float32).reshape(-1, self.dim)
+        sg = segments(levels, starts, lengths)
+        lat = None if latent is None else np.ascontiguousarray(latent, np.float32)
+        t_src = 0 if lat is None else lat.shape[1]
+        rc = check(_lib.lib().sw_arena_replace(self._h, entry_id, rows.shape[0], ptr(rows),
+                                               ptr(sg), ptr(lat), t_src), "sw_arena_replace")
+        return rc == _lib.SW_OK
+
+    def entry_count(self) -> int:
+        return int(_lib.lib().sw_arena_entry_count(self._h))
+
+    def contains(self, entry_id: int) -> bool:
+        return bool(_lib.lib().sw_arena_contains(self._h, entry_id))
+
+    def fill_synthetic(self, n: int, first_id: int = 1, seed: int = 1, delta: float = 1.0):
+        check(_lib.lib().sw_arena_fill_synthetic(self._h, n, first_id, seed, delta),
+              "sw_arena_fill_synthetic")
+
+    def read_rows(self, entry_id: int, cap: int = 32) -> np.ndarray:
+        out = np.zeros((cap, self.dim), np.float32)
+        n = check(_lib.lib().sw_arena_read_rows(self._h, entry_id, ptr(out), cap), "read_rows")
+        return out[:n]
+
+    def launch_info(self):
+        k, t, m = C.c_int32(), C.c_int32(), C.c_int32()
+        _lib.lib().sw_last_launch_info(self._h, C.byref(k), C.byref(t), C.byref(m))
+        return {"kernels": k.value, "tensor_cores": bool(t.value)}
+
+    # ------------------------------------------------------------------ hot path
+    def _dev(self, a, dtype):
+        torch = _torch()
+        if isinstance(a, torch.Tensor):
+            assert a.is_cuda and a.is_contiguous()
+            return a
+        return torch.from_numpy(np.ascontiguousarray(a, dtype)).to(f"cuda:{self.device}")
+
+    def search(self, queries, k: int):
+        """IvfIndex::search for each row of `queries` (exhaustive, exact). Returns (hits, n)."""
+        torch = _torch()
+        q = self._dev(queries, np.float32).reshape(-1, self.dim)
+        B = q.shape[0]
+        out = torch.empty(B * k * HIT_DTYPE.itemsize, dtype=torch.uint8, device=q.device)
+        n = torch.empty(B, dtype=torch.int32, device=q.device)
+        st = torch.cuda.current_stream(q.device).cuda_stream
+        check(_lib.lib().sw_search(self._h, ptr(q), B, k, ptr(out), ptr(n), st), "sw_search")
+        hits = out.cpu().numpy().view(HIT_DTYPE).reshape(B, k)
+        return hits, n.cpu().numpy()
+
+    def search_host(self, queries: np.ndarray, k: int):
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        B = q.shape[0]
+        out = np.zeros((B, k), HIT_DTYPE)
+        n = np.zeros(B, np.int32)
+        check(_lib.lib().sw_search_host(self._h, ptr(q), B, k, ptr(out), ptr(n)), "search_host")
+        return out, n
+
+    def plan(self, queries, reqs: np.ndarray, seed: int = 1, sel: SelectorConfig = None,
+             policy: Policy = None, stream=None, out=None):
+        torch = _torch()
+        sel = sel or SelectorConfig()
+        policy = policy or Policy()
+        q = self._dev(queries, np.float32)
+        r = self._dev(reqs.view(np.uint8) if isinstance(reqs, np.ndarray) else reqs, np.uint8)
+        B = q.shape[0]
+        if out is None:
+            out = torch.empty(B * CHOICE_DTYPE.itemsize, dtype=torch.uint8, device=q.device)
+        st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+        check(_lib.lib().sw_plan(self._h, ptr(q), ptr(r), B, seed, C.byref(sel.c()),
+                                 C.byref(policy.c()), ptr(out), st), "sw_plan")
+        return out
+
+    @staticmethod
+    def choices(buf) -> np.ndarray:
+        return buf.cpu().numpy().view(CHOICE_DTYPE)
+
+    def align_noise(self, choices_dev, reqs, t_out_max: int, eps=None, philox_seed: int = 0):
+        torch = _torch()
+        r = self._dev(reqs.view(np.uint8) if isinstance(reqs, np.ndarray) else reqs, np.uint8)
+        B = choices_dev.numel() // CHOICE_DTYPE.itemsize
+        C_, _, F = self.latent_shape
+        out = torch.zeros((B, C_, t_out_max, F), dtype=torch.float32, device=r.device)
+        e = None if eps is None else self._dev(eps, np.float32)
+        st = torch.cuda.current_stream(r.device).cuda_stream
+        check(_lib.lib().sw_align_noise(self._h, ptr(choices_dev), ptr(r), B, ptr(e),
+                                        philox_seed, ptr(out), t_out_max, st), "sw_align_noise")
+        return out
+
+    def warmstart_host(self, queries: np.ndarray, reqs: np.ndarray, d_out, t_out_max: int,
+                       seed: int = 1, sel: SelectorConfig = None, policy: Policy = None,
+                       philox_seed: int = 0, stream=None):
+        sel = sel or SelectorConfig()
+        policy = policy or Policy()
+        B = queries.shape[0]
+        ch = np.zeros(B, CHOICE_DTYPE)
+        check(_lib.lib().sw_warmstart_host(self._h, ptr(queries), ptr(reqs), B, seed,
+                                           C.byref(sel.c()), C.byref(policy.c()), philox_seed,
+                                           ptr(ch), ptr(d_out), t_out_max, stream),
+              "sw_warmstart_host")
+        return ch
+
+    # ------------------------------------------------------------------ component entry points
+    def score_select(self, sims, s_neg, durations, L, sel: SelectorConfig, rng_seed: int):
+        """score_candidates + select on one candidate set (selector.cpp:24-85)."""
+        sims = np.ascontiguousarray(sims, np.float64)
+        s_neg = np.ascontiguousarray(s_neg, np.float64)
+        dur = np.ascontiguousarray(durations, np.float64)
+        n = len(sims)
+        scores = np.zeros((n, 5), np.float64)
+        pick = np.zeros(2, np.int32)
+        check(_lib.lib().sw_score_select_host(self._h, n, ptr(sims), ptr(s_neg), ptr(dur), L,
+                                              C.byref(sel.c()), rng_seed, ptr(scores), ptr(pick)),
+              "score_select")
+        return scores, int(pick[0]), int(pick[1])
+
+    def gater(self, prompts, segs, T, explore: bool = False):
+        """context_features + choose_arm (gater.cpp:13-92) for B pairs."""
+        p = np.ascontiguousarray(prompts, np.float32).reshape(-1, self.dim)
+        s = np.ascontiguousarray(segs, np.float32).reshape(-1, self.dim)
+        T = np.ascontiguousarray(np.broadcast_to(T, (p.shape[0],)), np.int32)
+        B = p.shape[0]
+        phi = np.zeros((B, 11), np.float64)
+        arm = np.zeros(B, np.int32)
+        check(_lib.lib().sw_gater_host(self._h, ptr(p), ptr(s), ptr(T), B, int(explore),
+                                       ptr(phi), ptr(arm)), "gater")
+        return phi, arm
