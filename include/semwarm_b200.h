@@ -228,6 +228,21 @@ int sw_score_select_host(sw_ctx* ctx, int32_t n, const double* sims, const doubl
 /* context_features + choose_arm (gater.cpp:13-92) for B (prompt, segment) pairs. */
 int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const int32_t* T,
                   int32_t B, int32_t explore, double* phi_out, int32_t* arm_out);
+/* Stage profiling with CUDA events recorded on the launching stream around every kernel of the
+ * hot path (no host sync while enabled). Stages: SW_STAGE_*. sw_profile_read synchronizes the
+ * recorded events and returns the summed device time and launch count of one stage. */
+#define SW_STAGE_PREP 0
+#define SW_STAGE_SCORE_TC 1
+#define SW_STAGE_COMPACT 2
+#define SW_STAGE_RESCORE 3
+#define SW_STAGE_TOPK 4
+#define SW_STAGE_SELECT 5
+#define SW_STAGE_ALIGN 6
+#define SW_STAGE_MERGE 7
+#define SW_NUM_STAGES 8
+int sw_profile_enable(sw_ctx* ctx, int32_t on);
+int sw_profile_reset(sw_ctx* ctx);
+int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launches);
 /* Launch statistics of the last sw_plan/sw_search on this context (kernels launched, mode). */
 int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
                         int32_t* candidates_max);

@@ -66,6 +66,7 @@ static void free_ctx(Ctx& c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
+    for (cudaEvent_t e : c.prof_ev) cudaEventDestroy(e);
     if (c.mstream) cudaStreamDestroy(c.mstream);
 }
 
@@ -753,6 +754,51 @@ int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const in
         cudaFree(d_T);
         cudaFree(d_arm);
         cudaFree(d_phi);
+        return SW_OK;
+    });
+}
+
+int sw_profile_enable(sw_ctx* ctx, int32_t on) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        ctx->c.prof = on != 0;
+        return SW_OK;
+    });
+}
+
+static void prof_collect(Ctx& c) {
+    for (size_t i = 0; i < c.prof_used; ++i) {
+        SW_CUDA(cudaEventSynchronize(c.prof_ev[2 * i + 1]));
+        float ms = 0.0f;
+        SW_CUDA(cudaEventElapsedTime(&ms, c.prof_ev[2 * i], c.prof_ev[2 * i + 1]));
+        c.prof_ms[c.prof_stage[i]] += ms;
+        c.prof_n[c.prof_stage[i]] += 1;
+    }
+    c.prof_used = 0;
+}
+
+int sw_profile_reset(sw_ctx* ctx) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        SW_CUDA(cudaSetDevice(c.device));
+        prof_collect(c);
+        for (int s = 0; s < SW_NUM_STAGES; ++s) {
+            c.prof_ms[s] = 0.0;
+            c.prof_n[s] = 0;
+        }
+        return SW_OK;
+    });
+}
+
+int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launches) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && stage >= 0 && stage < SW_NUM_STAGES, "bad argument");
+        Ctx& c = ctx->c;
+        SW_CUDA(cudaSetDevice(c.device));
+        prof_collect(c);
+        if (total_ms) *total_ms = c.prof_ms[stage];
+        if (launches) *launches = c.prof_n[stage];
         return SW_OK;
     });
 }

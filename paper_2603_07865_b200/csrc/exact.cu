@@ -330,31 +330,46 @@ int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t
         SW_REQUIRE(c.high_water <= kCandCap,
                    "exact-only search is limited to 8192 slots; enable the tcgen05 path");
     }
-    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.thr, c.cand_n);
+    {
+        StageScope sc(c, SW_STAGE_PREP, st);
+        k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.thr, c.cand_n);
+    }
     ++kernels;
     int32_t* list = nullptr;
     int32_t* list_n = nullptr;
     int32_t* overflow = nullptr;
     if (tc) {
-        kernels += launch_score_tc(c, B, k, st);
+        {
+            StageScope sc(c, SW_STAGE_SCORE_TC, st);
+            kernels += launch_score_tc(c, B, k, st);
+        }
         list = c.cand_list;
         list_n = c.cand_n + c.Bmax;
         overflow = c.cand_n + 2 * c.Bmax;
-        k_compact<<<B, 256, 0, st>>>(k, c.cand_n, c.cand_slot, c.cand_score, c.q_norm,
-                                     c.maxnorm, 0.0081f, list, list_n, overflow);
+        {
+            StageScope sc(c, SW_STAGE_COMPACT, st);
+            k_compact<<<B, 256, 0, st>>>(k, c.cand_n, c.cand_slot, c.cand_score, c.q_norm,
+                                         c.maxnorm, 0.0081f, list, list_n, overflow);
+        }
         ++kernels;
     }
     const int implicit = tc ? 0 : 1;
     int gx = kRescoreBlocksPerQuery;
     if (implicit) gx = (int)std::max<int64_t>(1, (rows_hw + 127) / 128);
     dim3 g2(gx, B);
-    k_rescore<<<g2, 128, sizeof(float) * c.Df, st>>>(B, implicit, c.high_water, list, list_n, d_q,
-                                                     c.rows, c.nrows, c.valid, c.D, c.Df, c.Rp,
-                                                     c.logRp, c.cand_exact, c.cand_row);
+    {
+        StageScope sc(c, SW_STAGE_RESCORE, st);
+        k_rescore<<<g2, 128, sizeof(float) * c.Df, st>>>(B, implicit, c.high_water, list, list_n,
+                                                         d_q, c.rows, c.nrows, c.valid, c.D, c.Df,
+                                                         c.Rp, c.logRp, c.cand_exact, c.cand_row);
+    }
     ++kernels;
-    k_topk<<<B, 256, 0, st>>>(k, implicit, c.high_water, list, list_n, c.cand_exact, c.cand_row,
-                              c.ids, c.valid, c.nrows, c.segs, c.sneg, c.rows, d_q, c.D, c.Df,
-                              c.Rp, rank, overflow, c.hits, c.nhits);
+    {
+        StageScope sc(c, SW_STAGE_TOPK, st);
+        k_topk<<<B, 256, 0, st>>>(k, implicit, c.high_water, list, list_n, c.cand_exact,
+                                  c.cand_row, c.ids, c.valid, c.nrows, c.segs, c.sneg, c.rows, d_q,
+                                  c.D, c.Df, c.Rp, rank, overflow, c.hits, c.nhits);
+    }
     ++kernels;
     SW_CUDA(cudaGetLastError());
     c.last_tc = tc ? 1 : 0;

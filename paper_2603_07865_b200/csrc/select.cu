@@ -319,6 +319,7 @@ void launch_select(Ctx& c, const HitRec* d_hits, const int32_t* d_nh, int ld, co
     p.psi = c.psi;
     p.fd = c.fd;
     p.beta = c.beta;
+    StageScope sc(c, SW_STAGE_SELECT, st);
     k_select<<<(B + 63) / 64, 64, 0, st>>>(B, d_hits, d_nh, ld, d_req, p, d_out);
     SW_CUDA(cudaGetLastError());
 }
@@ -327,6 +328,7 @@ void launch_merge(Ctx& c, const HitRec* d_gathered, const int32_t* d_gn, int wor
                   cudaStream_t st) {
     SW_REQUIRE(world >= 1 && world <= 16, "world size must be in [1, 16]");
     if (B == 0) return;
+    StageScope sc(c, SW_STAGE_MERGE, st);
     k_merge<<<(B + 127) / 128, 128, 0, st>>>(B, k, world, d_gathered, d_gn, c.hits, c.nhits);
     SW_CUDA(cudaGetLastError());
 }

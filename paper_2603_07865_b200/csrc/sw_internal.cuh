@@ -142,8 +142,39 @@ struct Ctx {
     mutable std::shared_mutex mu;
 
     cudaStream_t mstream = nullptr;   // mutation stream
+    // stage profiling (CUDA events on the launching stream; single-threaded use)
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_ev;   // pool, pairs (start, stop)
+    std::vector<int> prof_stage;        // stage of each recorded pair
+    size_t prof_used = 0;
+    double prof_ms[SW_NUM_STAGES] = {};
+    int64_t prof_n[SW_NUM_STAGES] = {};
     // last launch info
     int last_kernels = 0, last_tc = 0, last_cand_max = 0;
+};
+
+// RAII stage timer: records a (start, stop) event pair around the enclosed launches.
+struct StageScope {
+    Ctx& c;
+    cudaStream_t st;
+    size_t pair = (size_t)-1;
+    StageScope(Ctx& cc, int stage, cudaStream_t s) : c(cc), st(s) {
+        if (!c.prof) return;
+        if (2 * (c.prof_used + 1) > c.prof_ev.size()) {
+            for (int i = 0; i < 2; ++i) {
+                cudaEvent_t e;
+                if (cudaEventCreate(&e) != cudaSuccess) return;
+                c.prof_ev.push_back(e);
+            }
+            c.prof_stage.push_back(0);
+        }
+        pair = c.prof_used++;
+        c.prof_stage[pair] = stage;
+        cudaEventRecord(c.prof_ev[2 * pair], st);
+    }
+    ~StageScope() {
+        if (pair != (size_t)-1) cudaEventRecord(c.prof_ev[2 * pair + 1], st);
+    }
 };
 
 // kernel-side launchers (implemented in the .cu files)

@@ -172,6 +172,20 @@ class WarmStartCache:
         n = check(_lib.lib().sw_arena_read_rows(self._h, entry_id, ptr(out), cap), "read_rows")
         return out[:n]
 
+    def profile(self, on: bool = True):
+        check(_lib.lib().sw_profile_enable(self._h, int(on)), "profile")
+
+    def profile_reset(self):
+        check(_lib.lib().sw_profile_reset(self._h), "profile_reset")
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(_lib.STAGES):
+            ms, n = C.c_double(), C.c_int64()
+            check(_lib.lib().sw_profile_read(self._h, i, C.byref(ms), C.byref(n)), "profile_read")
+            out[name] = (ms.value, n.value)
+        return out
+
     def launch_info(self):
         k, t, m = C.c_int32(), C.c_int32(), C.c_int32()
         _lib.lib().sw_last_launch_info(self._h, C.byref(k), C.byref(t), C.byref(m))
