@@ -267,7 +267,7 @@ void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, 
                            double delta, cudaStream_t st) {
     (void)delta;
     const int R = c.R;
-    const int64_t chunk = 65536;
+    const int64_t chunk = 32768;  // grid.y of the latent fill must stay <= 65535
     float* stage = nullptr;
     sw_segment* segs = nullptr;
     uint64_t* ids = nullptr;

@@ -49,45 +49,47 @@ struct TcParams {
     float eps_rel;
 };
 
-template <int RP>
-__device__ __forceinline__ void rare_path(const float (&v)[32], int c, int64_t tile, float& theta,
-                                          float (&list)[32], float& kth, float eps2, int q,
-                                          const TcParams& p) {
+// Emission + running top-list update for the entries of one 32-column chunk whose approximate
+// score reaches theta. `mask` has one bit per entry; the loop runs once per set bit (usually 0 or
+// 1), so a warp whose lanes rarely emit does not execute a 32x-unrolled body.
+template <int RP, int KL>
+__device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t mask, int c,
+                                           int64_t tile, float& theta, float (&list)[KL],
+                                           float& kth, float eps2, int q, const TcParams& p) {
     constexpr int E = 32 / RP;
+    while (mask) {
+        const int e = __ffs(mask) - 1;
+        mask &= mask - 1;
+        // em[e] through a binary mux tree (a dynamic register index would spill to local)
+        float t[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        float m = v[e * RP];
+        for (int j = 0; j < E; ++j) t[j] = em[j];
 #pragma unroll
-        for (int j = 1; j < RP; ++j) m = fmaxf(m, v[e * RP + j]);
-        m = fminf(1.0f, fmaxf(-1.0f, m));  // clamped like cosine_similarity (core.cpp:35-36)
-        if (m >= theta) {
-            const int64_t slot = (tile * BN + c * 32 + e * RP) / RP;
-            if (slot < p.n_slots && p.valid[slot]) {
-                int idx = atomicAdd(&p.cand_n[q], 1);
-                if (idx < kCandCap) {
-                    p.cand_slot[(int64_t)q * kCandCap + idx] = (int32_t)slot;
-                    p.cand_score[(int64_t)q * kCandCap + idx] = m;
-                }
-                // sorted insertion into the running list (descending)
-                float x = m;
+        for (int w = E / 2, b = 1; w >= 1; w >>= 1, b <<= 1)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float hi = fmaxf(list[i], x);
-                    x = fminf(list[i], x);
-                    list[i] = hi;
-                }
-                float kk = list[0];
-#pragma unroll
-                for (int i = 1; i < 32; ++i)
-                    if (i == p.k - 1) kk = list[i];
-                kth = kk;
-                theta = fmaxf(theta, kth - eps2);
-            }
+            for (int j = 0; j < w; ++j) t[j] = (e & b) ? t[2 * j + 1] : t[2 * j];
+        const float m = t[0];
+        if (m < theta) continue;  // theta may have risen within this chunk
+        const int64_t slot = (tile * BN + c * 32) / RP + e;
+        if (slot >= p.n_slots || !p.valid[slot]) continue;
+        const int idx = atomicAdd(&p.cand_n[q], 1);
+        if (idx < kCandCap) {
+            p.cand_slot[(int64_t)q * kCandCap + idx] = (int32_t)slot;
+            p.cand_score[(int64_t)q * kCandCap + idx] = m;
         }
+        float x = m;  // sorted insertion (descending)
+#pragma unroll
+        for (int i = 0; i < KL; ++i) {
+            const float hi = fmaxf(list[i], x);
+            x = fminf(list[i], x);
+            list[i] = hi;
+        }
+        kth = list[KL - 1];  // slots above the k real ones hold +inf (see init)
+        theta = fmaxf(theta, kth - eps2);
     }
 }
 
-template <int RP>
+template <int RP, int KL>
 __global__ void __launch_bounds__(THREADS, 1)
     k_score_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmE,
                const TcParams p) {
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kc = 0; kc < p.kch; ++kc, ++it) {
                     const int s = (int)(it % S);
                     const uint32_t ph = (it / S) & 1u;
-                    ptx::mbar_wait(bar(EMPTY + s), ph ^ 1u);
+                    ptx::mbar_wait_sleep(bar(EMPTY + s), ph ^ 1u);
                     ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
                     ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
                                      kc * 64, (int32_t)(tile * BN));
@@ -166,13 +168,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int lt = 0; lt < ntiles; ++lt) {
                 const int acc = lt & 1;
                 const uint32_t aph = (lt >> 1) & 1u;
-                ptx::mbar_wait(bar(TEMPTY + acc), aph ^ 1u);
+                ptx::mbar_wait_sleep(bar(TEMPTY + acc), aph ^ 1u);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kc = 0; kc < p.kch; ++kc, ++it) {
                     const int s = (int)(it % S);
                     const uint32_t ph = (it / S) & 1u;
-                    ptx::mbar_wait(bar(FULL + s), ph);
+                    ptx::mbar_wait_sleep(bar(FULL + s), ph);
                     ptx::tc_fence_after();
                     const uint32_t a0 = ptx::smem_u32(sA + kc * A_CHUNK);
                     const uint32_t b0 = ptx::smem_u32(sB + s * B_STAGE);
@@ -195,9 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         float eps2 = 0.0f;
         if (qvalid) eps2 = 2.0f * p.eps_rel * p.q_norm[q] * ord2f(*p.maxnorm);
         float theta = -INFINITY, kth = -INFINITY, published = -INFINITY;
-        float list[32];
+        // descending list; the top KL - k slots are +inf so list[KL-1] is always the k-th best
+        float list[KL];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) list[i] = -INFINITY;
+        for (int i = 0; i < KL; ++i) list[i] = (i < KL - p.k) ? INFINITY : -INFINITY;
         const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
 
         for (int lt = 0; lt < ntiles; ++lt) {
@@ -215,14 +218,31 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                 ptx::tmem_ld_wait();
-                float v[32];
+                // per-entry max over the entry's RP pyramid rows (adjacent columns), clamped
+                // to [-1, 1] like cosine_similarity (core.cpp:35-36)
+                constexpr int E = 32 / RP;
+                float em[E];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                float m = v[0];
+                for (int e = 0; e < E; ++e) {
+                    float m = __uint_as_float(r[e * RP]);
 #pragma unroll
-                for (int j = 1; j < 32; ++j) m = fmaxf(m, v[j]);
-                if (qvalid && fminf(1.0f, m) >= theta)
-                    rare_path<RP>(v, c, tile, theta, list, kth, eps2, q, p);
+                    for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[e * RP + j]));
+                    em[e] = fminf(1.0f, fmaxf(-1.0f, m));
+                }
+                // tree max (short dependency chain), then a bitmask only when needed
+                float t[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) t[e] = em[e];
+#pragma unroll
+                for (int w = E / 2; w >= 1; w >>= 1)
+#pragma unroll
+                    for (int e = 0; e < w; ++e) t[e] = fmaxf(t[e], t[e + w]);
+                if (qvalid && t[0] >= theta) {
+                    uint32_t mask = 0;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) mask |= (em[e] >= theta ? 1u : 0u) << e;
+                    emit_chunk<RP, KL>(em, mask, c, tile, theta, list, kth, eps2, q, p);
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -273,15 +293,23 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32
     return r == CUDA_SUCCESS;
 }
 
-template <int RP>
-void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+template <int RP, int KL>
+void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        SW_CUDA(cudaFuncSetAttribute(k_score_tc<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     c.smem_optin));
+        SW_CUDA(cudaFuncSetAttribute(k_score_tc<RP, KL>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem_optin));
         attr_set = true;
     }
-    k_score_tc<RP><<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+    k_score_tc<RP, KL><<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+}
+
+template <int RP>
+void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+    if (p.k <= 8)
+        launch_tc_kl<RP, 8>(c, p, grid, smem, st);
+    else
+        launch_tc_kl<RP, 32>(c, p, grid, smem, st);
 }
 
 }  // namespace
