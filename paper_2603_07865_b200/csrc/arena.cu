@@ -41,7 +41,8 @@ __global__ void k_insert_rows(int64_t n, const int64_t* __restrict__ slot_of,
                               float* __restrict__ rows, __nv_bfloat16* __restrict__ rows_bf,
                               double* __restrict__ sneg, sw_segment* __restrict__ segs,
                               uint64_t* __restrict__ slot_ids, int32_t* __restrict__ slot_nrows,
-                              uint8_t* __restrict__ valid, uint32_t* __restrict__ maxnorm,
+                              uint8_t* __restrict__ valid, uint32_t* __restrict__ valid_bits,
+                              uint32_t* __restrict__ maxnorm,
                               const float* __restrict__ neg, int have_neg, int D, int Df, int Dp,
                               int Rp) {
     int64_t e = blockIdx.x;
@@ -84,7 +85,14 @@ __global__ void k_insert_rows(int64_t n, const int64_t* __restrict__ slot_of,
         slot_ids[slot] = ids[e];
         slot_nrows[slot] = total;
         valid[slot] = 1;
+        atomicOr(&valid_bits[slot >> 5], 1u << (slot & 31));
     }
+}
+
+__global__ void k_clear_slot(int64_t slot, uint8_t* valid, uint32_t* valid_bits, int32_t* nrows) {
+    valid[slot] = 0;
+    nrows[slot] = 0;
+    atomicAnd(&valid_bits[slot >> 5], ~(1u << (slot & 31)));
 }
 
 __global__ void k_copy_latents(int64_t n, const int64_t* __restrict__ slot_of,
@@ -237,8 +245,13 @@ void launch_insert_rows_full(Ctx& c, int64_t n, const int64_t* d_slot, const int
         k_insert_rows<<<(unsigned)m, 128, 0, st>>>(
             m, d_slot + off, d_base ? d_base + off : nullptr, d_row_off + off, d_ids + off,
             d_rows, d_segs, c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid,
-            c.maxnorm, c.neg, c.have_neg ? 1 : 0, c.D, c.Df, c.Dp, c.Rp);
+            c.valid_bits, c.maxnorm, c.neg, c.have_neg ? 1 : 0, c.D, c.Df, c.Dp, c.Rp);
     }
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_clear_slot(Ctx& c, int64_t slot, cudaStream_t st) {
+    k_clear_slot<<<1, 1, 0, st>>>(slot, c.valid, c.valid_bits, c.nrows);
     SW_CUDA(cudaGetLastError());
 }
 

@@ -59,7 +59,8 @@ static void default_schedule(std::vector<double>& abar) {
 }
 
 static void free_ctx(Ctx& c) {
-    void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.tsrc,
+    void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
+                    c.slice_cnt, c.tsrc,
                     c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
                     c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
@@ -104,6 +105,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.ids, (size_t)c.S);
     dalloc(&c.nrows, (size_t)c.S);
     dalloc(&c.valid, (size_t)c.S);
+    dalloc(&c.valid_bits, (size_t)(c.S / 32 + 16));
     dalloc(&c.tsrc, (size_t)c.S);
     if (c.C > 0 && c.Tmax > 0 && c.F > 0)
         dalloc(&c.latent, (size_t)c.Lslots * c.C * c.Tmax * c.F);
@@ -115,6 +117,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.q_norm, (size_t)c.Bmax);
     dalloc(&c.thr, (size_t)c.Bmax);
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
+    dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_exact, (size_t)c.Bmax * kCandCap);
@@ -127,6 +130,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.d_choice_stage, (size_t)c.Bmax);
     SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
     SW_CUDA(cudaMemsetAsync(c.valid, 0, (size_t)c.S, c.mstream));
+    SW_CUDA(cudaMemsetAsync(c.valid_bits, 0, sizeof(uint32_t) * (size_t)(c.S / 32 + 16), c.mstream));
     SW_CUDA(cudaMemsetAsync(c.nrows, 0, sizeof(int32_t) * (size_t)c.S, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.tsrc, 0, sizeof(int32_t) * (size_t)c.S, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.rows_bf, 0, sizeof(__nv_bfloat16) * (size_t)nrow * c.Dp, c.mstream));
@@ -286,10 +290,7 @@ static void do_remove(Ctx& c, uint64_t id, bool* found) {
     const int64_t s = it->second;
     c.slot_of.erase(it);
     c.h_nrows[(size_t)s] = 0;
-    const uint8_t z = 0;
-    const int32_t zi = 0;
-    SW_CUDA(cudaMemcpyAsync(c.valid + s, &z, 1, cudaMemcpyHostToDevice, c.mstream));
-    SW_CUDA(cudaMemcpyAsync(c.nrows + s, &zi, 4, cudaMemcpyHostToDevice, c.mstream));
+    launch_clear_slot(c, s, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
     if (s == c.high_water - 1) {
         --c.high_water;

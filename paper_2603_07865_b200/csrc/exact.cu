@@ -51,19 +51,57 @@ __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
     }
 }
 
-// Block-wide k-th largest of n floats by k rounds of argmax with exclusion.
-__device__ float block_kth(const float* __restrict__ v, int n, int k, unsigned long long* sh) {
+// Gathers the per-(query, CTA) emission slices of the tcgen05 pass into shared memory, finds
+// T_a = the k-th best approximate entry score among them (k rounds of block argmax with
+// exclusion) and keeps the certified candidates approx >= T_a - 2 eps_q.
+__global__ void k_compact(int k, int n_chunks, int cap_local, const int32_t* __restrict__ slice_cnt,
+                          const int32_t* __restrict__ cand_slot, const float* __restrict__ cand_score,
+                          const float* __restrict__ q_norm, const uint32_t* __restrict__ maxnorm,
+                          float eps_rel, int32_t* __restrict__ out_slot, int32_t* __restrict__ out_n,
+                          int32_t* __restrict__ overflow) {
+    extern __shared__ uint8_t sm_raw[];
+    float* sc = reinterpret_cast<float*>(sm_raw);                 // [kCandCap]
+    int32_t* sl = reinterpret_cast<int32_t*>(sc + kCandCap);      // [kCandCap]
+    __shared__ int off[149];
+    __shared__ unsigned long long sh[33];
+    __shared__ int cnt;
+    __shared__ int ovf;
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        int o = 0, f = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            const int n = slice_cnt[(int64_t)b * n_chunks + c];
+            off[c] = o;
+            o += min(n, cap_local);
+            f |= n > cap_local;
+        }
+        off[n_chunks] = o;
+        ovf = f;
+        cnt = 0;
+    }
+    __syncthreads();
+    const int n = off[n_chunks];
+    for (int c = 0; c < n_chunks; ++c) {
+        const int m = off[c + 1] - off[c];
+        const int64_t src = (int64_t)b * kCandCap + (int64_t)c * cap_local;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            sc[off[c] + i] = cand_score[src + i];
+            sl[off[c] + i] = cand_slot[src + i];
+        }
+    }
+    __syncthreads();
+    // k-th largest (ties broken by position so every round removes exactly one element)
     unsigned long long prev = ~0ull;
     float kth = -INFINITY;
     for (int r = 0; r < k; ++r) {
         unsigned long long best = 0;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            unsigned long long key =
-                ((unsigned long long)f2ord(v[i]) << 32) | (0xFFFFFFFFu - (uint32_t)i);
+            const unsigned long long key =
+                ((unsigned long long)f2ord(sc[i]) << 32) | (0xFFFFFFFFu - (uint32_t)i);
             if (key < prev && key > best) best = key;
         }
         for (int o = 16; o; o >>= 1) {
-            unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
             best = x > best ? x : best;
         }
         if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
@@ -76,40 +114,25 @@ __device__ float block_kth(const float* __restrict__ v, int n, int k, unsigned l
         __syncthreads();
         best = sh[32];
         __syncthreads();
-        if (best == 0) return -INFINITY;  // fewer than k candidates
+        if (best == 0) {  // fewer than k candidates: keep everything
+            kth = -INFINITY;
+            break;
+        }
         prev = best;
         kth = ord2f((uint32_t)(best >> 32));
     }
-    return kth;
-}
-
-__global__ void k_compact(int k, const int32_t* __restrict__ cand_n_in,
-                          const int32_t* __restrict__ cand_slot, const float* __restrict__ cand_score,
-                          const float* __restrict__ q_norm, const uint32_t* __restrict__ maxnorm,
-                          float eps_rel, int32_t* __restrict__ out_slot, int32_t* __restrict__ out_n,
-                          int32_t* __restrict__ overflow) {
-    const int b = blockIdx.x;
-    __shared__ unsigned long long sh[33];
-    __shared__ int cnt;
-    const int n_raw = cand_n_in[b];
-    const int n = min(n_raw, kCandCap);
-    const float* sc = cand_score + (int64_t)b * kCandCap;
-    const int32_t* sl = cand_slot + (int64_t)b * kCandCap;
     const float eps2 = 2.0f * eps_rel * q_norm[b] * ord2f(*maxnorm);
-    float kth = block_kth(sc, n, k, sh);
-    const float cut = kth - eps2;  // -inf when fewer than k candidates
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
+    const float cut = kth - eps2;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         if (sc[i] >= cut) {
-            int j = atomicAdd(&cnt, 1);
+            const int j = atomicAdd(&cnt, 1);
             out_slot[(int64_t)b * kCandCap + j] = sl[i];
         }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         out_n[b] = cnt;
-        overflow[b] = n_raw > kCandCap ? 1 : 0;
+        overflow[b] = ovf;
     }
 }
 
@@ -348,8 +371,16 @@ int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t
         overflow = c.cand_n + 2 * c.Bmax;
         {
             StageScope sc(c, SW_STAGE_COMPACT, st);
-            k_compact<<<B, 256, 0, st>>>(k, c.cand_n, c.cand_slot, c.cand_score, c.q_norm,
-                                         c.maxnorm, 0.0081f, list, list_n, overflow);
+            static bool attr = false;
+            const size_t smem = (size_t)kCandCap * 8;
+            if (!attr) {
+                SW_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                attr = true;
+            }
+            k_compact<<<B, 256, smem, st>>>(k, c.last_chunks, kCandCap / c.last_chunks,
+                                            c.slice_cnt, c.cand_slot, c.cand_score, c.q_norm,
+                                            c.maxnorm, 0.0081f, list, list_n, overflow);
         }
         ++kernels;
     }

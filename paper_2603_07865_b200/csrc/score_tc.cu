@@ -39,23 +39,27 @@ struct TcParams {
     int64_t n_tiles;
     int64_t tiles_per_cta;
     int64_t n_slots;  // high-water slot count
-    const uint8_t* valid;
+    const uint32_t* valid_bits;  // one bit per slot
     const float* q_norm;
     const uint32_t* maxnorm;
     uint32_t* thr;
-    int32_t* cand_n;
-    int32_t* cand_slot;
+    int32_t* slice_cnt;  // [B][n_chunks] emissions per (query, CTA)
+    int32_t* cand_slot;  // [B][kCandCap], CTA y owns [y * cap_local, (y + 1) * cap_local)
     float* cand_score;
+    int n_chunks;
+    int cap_local;
     float eps_rel;
 };
 
 // Emission + running top-list update for the entries of one 32-column chunk whose approximate
-// score reaches theta. `mask` has one bit per entry; the loop runs once per set bit (usually 0 or
-// 1), so a warp whose lanes rarely emit does not execute a 32x-unrolled body.
+// score reaches theta. `mask` has one bit per (valid) entry; the loop runs once per set bit
+// (usually 0 or 1). Emissions go to this (query, CTA)'s private slice with a register counter:
+// no atomics and no loads on the emission path.
 template <int RP, int KL>
-__device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t mask, int c,
-                                           int64_t tile, float& theta, float (&list)[KL],
-                                           float& kth, float eps2, int q, const TcParams& p) {
+__device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t mask,
+                                           int64_t slot_c, float& theta, float (&list)[KL],
+                                           float& kth, float eps2, int& cnt, int64_t slice,
+                                           const TcParams& p) {
     constexpr int E = 32 / RP;
     while (mask) {
         const int e = __ffs(mask) - 1;
@@ -70,13 +74,11 @@ __device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t 
             for (int j = 0; j < w; ++j) t[j] = (e & b) ? t[2 * j + 1] : t[2 * j];
         const float m = t[0];
         if (m < theta) continue;  // theta may have risen within this chunk
-        const int64_t slot = (tile * BN + c * 32) / RP + e;
-        if (slot >= p.n_slots || !p.valid[slot]) continue;
-        const int idx = atomicAdd(&p.cand_n[q], 1);
-        if (idx < kCandCap) {
-            p.cand_slot[(int64_t)q * kCandCap + idx] = (int32_t)slot;
-            p.cand_score[(int64_t)q * kCandCap + idx] = m;
+        if (cnt < p.cap_local) {
+            p.cand_slot[slice + cnt] = (int32_t)(slot_c + e);
+            p.cand_score[slice + cnt] = m;
         }
+        ++cnt;
         float x = m;  // sorted insertion (descending)
 #pragma unroll
         for (int i = 0; i < KL; ++i) {
@@ -191,6 +193,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
     } else {
         // ---------------- epilogue: TMEM lane == query
+        constexpr int E = 32 / RP;          // entries per 32-column chunk
+        constexpr int SPT = BN / RP;        // slots per tile
+        constexpr int NW = SPT >= 32 ? SPT / 32 : 1;
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int q = qblock * BM + quarter * 32 + lane;
         const bool qvalid = q < p.B;
@@ -202,25 +207,33 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int i = 0; i < KL; ++i) list[i] = (i < KL - p.k) ? INFINITY : -INFINITY;
         const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+        const int64_t slice = (int64_t)q * kCandCap + (int64_t)blockIdx.y * p.cap_local;
+        int cnt = 0;
+        uint32_t g_next = qvalid ? __ldcg(&p.thr[q]) : 0u;  // shared k-th best, one tile ahead
 
         for (int lt = 0; lt < ntiles; ++lt) {
             const int acc = lt & 1;
             const uint32_t aph = (lt >> 1) & 1u;
             const int64_t tile = t0 + lt;
             if (qvalid) {
-                float g = ord2f(__ldcg(&p.thr[q]));
-                theta = fmaxf(theta, g - eps2);
+                theta = fmaxf(theta, ord2f(g_next) - eps2);
+                g_next = __ldcg(&p.thr[q]);
             }
+            // validity bits of this tile's slots, fetched before waiting on the accumulator
+            const int64_t slot0 = tile * SPT;
+            const int boff = (int)(slot0 & 31);
+            uint32_t vw[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) vw[w] = __ldg(p.valid_bits + (slot0 >> 5) + w);
             ptx::mbar_wait(bar(TFULL + acc), aph);
             ptx::tc_fence_after();
-#pragma unroll 1
+#pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                 ptx::tmem_ld_wait();
                 // per-entry max over the entry's RP pyramid rows (adjacent columns), clamped
                 // to [-1, 1] like cosine_similarity (core.cpp:35-36)
-                constexpr int E = 32 / RP;
                 float em[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -241,7 +254,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                     uint32_t mask = 0;
 #pragma unroll
                     for (int e = 0; e < E; ++e) mask |= (em[e] >= theta ? 1u : 0u) << e;
-                    emit_chunk<RP, KL>(em, mask, c, tile, theta, list, kth, eps2, q, p);
+                    const int bb = boff + c * E;
+                    uint32_t vbits = (NW > 1 ? vw[(c * E) >> 5] : vw[0]) >> (bb & 31);
+                    if (E < 32) vbits &= (1u << E) - 1u;
+                    mask &= vbits;
+                    if (mask)
+                        emit_chunk<RP, KL>(em, mask, slot0 + c * E, theta, list, kth, eps2, cnt,
+                                           slice, p);
                 }
             }
             ptx::tc_fence_before();
@@ -252,6 +271,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 published = kth;
             }
         }
+        if (qvalid) p.slice_cnt[(int64_t)q * p.n_chunks + blockIdx.y] = cnt;
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -323,6 +343,7 @@ bool encode_tensor_maps(Ctx& c) {
 
 // Returns the number of kernels launched (1).
 int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
+    // grid: x = 128-query block, y = contiguous range of 256-row tiles (<= 148 CTAs per block row)
     TcParams p{};
     p.B = B;
     p.kch = c.Dp / 64;
@@ -338,13 +359,16 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.tiles_per_cta = (p.n_tiles + chunks - 1) / chunks;
     chunks = (p.n_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
     p.n_slots = c.high_water;
-    p.valid = c.valid;
+    p.valid_bits = c.valid_bits;
     p.q_norm = c.q_norm;
     p.maxnorm = c.maxnorm;
     p.thr = c.thr;
-    p.cand_n = c.cand_n;
+    p.slice_cnt = c.slice_cnt;
     p.cand_slot = c.cand_slot;
     p.cand_score = c.cand_score;
+    p.n_chunks = (int)chunks;
+    p.cap_local = kCandCap / (int)chunks;
+    c.last_chunks = (int)chunks;
     // |bf16 dot - exact| <= (2u + u^2) |q||e| + fp32 accumulation slack; u = 2^-8
     p.eps_rel = 0.0081f;
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;

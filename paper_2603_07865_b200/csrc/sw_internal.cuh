@@ -41,7 +41,7 @@ void set_last_error(const std::string& msg);
 constexpr int kNumArms = 14;          // gater.hpp:13
 constexpr int kFeatureDim = 11;       // gater.hpp:28
 constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep running list
-constexpr int kCandCap = 8192;        // certified candidates per query
+constexpr int kCandCap = 16384;       // emitted candidates per query (split over the CTAs)
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
 
 // Per-shard top-k record (SW_HIT_RECORD_BYTES = 128): everything the replicated select /
@@ -98,6 +98,7 @@ struct Ctx {
     uint64_t* ids = nullptr;          // [S]
     int32_t* nrows = nullptr;         // [S]
     uint8_t* valid = nullptr;         // [S]
+    uint32_t* valid_bits = nullptr;   // [S/32 + pad] one bit per slot (read by the tcgen05 epilogue)
     int32_t* tsrc = nullptr;          // [S]
     float* latent = nullptr;          // [Lslots][C][Tmax][F]
     uint32_t* maxnorm = nullptr;      // ordered float bits, max row L2 norm
@@ -114,7 +115,9 @@ struct Ctx {
     __nv_bfloat16* q_bf = nullptr;  // [BmaxPad][Dp]
     float* q_norm = nullptr;        // [Bmax]
     uint32_t* thr = nullptr;        // [Bmax] shared running k-th best (ordered)
-    int32_t* cand_n = nullptr;      // [3][Bmax]: raw count | compacted count | overflow flag
+    int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
+    int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)
+    int last_chunks = 1;
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
     double* cand_exact = nullptr;   // [Bmax][kCandCap]
@@ -184,6 +187,7 @@ void launch_insert_rows_full(Ctx& c, int64_t n, const int64_t* d_slot, const int
 void launch_copy_latents(Ctx& c, int64_t n, const int64_t* d_slot, const float* d_lat,
                          const int64_t* d_lat_off, const int32_t* d_tsrc, cudaStream_t st);
 void launch_recompute_sneg(Ctx& c, cudaStream_t st);
+void launch_clear_slot(Ctx& c, int64_t slot, cudaStream_t st);
 void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, uint64_t seed,
                            double delta, cudaStream_t st);
 
