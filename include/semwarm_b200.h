@@ -231,15 +231,13 @@ int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const in
 /* Stage profiling with CUDA events recorded on the launching stream around every kernel of the
  * hot path (no host sync while enabled). Stages: SW_STAGE_*. sw_profile_read synchronizes the
  * recorded events and returns the summed device time and launch count of one stage. */
-#define SW_STAGE_PREP 0
-#define SW_STAGE_SCORE_TC 1
-#define SW_STAGE_COMPACT 2
-#define SW_STAGE_RESCORE 3
-#define SW_STAGE_TOPK 4
-#define SW_STAGE_SELECT 5
-#define SW_STAGE_ALIGN 6
-#define SW_STAGE_MERGE 7
-#define SW_NUM_STAGES 8
+#define SW_STAGE_PREP 0      /* queries -> bf16, |q| */
+#define SW_STAGE_SCORE_TC 1  /* tcgen05 scoring + certified candidate emission */
+#define SW_STAGE_FINISH 2    /* candidate filter + fp64 rescoring + top-k (+ select) */
+#define SW_STAGE_SELECT 3    /* standalone select (multi-GPU merge path) */
+#define SW_STAGE_ALIGN 4     /* align + noise */
+#define SW_STAGE_MERGE 5     /* multi-GPU record merge */
+#define SW_NUM_STAGES 6
 int sw_profile_enable(sw_ctx* ctx, int32_t on);
 int sw_profile_reset(sw_ctx* ctx);
 int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launches);

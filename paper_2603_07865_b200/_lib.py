@@ -137,7 +137,7 @@ EXPORTED = [
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read",
 ]
-STAGES = ["prep", "score_tc", "compact", "rescore", "topk", "select", "align", "merge"]
+STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 
 
 def check(rc: int, what: str = "") -> int:

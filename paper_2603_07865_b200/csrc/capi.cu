@@ -4,7 +4,7 @@
 #include <cmath>
 #include <cstring>
 
-#include "sw_internal.cuh"
+#include "select_dev.cuh"
 
 struct sw_ctx {
     sw::Ctx c;
@@ -60,7 +60,7 @@ static void default_schedule(std::vector<double>& abar) {
 
 static void free_ctx(Ctx& c) {
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
-                    c.slice_cnt, c.tsrc,
+                    c.slice_cnt, c.cta_topk, c.tsrc,
                     c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
                     c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
@@ -118,6 +118,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.thr, (size_t)c.Bmax);
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
     dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
+    dalloc(&c.cta_topk, (size_t)c.Bmax * 148 * kMaxTopK);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_exact, (size_t)c.Bmax * kCandCap);
@@ -570,9 +571,8 @@ static int plan_impl(Ctx& c, const float* d_q, const sw_request* d_req, int B, u
                      const sw_selector_config* sel, const sw_policy* pol, sw_choice* d_out,
                      cudaStream_t st) {
     check_sel(sel, pol);
-    int kn = launch_search(c, d_q, B, sel->top_k, 0, st);
-    launch_select(c, c.hits, c.nhits, kMaxTopK, d_q, d_req, B, seed, *sel, *pol, d_out, 0, st);
-    return kn + 1;
+    const dev::SelParams sp = dev::make_sel_params(c, seed, *sel, *pol);
+    return launch_search_fused(c, d_q, B, sel->top_k, 0, d_req, &sp, d_out, st);
 }
 
 int sw_plan(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, uint64_t seed,

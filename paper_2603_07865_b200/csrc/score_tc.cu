@@ -44,6 +44,7 @@ struct TcParams {
     const uint32_t* maxnorm;
     uint32_t* thr;
     int32_t* slice_cnt;  // [B][n_chunks] emissions per (query, CTA)
+    float* cta_topk;     // [B][n_chunks][32] final running lists
     int32_t* cand_slot;  // [B][kCandCap], CTA y owns [y * cap_local, (y + 1) * cap_local)
     float* cand_score;
     int n_chunks;
@@ -271,7 +272,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 published = kth;
             }
         }
-        if (qvalid) p.slice_cnt[(int64_t)q * p.n_chunks + blockIdx.y] = cnt;
+        if (qvalid) {
+            p.slice_cnt[(int64_t)q * p.n_chunks + blockIdx.y] = cnt;
+            // this CTA's exact local top-k (every entry below it was below the running k-th)
+            float* tk = p.cta_topk + ((int64_t)q * p.n_chunks + blockIdx.y) * kMaxTopK;
+#pragma unroll
+            for (int i = 0; i < KL; ++i)
+                if (i >= KL - p.k) tk[i - (KL - p.k)] = list[i];
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -364,13 +372,13 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.maxnorm = c.maxnorm;
     p.thr = c.thr;
     p.slice_cnt = c.slice_cnt;
+    p.cta_topk = c.cta_topk;
     p.cand_slot = c.cand_slot;
     p.cand_score = c.cand_score;
     p.n_chunks = (int)chunks;
     p.cap_local = kCandCap / (int)chunks;
     c.last_chunks = (int)chunks;
-    // |bf16 dot - exact| <= (2u + u^2) |q||e| + fp32 accumulation slack; u = 2^-8
-    p.eps_rel = 0.0081f;
+    p.eps_rel = kEpsRel;
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;
     dim3 grid((unsigned)qblocks, (unsigned)chunks);
     switch (c.Rp) {

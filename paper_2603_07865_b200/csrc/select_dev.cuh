@@ -1,0 +1,219 @@
+// Device-side restatement of score_candidates + select + context_features + choose_arm + t*,
+// shared by the per-request select kernel and the fused per-query finish kernel.
+// See select.cu for the parity notes (fp64 operation order, unfused products, exp() slack).
+#pragma once
+#include "sw_internal.cuh"
+
+namespace sw {
+namespace dev {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // core.cpp:58-63
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b,
+                                                uint64_t c) {  // core.cpp:65-71
+    uint64_t s = splitmix64(base ^ 0x53454d5741524dULL);
+    s = splitmix64(s ^ a);
+    s = splitmix64(s ^ b);
+    return splitmix64(s ^ c);
+}
+// First output of std::mt19937_64(seed): only state words 0, 1 and 156 feed the first refill.
+__device__ __forceinline__ uint64_t mt64_first(uint64_t seed) {
+    const uint64_t f = 6364136223846793005ULL;
+    uint64_t x = seed, x1 = 0;
+#pragma unroll 4
+    for (uint64_t i = 1; i <= 156; ++i) {
+        x = f * (x ^ (x >> 62)) + i;
+        if (i == 1) x1 = x;
+    }
+    const uint64_t y = (seed & 0xFFFFFFFF80000000ULL) | (x1 & 0x7FFFFFFFULL);
+    uint64_t z = x ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+__device__ __forceinline__ double clamp01(double v) { return fmin(1.0, fmax(0.0, v)); }
+
+__device__ __forceinline__ double softplus(double x) {  // gater.cpp:32-36
+    if (x > 30.0) return x;
+    if (x < -30.0) return exp(x);
+    return log1p(exp(x));
+}
+
+struct GateOut {
+    int pick;
+    uint32_t flags;
+};
+
+// score_candidates + select over n records; scores optionally written (n x 5).
+__device__ __forceinline__ GateOut gate_select(int n, const double* sims, const double* snegs,
+                               const double* durs, double L, double temp, double thr,
+                               uint64_t rng_seed, double* scores) {
+    double s_pos[kMaxTopK], a[kMaxTopK], b[kMaxTopK], q[kMaxTopK];
+    double max_pos = 0.0, max_neg_dis = 0.0;
+    for (int i = 0; i < n; ++i) {
+        s_pos[i] = clamp01(sims[i]);
+        max_pos = fmax(max_pos, s_pos[i]);
+        max_neg_dis = fmax(max_neg_dis, 1.0 - snegs[i]);
+    }
+    const double lo = 0.5 * L, hi = 1.5 * L;
+    for (int i = 0; i < n; ++i) {
+        a[i] = max_pos > 0.0 ? __ddiv_rn(s_pos[i], max_pos) : 0.0;
+        b[i] = max_neg_dis > 0.0 ? __ddiv_rn(1.0 - snegs[i], max_neg_dis) : 0.0;
+        const bool ok = durs[i] >= lo && durs[i] <= hi;
+        q[i] = ok ? fmin(a[i], b[i]) : 0.0;
+        if (scores) {
+            scores[i * 5 + 0] = s_pos[i];
+            scores[i * 5 + 1] = snegs[i];
+            scores[i * 5 + 2] = a[i];
+            scores[i * 5 + 3] = b[i];
+            scores[i * 5 + 4] = q[i];
+        }
+    }
+    GateOut g{-1, 0u};
+    int surv[kMaxTopK], ns = 0;
+    for (int i = 0; i < n; ++i)
+        if (q[i] >= thr) surv[ns++] = i;
+    if (ns == 0) return g;  // no survivor: miss, and no RNG draw (selector.cpp:67)
+    double max_s = s_pos[surv[0]];
+    for (int j = 0; j < ns; ++j) max_s = fmax(max_s, s_pos[surv[j]]);
+    double w[kMaxTopK], total = 0.0;
+    for (int j = 0; j < ns; ++j) {
+        w[j] = exp(__ddiv_rn(s_pos[surv[j]] - max_s, temp));
+        total = __dadd_rn(total, w[j]);
+    }
+    const double u = (double)(mt64_first(rng_seed) >> 11) * 0x1.0p-53;
+    const double target = __dmul_rn(u, total);
+    const double slack = 1e-13 * total;
+    double acc = 0.0;
+    g.pick = surv[ns - 1];
+    for (int j = 0; j < ns; ++j) {
+        acc = __dadd_rn(acc, w[j]);
+        if (fabs(acc - target) <= slack) g.flags |= SW_CHOICE_AMBIGUOUS_DRAW;
+        if (acc >= target) {
+            g.pick = surv[j];
+            break;
+        }
+    }
+    return g;
+}
+
+// choose_arm (gater.cpp:70-92): products and sums strictly unfused.
+__device__ __forceinline__ int choose_arm(const float* __restrict__ theta, const float* __restrict__ psi, int fd,
+                          double beta, const double* phi, int explore, uint32_t* flags) {
+    for (int i = 0; i < fd; ++i)
+        if (!isfinite(phi[i])) {
+            *flags |= SW_CHOICE_NONFINITE_PHI;
+            return 0;
+        }
+    int best = 0;
+    double best_score = -INFINITY, second = -INFINITY;
+    for (int a = 0; a < kNumArms; ++a) {
+        double s = 0.0;
+        for (int i = 0; i < fd; ++i) s = __dadd_rn(s, __dmul_rn((double)theta[a * fd + i], phi[i]));
+        if (explore) {
+            double u = 0.0;
+            for (int i = 0; i < fd; ++i) u = __dadd_rn(u, __dmul_rn((double)psi[a * fd + i], phi[i]));
+            s = __dadd_rn(s, __dmul_rn(beta, softplus(u)));
+        }
+        if (s >= best_score) {  // ties to the larger skip fraction
+            second = best_score;
+            best_score = s;
+            best = a;
+        } else if (s > second) {
+            second = s;
+        }
+    }
+    if (explore && fabs(best_score - second) <= 1e-13 * fmax(1.0, fabs(best_score)))
+        *flags |= SW_CHOICE_AMBIGUOUS_ARM;
+    return best;
+}
+
+struct SelParams {
+    uint64_t seed;
+    int top_k;
+    double temp, thr;
+    int policy, fixed_arm, rule_arm;
+    double rule_thr;
+    double fps;
+    const float* theta;
+    const float* psi;
+    int fd;
+    double beta;
+};
+
+
+// One request: the top-k hit records (sorted, (sim desc, id asc)) -> the ServeOutcome fields.
+__device__ __forceinline__ sw_choice select_one(const HitRec* __restrict__ h, int nh,
+                                                const sw_request& rq, const SelParams& p) {
+    uint32_t flags = 0;
+    if (nh < 0) {
+        nh = -nh - 1;
+        flags |= SW_CHOICE_INCOMPLETE;
+    }
+    nh = min(nh, p.top_k);
+    sw_choice c;
+    memset(&c, 0, sizeof(c));
+    c.pick = -1;
+    c.n_hits = nh;
+    int hit = 0;
+    double phi[kFeatureDim];
+    if (nh > 0) {
+        double sims[kMaxTopK], sn[kMaxTopK], du[kMaxTopK];
+        for (int i = 0; i < nh; ++i) {
+            sims[i] = h[i].sim;
+            sn[i] = h[i].s_neg;
+            du[i] = h[i].length_s;  // matched segment duration (pipeline.cpp:122)
+        }
+        GateOut g = gate_select(nh, sims, sn, du, rq.duration_s, p.temp, p.thr,
+                                derive_seed(p.seed, rq.id, 2, 0), nullptr);
+        flags |= g.flags;
+        if (g.pick >= 0) {
+            const HitRec& ch = h[g.pick];
+            hit = 1;
+            c.pick = g.pick;
+            c.entry_id = ch.entry_id;
+            c.segment.level = ch.level;
+            c.segment.start_s = ch.start_s;
+            c.segment.length_s = ch.length_s;
+            c.similarity = ch.sim;  // cos(prompt, seg_emb) (pipeline.cpp:173)
+            c.owner = ch.owner;
+            c.slot = ch.slot;
+            phi[0] = ch.sim;
+            for (int j = 0; j < 8; ++j) phi[1 + j] = ch.phi[j];
+            phi[9] = (double)rq.total_steps / 200.0;
+            phi[10] = 1.0;
+        }
+    }
+    int arm = 0;
+    if (hit) {
+        if (p.policy == SW_POLICY_EXPLOIT || p.policy == SW_POLICY_EXPLORE)
+            arm = choose_arm(p.theta, p.psi, p.fd, p.beta, phi, p.policy == SW_POLICY_EXPLORE,
+                             &flags);
+        else if (p.policy == SW_POLICY_RULE)
+            arm = c.similarity >= p.rule_thr ? p.rule_arm : 0;
+        else
+            arm = p.fixed_arm;
+    } else if (p.policy == SW_POLICY_FIXED) {
+        arm = p.fixed_arm;  // latency held constant even on a miss (pipeline.cpp:229-231)
+    }
+    const double skip = 0.05 * (double)arm;
+    c.hit = hit;
+    c.arm = arm;
+    c.skip_fraction = skip;
+    c.steps_skipped = (int32_t)llround(skip * (double)rq.total_steps);
+    c.t_out = hit ? (int32_t)llround(rq.duration_s * p.fps) : 0;
+    c.flags = flags;
+    return c;
+}
+
+SelParams make_sel_params(const Ctx& c, uint64_t seed, const sw_selector_config& sel,
+                          const sw_policy& pol);
+
+}  // namespace dev
+}  // namespace sw

@@ -19,6 +19,10 @@
 
 namespace sw {
 
+namespace dev {
+struct SelParams;
+}
+
 // --------------------------------------------------------------------------- errors
 struct Error : std::runtime_error {
     int code;
@@ -43,6 +47,9 @@ constexpr int kFeatureDim = 11;       // gater.hpp:28
 constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep running list
 constexpr int kCandCap = 16384;       // emitted candidates per query (split over the CTAs)
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
+// |bf16 dot - fp64 dot| <= kEpsRel * |q| * max|row|: bf16 rounding of both operands
+// (2u + u^2, u = 2^-8) plus fp32 tensor-core accumulation slack over K <= 512
+constexpr float kEpsRel = 0.0081f;
 
 // Per-shard top-k record (SW_HIT_RECORD_BYTES = 128): everything the replicated select /
 // gater stage needs, so the all-gather carries no embeddings.
@@ -117,6 +124,7 @@ struct Ctx {
     uint32_t* thr = nullptr;        // [Bmax] shared running k-th best (ordered)
     int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
     int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)
+    float* cta_topk = nullptr;      // [Bmax][148][32] each scoring CTA's final top-k (approx)
     int last_chunks = 1;
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
@@ -191,7 +199,10 @@ void launch_clear_slot(Ctx& c, int64_t slot, cudaStream_t st);
 void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, uint64_t seed,
                            double delta, cudaStream_t st);
 
+int launch_prep(Ctx& c, const float* d_q, int B, cudaStream_t st);
 int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t st);
+int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
+                        const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st);
 void launch_hits_to_public(Ctx& c, int B, int k, sw_hit* d_out, int32_t* d_n, cudaStream_t st);
 void launch_select(Ctx& c, const HitRec* d_hits, const int32_t* d_nh, int ld, const float* d_q,
                    const sw_request* d_req, int B, uint64_t seed, const sw_selector_config& sel,
