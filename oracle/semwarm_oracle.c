@@ -347,11 +347,13 @@ void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 /* u in (0,1): odd 24-bit numerator, exact in float */
 static float u01(uint32_t x) { return (float)((x >> 8) | 1u) * 0x1.0p-24f; }
 
+/* Box-Muller: r = sqrt(-2 ln u1) in fp32; cos/sin(2 pi u2) correctly rounded to fp32 (the
+ * device evaluates sincospif(2 u2), exact argument, <= 1 ulp). */
 static void box_muller(uint32_t a, uint32_t b, float* z0, float* z1) {
     float r = sqrtf(-2.0f * logf(u01(a)));
-    float th = 6.2831853071795865f * u01(b);
-    *z0 = r * cosf(th);
-    *z1 = r * sinf(th);
+    double th = 2.0 * M_PI * (double)u01(b);
+    *z0 = r * (float)cos(th);
+    *z1 = r * (float)sin(th);
 }
 
 void so_philox_normals(uint64_t seed, uint64_t rid, int64_t n, float* out) {

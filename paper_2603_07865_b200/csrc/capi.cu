@@ -60,7 +60,7 @@ static void default_schedule(std::vector<double>& abar) {
 
 static void free_ctx(Ctx& c) {
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
-                    c.slice_cnt, c.cta_topk, c.tsrc,
+                    c.slice_cnt, c.cta_topk, c.u_draw, c.tsrc,
                     c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
                     c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
@@ -119,6 +119,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
     dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
     dalloc(&c.cta_topk, (size_t)c.Bmax * 148 * kMaxTopK);
+    dalloc(&c.u_draw, (size_t)c.Bmax);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_exact, (size_t)c.Bmax * kCandCap);

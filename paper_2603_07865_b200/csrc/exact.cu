@@ -6,7 +6,7 @@
 // The certified-candidate filter, exact fp64 rescoring and top-k live in finish.cu.
 #include <cfloat>
 
-#include "sw_internal.cuh"
+#include "select_dev.cuh"
 
 namespace sw {
 
@@ -22,9 +22,14 @@ __device__ __forceinline__ double clamp_cos(double v) {
 
 __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
                        __nv_bfloat16* __restrict__ q_bf, float* __restrict__ q_norm,
-                       uint32_t* __restrict__ thr, int32_t* __restrict__ cand_n) {
+                       uint32_t* __restrict__ thr, int32_t* __restrict__ cand_n,
+                       const sw_request* __restrict__ req, uint64_t seed,
+                       double* __restrict__ u_draw) {
     const int b = blockIdx.x;
     if (b >= B) return;
+    // the request's selector draw Rng(derive_seed(seed, id, 2)).uniform() (pipeline.cpp:211),
+    // computed here by one lane of warp 1 so its 156-step MT seeding overlaps the conversion
+    if (req && threadIdx.x == 32) u_draw[b] = dev::uniform_draw(dev::derive_seed(seed, req[b].id, 2, 0));
     __shared__ double red[32];
     const float* qb = q + (int64_t)b * D;
     double s = 0.0;
@@ -68,9 +73,11 @@ __global__ void k_hits_to_public(int B, int k, const HitRec* __restrict__ hits,
 
 }  // namespace
 
-int launch_prep(Ctx& c, const float* d_q, int B, cudaStream_t st) {
+int launch_prep(Ctx& c, const float* d_q, int B, const sw_request* d_req, uint64_t seed,
+                cudaStream_t st) {
     StageScope sc(c, SW_STAGE_PREP, st);
-    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.thr, c.cand_n);
+    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.thr, c.cand_n, d_req, seed,
+                              c.u_draw);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

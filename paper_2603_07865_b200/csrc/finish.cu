@@ -19,10 +19,10 @@ namespace sw {
 
 namespace {
 
-constexpr int FT = 256;  // threads per query CTA
+constexpr int WPB = 4;  // queries (warps) per CTA
 
 struct FinishParams {
-    int k, rank, implicit_all, n_chunks, cap_local, do_select;
+    int B, k, rank, implicit_all, n_chunks, cap_local, do_select;
     int64_t n_slots;
     const int32_t* slice_cnt;
     const int32_t* cand_slot;
@@ -44,6 +44,7 @@ struct FinishParams {
     int32_t* best_row;
     HitRec* hits;
     int32_t* nhits;
+    const double* u_draw;
     dev::SelParams sp;
     const sw_request* reqs;
     sw_choice* out;
@@ -53,54 +54,50 @@ __device__ __forceinline__ bool before(double as, uint64_t aid, double bs, uint6
     return as > bs || (as == bs && aid < bid);
 }
 
-// block-wide max of a 64-bit key (all threads get the result)
-__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v,
-                                                            unsigned long long* sh) {
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
     for (int o = 16; o; o >>= 1) {
         const unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
         v = x > v ? x : v;
     }
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        v = threadIdx.x < (FT >> 5) ? sh[threadIdx.x] : 0ull;
-        for (int o = 16; o; o >>= 1) {
-            const unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
-            v = x > v ? x : v;
-        }
-        if (threadIdx.x == 0) sh[32] = v;
-    }
-    __syncthreads();
-    v = sh[32];
-    __syncthreads();
     return v;
 }
 
-__global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
-    extern __shared__ float4 qs4[];
-    float* qs = reinterpret_cast<float*>(qs4);
-    __shared__ unsigned long long red[33];
-    __shared__ int s_n, s_ovf;
-    __shared__ double s_sim[FT / 32];
-    __shared__ uint64_t s_id[FT / 32];
-    __shared__ int64_t s_slot[FT / 32], s_item[FT / 32];
-    __shared__ int64_t sel_slot[kMaxTopK];
-    __shared__ int32_t sel_row[kMaxTopK];
-    __shared__ double sel_sim[kMaxTopK];
-    __shared__ int sel_n;
-    const int b = blockIdx.x;
-    const float* qb = p.q + (int64_t)b * p.D;
-    for (int d = threadIdx.x; d < p.Df; d += FT) qs[d] = d < p.D ? qb[d] : 0.0f;
-    if (threadIdx.x == 0) {
-        s_n = 0;
-        s_ovf = 0;
-        sel_n = 0;
+// fp64 sequential dot of a stored row with the query in shared memory (core.cpp:26-30)
+__device__ __forceinline__ double seq_dot4(const float4* __restrict__ rp,
+                                           const float4* __restrict__ qs4, int n4) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int d4 = 0; d4 < n4; ++d4) {
+        const float4 x = __ldg(rp + d4);
+        const float4 y = qs4[d4];
+        s = fma((double)y.x, (double)x.x, s);
+        s = fma((double)y.y, (double)x.y, s);
+        s = fma((double)y.z, (double)x.z, s);
+        s = fma((double)y.w, (double)x.w, s);
     }
-    __syncthreads();
+    return s;
+}
+
+// One warp per query: no block barriers, only warp shuffles / ballots.
+__global__ void __launch_bounds__(32 * WPB) k_finish(const FinishParams p) {
+    extern __shared__ float4 qs_all[];
+    __shared__ int64_t sel_slot[WPB][kMaxTopK];
+    __shared__ int32_t sel_row[WPB][kMaxTopK];
+    __shared__ double sel_sim[WPB][kMaxTopK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * WPB + warp;
+    if (b >= p.B) return;
+    const unsigned full = 0xffffffffu;
+    float4* qs4 = qs_all + warp * (p.Df >> 2);
+    float* qs = reinterpret_cast<float*>(qs4);
+    const float* qb = p.q + (int64_t)b * p.D;
+    for (int d = lane; d < p.Df; d += 32) qs[d] = d < p.D ? qb[d] : 0.0f;
+    __syncwarp();
     const int64_t base = (int64_t)b * kCandCap;
 
     // ---------------- A: certified candidate set
-    int64_t n;
+    int64_t n = 0;
+    bool ovf = false;
     if (!p.implicit_all) {
         const int m = p.n_chunks * p.k;
         const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
@@ -108,15 +105,15 @@ __global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
         float kth = -INFINITY;
         for (int r = 0; r < p.k; ++r) {
             unsigned long long best = 0;
-            for (int i = threadIdx.x; i < m; i += FT) {
+            for (int i = lane; i < m; i += 32) {
                 const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
                 if (v == -INFINITY) continue;
                 const unsigned long long key =
                     ((unsigned long long)f2ord(v) << 32) | (0xFFFFFFFFu - (uint32_t)i);
                 if (key < prev && key > best) best = key;
             }
-            best = block_max_u64(best, red);
-            if (best == 0) {  // fewer than k valid entries in the whole shard: keep all
+            best = warp_max_u64(best);
+            if (best == 0) {  // fewer than k valid entries in the shard: keep everything
                 kth = -INFINITY;
                 break;
             }
@@ -124,75 +121,103 @@ __global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
             kth = ord2f((uint32_t)(best >> 32));
         }
         const float cut = kth - 2.0f * p.eps_rel * p.q_norm[b] * ord2f(*p.maxnorm);
-        for (int c = 0; c < p.n_chunks; ++c) {
-            const int cnt = p.slice_cnt[(int64_t)b * p.n_chunks + c];
-            const int mc = min(cnt, p.cap_local);
-            if (cnt > p.cap_local && threadIdx.x == 0) s_ovf = 1;
-            const int64_t src = base + (int64_t)c * p.cap_local;
-            for (int i = threadIdx.x; i < mc; i += FT) {
-                if (p.cand_score[src + i] >= cut) {
-                    const int j = atomicAdd(&s_n, 1);
-                    p.list[base + j] = p.cand_slot[src + i];
+        for (int c0 = 0; c0 < p.n_chunks; c0 += 32) {
+            const int my_cnt = c0 + lane < p.n_chunks
+                                   ? p.slice_cnt[(int64_t)b * p.n_chunks + c0 + lane] : 0;
+            ovf = ovf || __any_sync(full, my_cnt > p.cap_local);
+            const int cmax = min(32, p.n_chunks - c0);
+            for (int j = 0; j < cmax; ++j) {
+                const int cnt = min(__shfl_sync(full, my_cnt, j), p.cap_local);
+                const int64_t src = base + (int64_t)(c0 + j) * p.cap_local;
+                for (int i0 = 0; i0 < cnt; i0 += 32) {
+                    const int i = i0 + lane;
+                    const bool pass = i < cnt && p.cand_score[src + i] >= cut;
+                    const unsigned bal = __ballot_sync(full, pass);
+                    if (pass) p.list[base + n + __popc(bal & ((1u << lane) - 1u))] = p.cand_slot[src + i];
+                    n += __popc(bal);
                 }
             }
         }
-        __syncthreads();
-        n = s_n;
+        __syncwarp();
     } else {
         n = p.n_slots;
     }
 
-    // ---------------- B: exact rescoring, one thread per (candidate, pyramid row)
+    // ---------------- B: exact rescoring, lane = (candidate, pyramid row); 2 chains per lane
     const int64_t items = n << p.logRp;
-    const int64_t items_w = (items + 31) & ~int64_t(31);  // whole warps: shuffles converge
-    for (int64_t w = threadIdx.x; w < items_w; w += FT) {
-        const int64_t i = w >> p.logRp;
-        const int r = (int)(w & (p.Rp - 1));
-        double sim = -DBL_MAX;
-        int row = 0x7fffffff;
-        if (w < items) {
-            const int64_t slot = p.implicit_all ? i : (int64_t)p.list[base + i];
-            if (p.valid[slot] && r < p.nrows[slot]) {
-                const float4* rp =
-                    reinterpret_cast<const float4*>(p.rows + (slot * p.Rp + r) * p.Df);
-                double s = 0.0;
-#pragma unroll 4
-                for (int d4 = 0; d4 < (p.Df >> 2); ++d4) {
-                    const float4 x = __ldg(rp + d4);
-                    const float4 y = qs4[d4];
-                    s = fma((double)y.x, (double)x.x, s);
-                    s = fma((double)y.y, (double)x.y, s);
-                    s = fma((double)y.z, (double)x.z, s);
-                    s = fma((double)y.w, (double)x.w, s);
+    const int64_t items_w = (items + 31) & ~int64_t(31);
+    const int n4 = p.Df >> 2;
+    for (int64_t w0 = lane; w0 < items_w; w0 += 64) {
+        double sim[2] = {-DBL_MAX, -DBL_MAX};
+        int row[2] = {0x7fffffff, 0x7fffffff};
+        const float4* rp[2] = {nullptr, nullptr};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t w = w0 + 32 * h;
+            if (w < items) {
+                const int64_t i = w >> p.logRp;
+                const int r = (int)(w & (p.Rp - 1));
+                const int64_t slot = p.implicit_all ? i : (int64_t)p.list[base + i];
+                if (p.valid[slot] && r < p.nrows[slot]) {
+                    rp[h] = reinterpret_cast<const float4*>(p.rows + (slot * p.Rp + r) * p.Df);
+                    row[h] = r;
                 }
-                sim = fmin(1.0, fmax(-1.0, s));
-                row = r;
             }
         }
-        for (int o = 1; o < p.Rp; o <<= 1) {
-            const double os = __shfl_xor_sync(0xffffffffu, sim, o);
-            const int orow = __shfl_xor_sync(0xffffffffu, row, o);
-            if (os > sim || (os == sim && orow < row)) {
-                sim = os;
-                row = orow;
+        // two independent sequential chains interleaved for ILP (each keeps its own order)
+        double s0 = 0.0, s1 = 0.0;
+        if (rp[0] && rp[1]) {
+#pragma unroll 2
+            for (int d4 = 0; d4 < n4; ++d4) {
+                const float4 x0 = __ldg(rp[0] + d4), x1 = __ldg(rp[1] + d4);
+                const float4 y = qs4[d4];
+                s0 = fma((double)y.x, (double)x0.x, s0);
+                s1 = fma((double)y.x, (double)x1.x, s1);
+                s0 = fma((double)y.y, (double)x0.y, s0);
+                s1 = fma((double)y.y, (double)x1.y, s1);
+                s0 = fma((double)y.z, (double)x0.z, s0);
+                s1 = fma((double)y.z, (double)x1.z, s1);
+                s0 = fma((double)y.w, (double)x0.w, s0);
+                s1 = fma((double)y.w, (double)x1.w, s1);
             }
+        } else if (rp[0]) {
+            s0 = seq_dot4(rp[0], qs4, n4);
+        } else if (rp[1]) {
+            s1 = seq_dot4(rp[1], qs4, n4);
         }
-        if (w < items && r == 0) {
-            p.exact[base + i] = sim;
-            p.best_row[base + i] = row;
+        if (rp[0]) sim[0] = fmin(1.0, fmax(-1.0, s0));
+        if (rp[1]) sim[1] = fmin(1.0, fmax(-1.0, s1));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double sm = sim[h];
+            int rw = row[h];
+            for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest row
+                const double os = __shfl_xor_sync(full, sm, o);
+                const int orow = __shfl_xor_sync(full, rw, o);
+                if (os > sm || (os == sm && orow < rw)) {
+                    sm = os;
+                    rw = orow;
+                }
+            }
+            const int64_t w = w0 + 32 * h;
+            if (w < items && (w & (p.Rp - 1)) == 0) {
+                p.exact[base + (w >> p.logRp)] = sm;
+                p.best_row[base + (w >> p.logRp)] = rw;
+            }
         }
     }
-    __syncthreads();
+    __syncwarp();
 
-    // ---------------- C: top-k, (sim desc, id asc)
+    // ---------------- C: top-k by (sim desc, id asc)
     double prev_sim = DBL_MAX;
     uint64_t prev_id = 0;
     bool have_prev = false;
+    int nh = 0;
     for (int r = 0; r < p.k; ++r) {
         double bs = -DBL_MAX;
         uint64_t bid = ~0ull;
         int64_t bslot = -1, bitem = -1;
-        for (int64_t i = threadIdx.x; i < n; i += FT) {
+        for (int64_t i = lane; i < n; i += 32) {
             const int64_t slot = p.implicit_all ? i : (int64_t)p.list[base + i];
             if (p.implicit_all && !p.valid[slot]) continue;
             const double s = p.exact[base + i];
@@ -207,10 +232,10 @@ __global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
             }
         }
         for (int o = 16; o; o >>= 1) {
-            const double os = __shfl_xor_sync(0xffffffffu, bs, o);
-            const uint64_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
-            const int64_t oslot = __shfl_xor_sync(0xffffffffu, bslot, o);
-            const int64_t oitem = __shfl_xor_sync(0xffffffffu, bitem, o);
+            const double os = __shfl_xor_sync(full, bs, o);
+            const uint64_t oid = __shfl_xor_sync(full, bid, o);
+            const int64_t oslot = __shfl_xor_sync(full, bslot, o);
+            const int64_t oitem = __shfl_xor_sync(full, bitem, o);
             if (oslot >= 0 && (bslot < 0 || before(os, oid, bs, bid))) {
                 bs = os;
                 bid = oid;
@@ -218,43 +243,24 @@ __global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
                 bitem = oitem;
             }
         }
-        if ((threadIdx.x & 31) == 0) {
-            s_sim[threadIdx.x >> 5] = bs;
-            s_id[threadIdx.x >> 5] = bid;
-            s_slot[threadIdx.x >> 5] = bslot;
-            s_item[threadIdx.x >> 5] = bitem;
+        if (bslot < 0) break;
+        if (lane == 0) {
+            sel_slot[warp][nh] = bslot;
+            sel_row[warp][nh] = p.best_row[base + bitem];
+            sel_sim[warp][nh] = bs;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int w0 = -1;
-            for (int w = 0; w < FT / 32; ++w) {
-                if (s_slot[w] < 0) continue;
-                if (w0 < 0 || before(s_sim[w], s_id[w], s_sim[w0], s_id[w0])) w0 = w;
-            }
-            if (w0 >= 0) {
-                sel_slot[sel_n] = s_slot[w0];
-                sel_row[sel_n] = p.best_row[base + s_item[w0]];
-                sel_sim[sel_n] = s_sim[w0];
-                red[0] = s_id[w0];
-                sel_n++;
-            }
-            red[1] = w0 >= 0 ? 1 : 0;
-        }
-        __syncthreads();
-        if (red[1] == 0) break;
-        prev_sim = sel_sim[sel_n - 1];
-        prev_id = red[0];
+        ++nh;
+        prev_sim = bs;
+        prev_id = bid;
         have_prev = true;
-        __syncthreads();
     }
-    __syncthreads();
-    const int nh = sel_n;
+    __syncwarp();
 
-    // ---------------- D: enrichment (8 threads per hit)
+    // ---------------- D: enrichment (8 lanes per hit)
     HitRec* hb = p.hits + (int64_t)b * kMaxTopK;
-    for (int t = threadIdx.x; t < nh * 8; t += FT) {
+    for (int t = lane; t < nh * 8; t += 32) {
         const int h = t >> 3, j = t & 7;
-        const int64_t row = sel_slot[h] * p.Rp + sel_row[h];
+        const int64_t row = sel_slot[warp][h] * p.Rp + sel_row[warp][h];
         const float* rp = p.rows + row * p.Df;
         const size_t lo = (size_t)j * p.D / 8, hi = (size_t)(j + 1) * p.D / 8;
         double s = 0.0;
@@ -262,23 +268,26 @@ __global__ void __launch_bounds__(FT) k_finish(const FinishParams p) {
         hb[h].phi[j] = s;
         if (j == 0) {
             const sw_segment sg = p.segs[row];
-            hb[h].sim = sel_sim[h];
-            hb[h].entry_id = p.ids[sel_slot[h]];
+            hb[h].sim = sel_sim[warp][h];
+            hb[h].entry_id = p.ids[sel_slot[warp][h]];
             hb[h].level = sg.level;
-            hb[h].slot = (int32_t)sel_slot[h];
+            hb[h].slot = (int32_t)sel_slot[warp][h];
             hb[h].start_s = sg.start_s;
             hb[h].length_s = sg.length_s;
             hb[h].s_neg = p.sneg[row];
-            hb[h].row = sel_row[h];
+            hb[h].row = sel_row[warp][h];
             hb[h].owner = p.rank;
         }
     }
-    const int nh_code = s_ovf ? -nh - 1 : nh;
-    if (threadIdx.x == 0) p.nhits[b] = nh_code;
-    __syncthreads();
+    const int nh_code = ovf ? -nh - 1 : nh;
+    if (lane == 0) p.nhits[b] = nh_code;
+    __syncwarp();
 
     // ---------------- E: gate + select + Skip Gater + t*
-    if (p.do_select && threadIdx.x == 0) p.out[b] = dev::select_one(hb, nh_code, p.reqs[b], p.sp);
+    if (p.do_select) {
+        const sw_choice c = dev::select_warp(hb, nh_code, p.u_draw[b], p.reqs[b], p.sp, lane);
+        if (lane == 0) p.out[b] = c;
+    }
 }
 
 }  // namespace
@@ -300,12 +309,13 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     if (!tc)
         SW_REQUIRE(c.high_water <= kCandCap,
                    "exact-only search is limited to 16384 slots; enable the tcgen05 path");
-    kernels += launch_prep(c, d_q, B, st);
+    kernels += launch_prep(c, d_q, B, d_req, sp ? sp->seed : 0, st);
     if (tc) {
         StageScope sc(c, SW_STAGE_SCORE_TC, st);
         kernels += launch_score_tc(c, B, k, st);
     }
     FinishParams p{};
+    p.B = B;
     p.k = k;
     p.rank = rank;
     p.implicit_all = tc ? 0 : 1;
@@ -336,12 +346,13 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.best_row = c.cand_row;
     p.hits = c.hits;
     p.nhits = c.nhits;
+    p.u_draw = c.u_draw;
     if (sp) p.sp = *sp;
     p.reqs = d_req;
     p.out = d_out;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
-        k_finish<<<B, FT, sizeof(float) * c.Df, st>>>(p);
+        k_finish<<<(B + WPB - 1) / WPB, 32 * WPB, sizeof(float) * c.Df * WPB, st>>>(p);
     }
     SW_CUDA(cudaGetLastError());
     c.last_tc = tc ? 1 : 0;

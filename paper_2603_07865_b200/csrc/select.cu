@@ -66,7 +66,7 @@ __global__ void k_score_select_one(int n, const double* sims, const double* sneg
                                    const double* durs, double L, double temp, double thr,
                                    uint64_t rng_seed, double* scores, int32_t* pick) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        GateOut g = gate_select(n, sims, sneg, durs, L, temp, thr, rng_seed, scores);
+        GateOut g = gate_select(n, sims, sneg, durs, L, temp, thr, uniform_draw(rng_seed), scores);
         pick[0] = g.pick;
         pick[1] = (int32_t)g.flags;
     }

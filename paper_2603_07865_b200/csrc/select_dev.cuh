@@ -51,9 +51,15 @@ struct GateOut {
 };
 
 // score_candidates + select over n records; scores optionally written (n x 5).
+// Rng(seed).uniform() (core.hpp:83): (first mt19937_64 output >> 11) * 2^-53
+__device__ __forceinline__ double uniform_draw(uint64_t rng_seed) {
+    return (double)(mt64_first(rng_seed) >> 11) * 0x1.0p-53;
+}
+
+// u: the request's selector draw (uniform_draw(derive_seed(seed, id, 2)), pipeline.cpp:211)
 __device__ __forceinline__ GateOut gate_select(int n, const double* sims, const double* snegs,
                                const double* durs, double L, double temp, double thr,
-                               uint64_t rng_seed, double* scores) {
+                               double u, double* scores) {
     double s_pos[kMaxTopK], a[kMaxTopK], b[kMaxTopK], q[kMaxTopK];
     double max_pos = 0.0, max_neg_dis = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -87,7 +93,6 @@ __device__ __forceinline__ GateOut gate_select(int n, const double* sims, const 
         w[j] = exp(__ddiv_rn(s_pos[surv[j]] - max_s, temp));
         total = __dadd_rn(total, w[j]);
     }
-    const double u = (double)(mt64_first(rng_seed) >> 11) * 0x1.0p-53;
     const double target = __dmul_rn(u, total);
     const double slack = 1e-13 * total;
     double acc = 0.0;
@@ -103,6 +108,20 @@ __device__ __forceinline__ GateOut gate_select(int n, const double* sims, const 
     return g;
 }
 
+// value (+ beta * uncertainty) of one arm: head_dot (gater.cpp:52-58), products and sums unfused
+__device__ __forceinline__ double arm_score(const float* __restrict__ theta,
+                                            const float* __restrict__ psi, int fd, double beta,
+                                            const double* phi, int a, int explore) {
+    double s = 0.0;
+    for (int i = 0; i < fd; ++i) s = __dadd_rn(s, __dmul_rn((double)theta[a * fd + i], phi[i]));
+    if (explore) {
+        double u = 0.0;
+        for (int i = 0; i < fd; ++i) u = __dadd_rn(u, __dmul_rn((double)psi[a * fd + i], phi[i]));
+        s = __dadd_rn(s, __dmul_rn(beta, softplus(u)));
+    }
+    return s;
+}
+
 // choose_arm (gater.cpp:70-92): products and sums strictly unfused.
 __device__ __forceinline__ int choose_arm(const float* __restrict__ theta, const float* __restrict__ psi, int fd,
                           double beta, const double* phi, int explore, uint32_t* flags) {
@@ -114,13 +133,7 @@ __device__ __forceinline__ int choose_arm(const float* __restrict__ theta, const
     int best = 0;
     double best_score = -INFINITY, second = -INFINITY;
     for (int a = 0; a < kNumArms; ++a) {
-        double s = 0.0;
-        for (int i = 0; i < fd; ++i) s = __dadd_rn(s, __dmul_rn((double)theta[a * fd + i], phi[i]));
-        if (explore) {
-            double u = 0.0;
-            for (int i = 0; i < fd; ++i) u = __dadd_rn(u, __dmul_rn((double)psi[a * fd + i], phi[i]));
-            s = __dadd_rn(s, __dmul_rn(beta, softplus(u)));
-        }
+        const double s = arm_score(theta, psi, fd, beta, phi, a, explore);
         if (s >= best_score) {  // ties to the larger skip fraction
             second = best_score;
             best_score = s;
@@ -171,7 +184,7 @@ __device__ __forceinline__ sw_choice select_one(const HitRec* __restrict__ h, in
             du[i] = h[i].length_s;  // matched segment duration (pipeline.cpp:122)
         }
         GateOut g = gate_select(nh, sims, sn, du, rq.duration_s, p.temp, p.thr,
-                                derive_seed(p.seed, rq.id, 2, 0), nullptr);
+                                uniform_draw(derive_seed(p.seed, rq.id, 2, 0)), nullptr);
         flags |= g.flags;
         if (g.pick >= 0) {
             const HitRec& ch = h[g.pick];
@@ -199,6 +212,97 @@ __device__ __forceinline__ sw_choice select_one(const HitRec* __restrict__ h, in
             arm = c.similarity >= p.rule_thr ? p.rule_arm : 0;
         else
             arm = p.fixed_arm;
+    } else if (p.policy == SW_POLICY_FIXED) {
+        arm = p.fixed_arm;  // latency held constant even on a miss (pipeline.cpp:229-231)
+    }
+    const double skip = 0.05 * (double)arm;
+    c.hit = hit;
+    c.arm = arm;
+    c.skip_fraction = skip;
+    c.steps_skipped = (int32_t)llround(skip * (double)rq.total_steps);
+    c.t_out = hit ? (int32_t)llround(rq.duration_s * p.fps) : 0;
+    c.flags = flags;
+    return c;
+}
+
+// Warp-cooperative select_one for one request: lane 0 runs the gate and the draw (u precomputed),
+// lanes 0..13 score one arm each, and the argmax keeps choose_arm's ">=" rule (ties -> larger
+// arm). The result is valid in lane 0.
+__device__ __forceinline__ sw_choice select_warp(const HitRec* __restrict__ h, int nh, double u,
+                                                 const sw_request& rq, const SelParams& p,
+                                                 int lane) {
+    uint32_t flags = 0;
+    if (nh < 0) {
+        nh = -nh - 1;
+        flags |= SW_CHOICE_INCOMPLETE;
+    }
+    nh = min(nh, p.top_k);
+    int pick = -1;
+    if (lane == 0 && nh > 0) {
+        double sims[kMaxTopK], sn[kMaxTopK], du[kMaxTopK];
+        for (int i = 0; i < nh; ++i) {
+            sims[i] = h[i].sim;
+            sn[i] = h[i].s_neg;
+            du[i] = h[i].length_s;  // matched segment duration (pipeline.cpp:122)
+        }
+        const GateOut g = gate_select(nh, sims, sn, du, rq.duration_s, p.temp, p.thr, u, nullptr);
+        flags |= g.flags;
+        pick = g.pick;
+    }
+    pick = __shfl_sync(0xffffffffu, pick, 0);
+    sw_choice c;
+    memset(&c, 0, sizeof(c));
+    c.pick = pick;
+    c.n_hits = nh;
+    const int hit = pick >= 0;
+    int arm = 0;
+    if (hit) {
+        const HitRec& ch = h[pick];
+        c.entry_id = ch.entry_id;
+        c.segment.level = ch.level;
+        c.segment.start_s = ch.start_s;
+        c.segment.length_s = ch.length_s;
+        c.similarity = ch.sim;  // cos(prompt, seg_emb) (pipeline.cpp:173)
+        c.owner = ch.owner;
+        c.slot = ch.slot;
+        if (p.policy == SW_POLICY_EXPLOIT || p.policy == SW_POLICY_EXPLORE) {
+            double phi[kFeatureDim];
+            phi[0] = ch.sim;
+            for (int j = 0; j < 8; ++j) phi[1 + j] = ch.phi[j];
+            phi[9] = (double)rq.total_steps / 200.0;
+            phi[10] = 1.0;
+            bool finite = true;
+            for (int i = 0; i < kFeatureDim; ++i) finite = finite && isfinite(phi[i]);
+            if (!finite) {
+                flags |= SW_CHOICE_NONFINITE_PHI;  // gater.cpp:71-76
+            } else {
+                const int explore = p.policy == SW_POLICY_EXPLORE;
+                double s = lane < kNumArms
+                               ? arm_score(p.theta, p.psi, p.fd, p.beta, phi, lane, explore)
+                               : -INFINITY;
+                // argmax; equal scores -> larger arm (the ">=" scan of gater.cpp:85)
+                double bs = s;
+                int ba = lane < kNumArms ? lane : -1;
+                for (int o = 16; o; o >>= 1) {
+                    const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+                    const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
+                    if (os > bs || (os == bs && oa > ba)) {
+                        bs = os;
+                        ba = oa;
+                    }
+                }
+                arm = ba;
+                if (explore) {
+                    double sec = lane == arm ? -INFINITY : s;
+                    for (int o = 16; o; o >>= 1) sec = fmax(sec, __shfl_xor_sync(0xffffffffu, sec, o));
+                    if (fabs(bs - sec) <= 1e-13 * fmax(1.0, fabs(bs))) flags |= SW_CHOICE_AMBIGUOUS_ARM;
+                }
+            }
+        } else if (p.policy == SW_POLICY_RULE) {
+            arm = c.similarity >= p.rule_thr ? p.rule_arm : 0;
+        } else {
+            arm = p.fixed_arm;
+        }
     } else if (p.policy == SW_POLICY_FIXED) {
         arm = p.fixed_arm;  // latency held constant even on a miss (pipeline.cpp:229-231)
     }

@@ -125,6 +125,7 @@ struct Ctx {
     int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
     int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)
     float* cta_topk = nullptr;      // [Bmax][148][32] each scoring CTA's final top-k (approx)
+    double* u_draw = nullptr;       // [Bmax] per-request selector draw
     int last_chunks = 1;
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
@@ -199,7 +200,8 @@ void launch_clear_slot(Ctx& c, int64_t slot, cudaStream_t st);
 void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, uint64_t seed,
                            double delta, cudaStream_t st);
 
-int launch_prep(Ctx& c, const float* d_q, int B, cudaStream_t st);
+int launch_prep(Ctx& c, const float* d_q, int B, const sw_request* d_req, uint64_t seed,
+                cudaStream_t st);
 int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t st);
 int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
                         const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st);
