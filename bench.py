@@ -331,6 +331,7 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     ch = wc.choices(choices)
+    qs = wc.query_stats(B) if world == 1 else None
     kernels_per_step = sum(n for (_, n) in prof.values()) / max(1, steps)
     if args.profile_only:
         if rank == 0:
@@ -457,6 +458,11 @@ def main():
         "stage_ms": stage_ms,
         "selector_p50_ms": lat,
         "hit_rate": round(float(hits.mean()), 4),
+        "candidates": None if qs is None else {
+            "emitted_mean": float(qs[:, 0].mean()), "kept_mean": float(qs[:, 1].mean()),
+            "kept_max": int(qs[:, 1].max()),
+            "finish_phase_kcycles_mean": [round(float(qs[:, j].mean()) / 1e3, 2) for j in (2, 3, 4, 5)],
+            "finish_phase_kcycles_max": [round(float(qs[:, j].max()) / 1e3, 2) for j in (2, 3, 4, 5)]},
         "e2e": e2e,
         "gpu_launches": int(round(kernels_per_step * steps)),
         "clocks": clk.summary(),

@@ -241,6 +241,10 @@ int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const in
 int sw_profile_enable(sw_ctx* ctx, int32_t on);
 int sw_profile_reset(sw_ctx* ctx);
 int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launches);
+/* Per-query statistics of the last search/plan (B x 8 int32): emitted candidates, certified
+ * candidates rescored, then device clock cycles of the finish phases (filter, rescore, top-k +
+ * enrichment, select). Synchronizes the device. */
+int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats);
 /* Launch statistics of the last sw_plan/sw_search on this context (kernels launched, mode). */
 int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
                         int32_t* candidates_max);

@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
         "sw_gater_host": ([vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
         "sw_last_launch_info": ([vp, vp, vp, vp], C.c_int),
         "sw_profile_enable": ([vp, i32], C.c_int),
+        "sw_debug_query_stats": ([vp, i32, vp], C.c_int),
         "sw_profile_reset": ([vp], C.c_int),
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
     }
@@ -135,7 +136,7 @@ EXPORTED = [
     "sw_arena_fill_synthetic", "sw_arena_read_rows", "sw_search", "sw_search_host", "sw_plan",
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host", "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
-    "sw_profile_enable", "sw_profile_reset", "sw_profile_read",
+    "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

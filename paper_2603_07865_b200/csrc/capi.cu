@@ -60,7 +60,7 @@ static void default_schedule(std::vector<double>& abar) {
 
 static void free_ctx(Ctx& c) {
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
-                    c.slice_cnt, c.cta_topk, c.u_draw, c.tsrc,
+                    c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
                     c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
                     c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
@@ -120,6 +120,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
     dalloc(&c.cta_topk, (size_t)c.Bmax * 148 * kMaxTopK);
     dalloc(&c.u_draw, (size_t)c.Bmax);
+    dalloc(&c.dbg, (size_t)c.Bmax * 8);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_exact, (size_t)c.Bmax * kCandCap);
@@ -801,6 +802,16 @@ int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launc
         prof_collect(c);
         if (total_ms) *total_ms = c.prof_ms[stage];
         if (launches) *launches = c.prof_n[stage];
+        return SW_OK;
+    });
+}
+
+int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && stats && B >= 0 && B <= ctx->c.Bmax, "bad argument");
+        SW_CUDA(cudaSetDevice(ctx->c.device));
+        SW_CUDA(cudaDeviceSynchronize());
+        SW_CUDA(cudaMemcpy(stats, ctx->c.dbg, sizeof(int32_t) * 8 * B, cudaMemcpyDeviceToHost));
         return SW_OK;
     });
 }

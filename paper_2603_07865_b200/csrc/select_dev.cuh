@@ -112,11 +112,16 @@ __device__ __forceinline__ GateOut gate_select(int n, const double* sims, const 
 __device__ __forceinline__ double arm_score(const float* __restrict__ theta,
                                             const float* __restrict__ psi, int fd, double beta,
                                             const double* phi, int a, int explore) {
+    (void)fd;  // always kFeatureDim (sw_set_gater enforces it); constant bounds keep phi in registers
     double s = 0.0;
-    for (int i = 0; i < fd; ++i) s = __dadd_rn(s, __dmul_rn((double)theta[a * fd + i], phi[i]));
+#pragma unroll
+    for (int i = 0; i < kFeatureDim; ++i)
+        s = __dadd_rn(s, __dmul_rn((double)theta[a * kFeatureDim + i], phi[i]));
     if (explore) {
         double u = 0.0;
-        for (int i = 0; i < fd; ++i) u = __dadd_rn(u, __dmul_rn((double)psi[a * fd + i], phi[i]));
+#pragma unroll
+        for (int i = 0; i < kFeatureDim; ++i)
+            u = __dadd_rn(u, __dmul_rn((double)psi[a * kFeatureDim + i], phi[i]));
         s = __dadd_rn(s, __dmul_rn(beta, softplus(u)));
     }
     return s;
@@ -225,6 +230,54 @@ __device__ __forceinline__ sw_choice select_one(const HitRec* __restrict__ h, in
     return c;
 }
 
+__device__ __forceinline__ double warp_max_d(double v) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// gate_select with candidate i held by lane i (n <= 32): the same fp64 operations; the two
+// order-dependent sums (softmax total and the cumulative scan) run in candidate order through
+// shuffles, identically in every lane. No per-thread arrays, so nothing lands in local memory.
+__device__ __forceinline__ GateOut gate_select_warp(int n, double sim, double sneg, double dur,
+                                                    double L, double temp, double thr, double u,
+                                                    int lane) {
+    const unsigned full = 0xffffffffu;
+    const bool act = lane < n;
+    const double s_pos = act ? clamp01(sim) : 0.0;
+    const double max_pos = warp_max_d(act ? s_pos : 0.0);          // starts at 0.0
+    const double max_neg_dis = warp_max_d(act ? 1.0 - sneg : 0.0);  // starts at 0.0
+    const double a = max_pos > 0.0 ? __ddiv_rn(s_pos, max_pos) : 0.0;
+    const double b = max_neg_dis > 0.0 ? __ddiv_rn(1.0 - sneg, max_neg_dis) : 0.0;
+    const bool ok = dur >= 0.5 * L && dur <= 1.5 * L;
+    const double q = ok ? fmin(a, b) : 0.0;
+    const unsigned surv = __ballot_sync(full, act && q >= thr);
+    GateOut g{-1, 0u};
+    if (!surv) return g;  // no survivor: miss, and no RNG draw (selector.cpp:67)
+    const bool me = (surv >> lane) & 1u;
+    const double max_s = warp_max_d(me ? s_pos : -INFINITY);
+    const double w = me ? exp(__ddiv_rn(s_pos - max_s, temp)) : 0.0;
+    double total = 0.0;
+    for (int j = 0; j < 32; ++j) {
+        const double wj = __shfl_sync(full, w, j);
+        if ((surv >> j) & 1u) total = __dadd_rn(total, wj);
+    }
+    const double target = __dmul_rn(u, total);
+    const double slack = 1e-13 * total;
+    double acc = 0.0;
+    g.pick = 31 - __clz(surv);  // last survivor (selector.cpp:84)
+    for (int j = 0; j < 32; ++j) {
+        const double wj = __shfl_sync(full, w, j);
+        if (!((surv >> j) & 1u)) continue;
+        acc = __dadd_rn(acc, wj);
+        if (fabs(acc - target) <= slack) g.flags |= SW_CHOICE_AMBIGUOUS_DRAW;
+        if (acc >= target) {
+            g.pick = j;
+            break;
+        }
+    }
+    return g;
+}
+
 // Warp-cooperative select_one for one request: lane 0 runs the gate and the draw (u precomputed),
 // lanes 0..13 score one arm each, and the argmax keeps choose_arm's ">=" rule (ties -> larger
 // arm). The result is valid in lane 0.
@@ -238,18 +291,15 @@ __device__ __forceinline__ sw_choice select_warp(const HitRec* __restrict__ h, i
     }
     nh = min(nh, p.top_k);
     int pick = -1;
-    if (lane == 0 && nh > 0) {
-        double sims[kMaxTopK], sn[kMaxTopK], du[kMaxTopK];
-        for (int i = 0; i < nh; ++i) {
-            sims[i] = h[i].sim;
-            sn[i] = h[i].s_neg;
-            du[i] = h[i].length_s;  // matched segment duration (pipeline.cpp:122)
-        }
-        const GateOut g = gate_select(nh, sims, sn, du, rq.duration_s, p.temp, p.thr, u, nullptr);
+    if (nh > 0) {
+        const bool act = lane < nh;
+        // matched segment duration (pipeline.cpp:122)
+        const GateOut g = gate_select_warp(nh, act ? h[lane].sim : 0.0, act ? h[lane].s_neg : 0.0,
+                                           act ? h[lane].length_s : 0.0, rq.duration_s, p.temp,
+                                           p.thr, u, lane);
         flags |= g.flags;
         pick = g.pick;
     }
-    pick = __shfl_sync(0xffffffffu, pick, 0);
     sw_choice c;
     memset(&c, 0, sizeof(c));
     c.pick = pick;
@@ -268,10 +318,12 @@ __device__ __forceinline__ sw_choice select_warp(const HitRec* __restrict__ h, i
         if (p.policy == SW_POLICY_EXPLOIT || p.policy == SW_POLICY_EXPLORE) {
             double phi[kFeatureDim];
             phi[0] = ch.sim;
+#pragma unroll
             for (int j = 0; j < 8; ++j) phi[1 + j] = ch.phi[j];
             phi[9] = (double)rq.total_steps / 200.0;
             phi[10] = 1.0;
             bool finite = true;
+#pragma unroll
             for (int i = 0; i < kFeatureDim; ++i) finite = finite && isfinite(phi[i]);
             if (!finite) {
                 flags |= SW_CHOICE_NONFINITE_PHI;  // gater.cpp:71-76

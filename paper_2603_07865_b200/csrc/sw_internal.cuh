@@ -126,6 +126,7 @@ struct Ctx {
     int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)
     float* cta_topk = nullptr;      // [Bmax][148][32] each scoring CTA's final top-k (approx)
     double* u_draw = nullptr;       // [Bmax] per-request selector draw
+    int32_t* dbg = nullptr;         // [Bmax][8] per-query finish stats (sw_debug_query_stats)
     int last_chunks = 1;
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]

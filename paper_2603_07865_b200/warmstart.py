@@ -186,6 +186,12 @@ class WarmStartCache:
             out[name] = (ms.value, n.value)
         return out
 
+    def query_stats(self, B: int) -> np.ndarray:
+        """Per-query finish stats of the last search/plan: emitted, kept, phase cycles x4."""
+        out = np.zeros((B, 8), np.int32)
+        check(_lib.lib().sw_debug_query_stats(self._h, B, ptr(out)), "query_stats")
+        return out
+
     def launch_info(self):
         k, t, m = C.c_int32(), C.c_int32(), C.c_int32()
         _lib.lib().sw_last_launch_info(self._h, C.byref(k), C.byref(t), C.byref(m))
