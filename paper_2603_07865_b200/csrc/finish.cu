@@ -1,4 +1,4 @@
-// K2 + K3 fused — everything after the tcgen05 scoring pass, one warp per query:
+// K2 + K3 fused — everything after the tcgen05 scoring pass, one 128-thread CTA per query:
 //
 //  A  certified candidates: T_a = k-th best approximate entry score, taken from the union of the
 //     scoring CTAs' final running lists (the global top-k is inside that union), then every
@@ -19,7 +19,9 @@ namespace sw {
 
 namespace {
 
-constexpr int WPB = 4;  // queries (warps) per CTA
+constexpr int FT = 128;     // threads per query CTA
+constexpr int NWARP = FT / 32;
+constexpr int SMAXC = 512;  // candidates whose exact results stay in shared memory
 
 struct FinishParams {
     int B, k, rank, implicit_all, n_chunks, cap_local, do_select;
@@ -51,6 +53,18 @@ struct FinishParams {
     sw_choice* out;
 };
 
+struct FinSmem {
+    double ex[SMAXC];  // exact similarity per candidate
+    uint64_t id[SMAXC];
+    int32_t slot[SMAXC];
+    int32_t brow[SMAXC];
+    int64_t sel_slot[kMaxTopK];
+    int32_t sel_row[kMaxTopK];
+    double sel_sim[kMaxTopK];
+    float cut;
+    int n, ovf, nh, emitted;
+};
+
 __device__ __forceinline__ bool before(double as, uint64_t aid, double bs, uint64_t bid) {
     return as > bs || (as == bs && aid < bid);
 }
@@ -63,219 +77,161 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
-// fp64 sequential dot of a stored row with the query in shared memory (core.cpp:26-30)
-__device__ __forceinline__ double seq_dot4(const float4* __restrict__ rp,
-                                           const float4* __restrict__ qs4, int n4) {
+// Sequential fp64 dot (core.cpp:26-30) of a global row with the query (doubles in smem), N4
+// float4 steps, with a PF-deep ring of row loads in flight so the chain never waits on memory.
+template <int N4, int PF>
+__device__ __forceinline__ double chain_dot(const float4* __restrict__ rp,
+                                            const double* __restrict__ qd) {
+    float4 ring[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) ring[i] = __ldg(rp + i);
     double s = 0.0;
-#pragma unroll 4
-    for (int d4 = 0; d4 < n4; ++d4) {
-        const float4 x = __ldg(rp + d4);
-        const float4 y = qs4[d4];
-        s = fma((double)y.x, (double)x.x, s);
-        s = fma((double)y.y, (double)x.y, s);
-        s = fma((double)y.z, (double)x.z, s);
-        s = fma((double)y.w, (double)x.w, s);
+#pragma unroll
+    for (int i = 0; i < N4; ++i) {
+        const float4 x = ring[i % PF];
+        if (i + PF < N4) ring[i % PF] = __ldg(rp + i + PF);
+        s = fma(qd[4 * i + 0], (double)x.x, s);
+        s = fma(qd[4 * i + 1], (double)x.y, s);
+        s = fma(qd[4 * i + 2], (double)x.z, s);
+        s = fma(qd[4 * i + 3], (double)x.w, s);
     }
     return s;
 }
 
-constexpr int SCH = 64;         // dims per staged chunk
-constexpr int SPAD = SCH + 4;   // row stride 272 B: 16 B aligned for cp.async, and the 8 lanes of
-                                // each LDS.128 phase hit disjoint banks (row l -> banks 4l..4l+3)
-constexpr int SMAXC = 256;      // candidates whose exact results stay in shared memory
-
-struct WarpSmem {
-    float stage[2][32][SPAD];  // double-buffered: 32 candidate rows x one 64-dim chunk
-    int32_t pref[160];         // prefix of emission-slice sizes
-    double ex[SMAXC];          // exact similarity per candidate
-    int32_t slot[SMAXC];
-    int32_t brow[SMAXC];
-};
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
+                                                const double* __restrict__ qd, int n4) {
+    switch (n4) {
+        case 128: return chain_dot<128, 16>(rp, qd);
+        case 64: return chain_dot<64, 16>(rp, qd);
+        case 32: return chain_dot<32, 16>(rp, qd);
+        case 16: return chain_dot<16, 16>(rp, qd);
+        default: break;
+    }
+    double s = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < n4; ++i) {
+        const float4 x = __ldg(rp + i);
+        s = fma(qd[4 * i + 0], (double)x.x, s);
+        s = fma(qd[4 * i + 1], (double)x.y, s);
+        s = fma(qd[4 * i + 2], (double)x.z, s);
+        s = fma(qd[4 * i + 3], (double)x.w, s);
+    }
+    return s;
 }
 
-// One warp per query: no block barriers, only warp shuffles / ballots.
-__global__ void __launch_bounds__(32 * WPB) k_finish(const FinishParams p) {
-    extern __shared__ float4 dyn[];
-    __shared__ int64_t sel_slot[WPB][kMaxTopK];
-    __shared__ int32_t sel_row[WPB][kMaxTopK];
-    __shared__ double sel_sim[WPB][kMaxTopK];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * WPB + warp;
-    if (b >= p.B) return;
+__global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
+    extern __shared__ double qd[];  // query as doubles, Df
+    __shared__ FinSmem S;
+    const int b = blockIdx.x;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const unsigned full = 0xffffffffu;
-    WarpSmem& W = reinterpret_cast<WarpSmem*>(dyn)[warp];
-    double* qd = reinterpret_cast<double*>(reinterpret_cast<WarpSmem*>(dyn) + WPB) + warp * p.Df;
     const float* qb = p.q + (int64_t)b * p.D;
-    for (int d = lane; d < p.Df; d += 32) qd[d] = d < p.D ? (double)qb[d] : 0.0;
-    __syncwarp();
+    for (int d = t; d < p.Df; d += FT) qd[d] = d < p.D ? (double)qb[d] : 0.0;
+    if (t == 0) {
+        S.n = 0;
+        S.ovf = 0;
+        S.emitted = 0;
+    }
     const int64_t base = (int64_t)b * kCandCap;
     const long long t_start = clock64();
-    int emitted = 0;
 
     // ---------------- A: certified candidate set
-    int64_t n = 0;
-    bool ovf = false;
     if (!p.implicit_all) {
-        // T_a = k-th best approx entry score over the union of the scoring CTAs' final lists
-        const int m = p.n_chunks * p.k;
-        const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
-        float vals[8];
-        int nv = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {  // m <= 256 stays in registers (148 CTAs x 8 = 1184 max)
-            const int i = lane + 32 * u;
-            vals[u] = i < m ? tk[(i / p.k) * kMaxTopK + (i % p.k)] : -INFINITY;
+        if (warp == 0) {  // T_a over the union of the scoring CTAs' final lists
+            const int m = p.n_chunks * p.k;
+            const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
+            unsigned long long prev = ~0ull;
+            float kth = -INFINITY;
+            for (int r = 0; r < p.k; ++r) {
+                unsigned long long best = 0;
+                for (int i = lane; i < m; i += 32) {
+                    const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
+                    if (v == -INFINITY) continue;
+                    const unsigned long long key =
+                        ((unsigned long long)f2ord(v) << 32) | (0xFFFFFFFFu - (uint32_t)i);
+                    if (key < prev && key > best) best = key;
+                }
+                best = warp_max_u64(best);
+                if (best == 0) {  // fewer than k valid entries in the shard: keep everything
+                    kth = -INFINITY;
+                    break;
+                }
+                prev = best;
+                kth = ord2f((uint32_t)(best >> 32));
+            }
+            if (lane == 0) S.cut = kth - 2.0f * p.eps_rel * p.q_norm[b] * ord2f(*p.maxnorm);
         }
-        nv = min(8, (m + 31) / 32);
-        unsigned long long prev = ~0ull;
-        float kth = -INFINITY;
-        for (int r = 0; r < p.k; ++r) {
-            unsigned long long best = 0;
+        __syncthreads();
+        const float cut = S.cut;
+        // warp w filters slices c = w, w+4, ...: 4 scores + 4 slots per lane per load
+        int emitted = 0;
+        for (int c = warp; c < p.n_chunks; c += NWARP) {
+            const int raw = p.slice_cnt[(int64_t)b * p.n_chunks + c];
+            if (raw > p.cap_local && lane == 0) S.ovf = 1;
+            const int cnt = min(raw, p.cap_local);
+            emitted += cnt;
+            const int64_t src = base + (int64_t)c * p.cap_local;  // cap_local % 4 == 0
+            for (int i0 = 0; i0 < cnt; i0 += 128) {
+                const int i = i0 + 4 * lane;
+                float4 sc = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                int4 sl = make_int4(0, 0, 0, 0);
+                if (i < cnt) {
+                    sc = *reinterpret_cast<const float4*>(p.cand_score + src + i);
+                    sl = *reinterpret_cast<const int4*>(p.cand_slot + src + i);
+                }
+                const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+                const int slv[4] = {sl.x, sl.y, sl.z, sl.w};
+                int mine = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (u >= nv || vals[u] == -INFINITY) continue;
-                const unsigned long long key = ((unsigned long long)f2ord(vals[u]) << 32) |
-                                               (0xFFFFFFFFu - (uint32_t)(lane + 32 * u));
-                if (key < prev && key > best) best = key;
-            }
-            for (int i = lane + 256; i < m; i += 32) {  // rare: more than 256 list values
-                const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
-                if (v == -INFINITY) continue;
-                const unsigned long long key =
-                    ((unsigned long long)f2ord(v) << 32) | (0xFFFFFFFFu - (uint32_t)i);
-                if (key < prev && key > best) best = key;
-            }
-            best = warp_max_u64(best);
-            if (best == 0) {  // fewer than k valid entries in the shard: keep everything
-                kth = -INFINITY;
-                break;
-            }
-            prev = best;
-            kth = ord2f((uint32_t)(best >> 32));
-        }
-        const float cut = kth - 2.0f * p.eps_rel * p.q_norm[b] * ord2f(*p.maxnorm);
-        // prefix sums of the slice sizes, then one flattened pass with many loads in flight
-        int run = 0;
-        for (int c0 = 0; c0 < p.n_chunks; c0 += 32) {
-            const int raw = c0 + lane < p.n_chunks
-                                ? p.slice_cnt[(int64_t)b * p.n_chunks + c0 + lane] : 0;
-            ovf = ovf || __any_sync(full, raw > p.cap_local);
-            int v = min(raw, p.cap_local);
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(full, v, o);
-                if (lane >= o) v += t;
-            }
-            if (c0 + lane < p.n_chunks) W.pref[c0 + lane + 1] = run + v;
-            run += __shfl_sync(full, v, 31);
-        }
-        if (lane == 0) W.pref[0] = 0;
-        __syncwarp();
-        const int T = run;
-        emitted = T;
-        for (int t0 = 0; t0 < T; t0 += 32 * 8) {
-            float sc[8];
-            int64_t at[8];
+                for (int u = 0; u < 4; ++u) mine += (i + u < cnt && scv[u] >= cut) ? 1 : 0;
+                int incl = mine;  // warp inclusive scan of per-lane pass counts
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(full, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int tot = __shfl_sync(full, incl, 31);
+                int wbase = 0;
+                if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
+                wbase = __shfl_sync(full, wbase, 0);
+                int pos = wbase + incl - mine;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + 32 * u + lane;
-                sc[u] = -INFINITY;
-                at[u] = -1;
-                if (t < T) {
-                    int lo = 0, hi = p.n_chunks;  // chunk c with pref[c] <= t < pref[c+1]
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (W.pref[mid] <= t) lo = mid; else hi = mid;
+                for (int u = 0; u < 4; ++u) {
+                    if (i + u < cnt && scv[u] >= cut) {
+                        if (pos < SMAXC) S.slot[pos] = slv[u];
+                        p.list[base + pos] = slv[u];
+                        ++pos;
                     }
-                    at[u] = base + (int64_t)lo * p.cap_local + (t - W.pref[lo]);
-                    sc[u] = p.cand_score[at[u]];
                 }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const bool pass = at[u] >= 0 && sc[u] >= cut;
-                const unsigned bal = __ballot_sync(full, pass);
-                if (pass) {
-                    const int64_t j = n + __popc(bal & ((1u << lane) - 1u));
-                    const int32_t sl = p.cand_slot[at[u]];
-                    p.list[base + j] = sl;
-                    if (j < SMAXC) W.slot[j] = sl;
-                }
-                n += __popc(bal);
             }
         }
-        __syncwarp();
-    } else {
-        n = p.n_slots;
+        if (lane == 0) atomicAdd(&S.emitted, emitted);  // every lane summed the same counts
+    } else if (t == 0) {
+        S.n = (int)p.n_slots;
     }
-
+    __syncthreads();
+    const int64_t n = S.n;
     const long long t_a = clock64();
-    // ---------------- B: exact rescoring. Items = (candidate, pyramid row); 32 items per round,
-    // their rows staged cooperatively (coalesced, all loads in flight) 128 dims at a time into
-    // padded shared memory; lane l then runs ITS row's sequential fp64 chain.
+
+    // ---------------- B: exact rescoring, thread = (candidate, pyramid row)
     const int64_t items = n << p.logRp;
-    for (int64_t g0 = 0; g0 < items; g0 += 32) {
-        const int64_t w = g0 + lane;
+    for (int64_t w0 = 0; w0 < items; w0 += FT) {
+        const int64_t w = w0 + t;
         const int64_t i = w >> p.logRp;
         const int r = (int)(w & (p.Rp - 1));
-        int64_t row = -1;
+        double sim = -DBL_MAX;
+        int rw = 0x7fffffff;
+        int64_t slot = -1;
         if (w < items) {
-            const int64_t slot = p.implicit_all ? i
-                                 : (i < SMAXC ? (int64_t)W.slot[i] : (int64_t)p.list[base + i]);
-            if (p.valid[slot] && r < p.nrows[slot]) row = slot * p.Rp + r;
+            slot = p.implicit_all ? i : (i < SMAXC ? (int64_t)S.slot[i] : (int64_t)p.list[base + i]);
+            if (p.valid[slot] && r < p.nrows[slot]) {
+                const double s = chain_dot_any(
+                    reinterpret_cast<const float4*>(p.rows + (slot * p.Rp + r) * p.Df), qd,
+                    p.Df >> 2);
+                sim = fmin(1.0, fmax(-1.0, s));  // core.cpp:35-36
+                rw = r;
+            }
         }
-        double s = 0.0;
-        const int nch = (p.Df + SCH - 1) / SCH;
-        auto issue = [&](int ch) {  // 32 rows x 64 dims, 16 B per lane per row, all in flight
-            const int d0 = ch * SCH;
-            const int dn = min(SCH, p.Df - d0);
-            for (int j = 0; j < 32; ++j) {
-                const int64_t rj = __shfl_sync(full, row, j);
-                if (rj >= 0 && 4 * lane < dn)
-                    cp_async16(&W.stage[ch & 1][j][4 * lane], p.rows + rj * p.Df + d0 + 4 * lane);
-            }
-            cp_async_commit();
-        };
-        __syncwarp();
-        issue(0);
-        for (int ch = 0; ch < nch; ++ch) {
-            if (ch + 1 < nch) {
-                issue(ch + 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncwarp();
-            if (row >= 0) {
-                const int d0 = ch * SCH;
-                const int dn4 = min(SCH, p.Df - d0) >> 2;
-                const float4* sr4 = reinterpret_cast<const float4*>(&W.stage[ch & 1][lane][0]);
-                const double* qq = qd + d0;
-                for (int d4 = 0; d4 < dn4; ++d4) {  // sequential order i = 0..D-1
-                    const float4 x = sr4[d4];
-                    s = fma(qq[4 * d4 + 0], (double)x.x, s);
-                    s = fma(qq[4 * d4 + 1], (double)x.y, s);
-                    s = fma(qq[4 * d4 + 2], (double)x.z, s);
-                    s = fma(qq[4 * d4 + 3], (double)x.w, s);
-                }
-            }
-            __syncwarp();  // the buffer is refilled two chunks later
-        }
-        double sim = row >= 0 ? fmin(1.0, fmax(-1.0, s)) : -DBL_MAX;
-        int rw = row >= 0 ? r : 0x7fffffff;
-        for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest row
+        for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest row (index.cpp:311)
             const double os = __shfl_xor_sync(full, sim, o);
             const int orow = __shfl_xor_sync(full, rw, o);
             if (os > sim || (os == sim && orow < rw)) {
@@ -285,104 +241,113 @@ __global__ void __launch_bounds__(32 * WPB) k_finish(const FinishParams p) {
         }
         if (w < items && r == 0) {
             if (i < SMAXC) {
-                W.ex[i] = sim;
-                W.brow[i] = rw;
-                if (p.implicit_all) W.slot[i] = (int32_t)i;
+                S.ex[i] = sim;
+                S.brow[i] = rw;
+                S.slot[i] = (int32_t)slot;
+                S.id[i] = p.ids[slot];
             } else {
                 p.exact[base + i] = sim;
                 p.best_row[base + i] = rw;
             }
         }
     }
-    __syncwarp();
-
+    __syncthreads();
     const long long t_b = clock64();
-    // ---------------- C: top-k by (sim desc, id asc)
-    double prev_sim = DBL_MAX;
-    uint64_t prev_id = 0;
-    bool have_prev = false;
-    int nh = 0;
-    for (int r = 0; r < p.k; ++r) {
-        double bs = -DBL_MAX;
-        uint64_t bid = ~0ull;
-        int64_t bslot = -1;
-        int brw = 0;
-        for (int64_t i = lane; i < n; i += 32) {
-            const bool sm = i < SMAXC;
-            const int64_t slot = sm ? (int64_t)W.slot[i]
-                                    : (p.implicit_all ? i : (int64_t)p.list[base + i]);
-            const double s = sm ? W.ex[i] : p.exact[base + i];
-            if (s == -DBL_MAX) continue;  // invalid slot or entry without rows
-            const uint64_t id = p.ids[slot];
-            if (have_prev && !before(prev_sim, prev_id, s, id)) continue;
-            if (bslot < 0 || before(s, id, bs, bid)) {
-                bs = s;
-                bid = id;
-                bslot = slot;
-                brw = sm ? W.brow[i] : p.best_row[base + i];
-            }
-        }
-        for (int o = 16; o; o >>= 1) {
-            const double os = __shfl_xor_sync(full, bs, o);
-            const uint64_t oid = __shfl_xor_sync(full, bid, o);
-            const int64_t oslot = __shfl_xor_sync(full, bslot, o);
-            const int orw = __shfl_xor_sync(full, brw, o);
-            if (oslot >= 0 && (bslot < 0 || before(os, oid, bs, bid))) {
-                bs = os;
-                bid = oid;
-                bslot = oslot;
-                brw = orw;
-            }
-        }
-        if (bslot < 0) break;
-        if (lane == 0) {
-            sel_slot[warp][nh] = bslot;
-            sel_row[warp][nh] = brw;
-            sel_sim[warp][nh] = bs;
-        }
-        ++nh;
-        prev_sim = bs;
-        prev_id = bid;
-        have_prev = true;
-    }
-    __syncwarp();
 
-    // ---------------- D: enrichment (8 lanes per hit)
+    // ---------------- C: top-k by (sim desc, id asc) (index.cpp:320-324), warp 0
+    if (warp == 0) {
+        double prev_sim = DBL_MAX;
+        uint64_t prev_id = 0;
+        bool have_prev = false;
+        int nh = 0;
+        for (int r = 0; r < p.k; ++r) {
+            double bs = -DBL_MAX;
+            uint64_t bid = ~0ull;
+            int64_t bslot = -1;
+            int brw = 0;
+            for (int64_t i = lane; i < n; i += 32) {
+                const bool sm = i < SMAXC;
+                const double sv = sm ? S.ex[i] : p.exact[base + i];
+                if (sv == -DBL_MAX) continue;  // invalid slot or entry without rows
+                const int64_t slot = sm ? (int64_t)S.slot[i]
+                                        : (p.implicit_all ? i : (int64_t)p.list[base + i]);
+                const uint64_t id = sm ? S.id[i] : p.ids[slot];
+                if (have_prev && !before(prev_sim, prev_id, sv, id)) continue;
+                if (bslot < 0 || before(sv, id, bs, bid)) {
+                    bs = sv;
+                    bid = id;
+                    bslot = slot;
+                    brw = sm ? S.brow[i] : p.best_row[base + i];
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double os = __shfl_xor_sync(full, bs, o);
+                const uint64_t oid = __shfl_xor_sync(full, bid, o);
+                const int64_t oslot = __shfl_xor_sync(full, bslot, o);
+                const int orw = __shfl_xor_sync(full, brw, o);
+                if (oslot >= 0 && (bslot < 0 || before(os, oid, bs, bid))) {
+                    bs = os;
+                    bid = oid;
+                    bslot = oslot;
+                    brw = orw;
+                }
+            }
+            if (bslot < 0) break;
+            if (lane == 0) {
+                S.sel_slot[nh] = bslot;
+                S.sel_row[nh] = brw;
+                S.sel_sim[nh] = bs;
+            }
+            ++nh;
+            prev_sim = bs;
+            prev_id = bid;
+            have_prev = true;
+        }
+        if (lane == 0) S.nh = nh;
+    }
+    __syncthreads();
+    const int nh = S.nh;
+
+    // ---------------- D: enrichment (8 threads per hit): s_neg + gater block sums
     HitRec* hb = p.hits + (int64_t)b * kMaxTopK;
-    for (int t = lane; t < nh * 8; t += 32) {
-        const int h = t >> 3, j = t & 7;
-        const int64_t row = sel_slot[warp][h] * p.Rp + sel_row[warp][h];
+    for (int tt = t; tt < nh * 8; tt += FT) {
+        const int h = tt >> 3, j = tt & 7;
+        const int64_t row = S.sel_slot[h] * p.Rp + S.sel_row[h];
         const float* rp = p.rows + row * p.Df;
         const size_t lo = (size_t)j * p.D / 8, hi = (size_t)(j + 1) * p.D / 8;
         double s = 0.0;
-        for (size_t i = lo; i < hi; ++i) s = fma(qd[i], (double)rp[i], s);
+        if ((p.D & 31) == 0 && hi - lo == 64 && (lo & 3) == 0) {
+            s = chain_dot<16, 16>(reinterpret_cast<const float4*>(rp + lo), qd + lo);
+        } else {
+            for (size_t i = lo; i < hi; ++i) s = fma(qd[i], (double)rp[i], s);
+        }
         hb[h].phi[j] = s;
         if (j == 0) {
             const sw_segment sg = p.segs[row];
-            hb[h].sim = sel_sim[warp][h];
-            hb[h].entry_id = p.ids[sel_slot[warp][h]];
+            hb[h].sim = S.sel_sim[h];
+            hb[h].entry_id = p.ids[S.sel_slot[h]];
             hb[h].level = sg.level;
-            hb[h].slot = (int32_t)sel_slot[warp][h];
+            hb[h].slot = (int32_t)S.sel_slot[h];
             hb[h].start_s = sg.start_s;
             hb[h].length_s = sg.length_s;
             hb[h].s_neg = p.sneg[row];
-            hb[h].row = sel_row[warp][h];
+            hb[h].row = S.sel_row[h];
             hb[h].owner = p.rank;
         }
     }
-    const int nh_code = ovf ? -nh - 1 : nh;
-    if (lane == 0) p.nhits[b] = nh_code;
-    __syncwarp();
+    const int nh_code = S.ovf ? -nh - 1 : nh;
+    if (t == 0) p.nhits[b] = nh_code;
+    __syncthreads();
     const long long t_d = clock64();
 
-    // ---------------- E: gate + select + Skip Gater + t*
-    if (p.do_select) {
+    // ---------------- E: gate + select + Skip Gater + t* (warp 0)
+    if (p.do_select && warp == 0) {
         const sw_choice c = dev::select_warp(hb, nh_code, p.u_draw[b], p.reqs[b], p.sp, lane);
         if (lane == 0) p.out[b] = c;
     }
-    if (lane == 0) {
+    if (t == 0) {
         int32_t* d = p.dbg + (int64_t)b * 8;
-        d[0] = emitted;
+        d[0] = S.emitted;
         d[1] = (int32_t)n;
         d[2] = (int32_t)(t_a - t_start);
         d[3] = (int32_t)(t_b - t_a);
@@ -421,7 +386,7 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.rank = rank;
     p.implicit_all = tc ? 0 : 1;
     p.n_chunks = c.last_chunks;
-    p.cap_local = kCandCap / c.last_chunks;
+    p.cap_local = (kCandCap / c.last_chunks) & ~3;
     p.do_select = sp != nullptr;
     p.n_slots = c.high_water;
     p.slice_cnt = c.slice_cnt;
@@ -454,14 +419,14 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.out = d_out;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
-        const size_t smem = sizeof(WarpSmem) * WPB + sizeof(double) * c.Df * WPB;
+        const size_t smem = sizeof(double) * c.Df;
         static size_t attr = 0;
         if (smem > attr) {
             SW_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             attr = smem;
         }
-        k_finish<<<(B + WPB - 1) / WPB, 32 * WPB, smem, st>>>(p);
+        k_finish<<<B, FT, smem, st>>>(p);
     }
     SW_CUDA(cudaGetLastError());
     c.last_tc = tc ? 1 : 0;

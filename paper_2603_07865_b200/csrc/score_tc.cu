@@ -376,7 +376,7 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.cand_slot = c.cand_slot;
     p.cand_score = c.cand_score;
     p.n_chunks = (int)chunks;
-    p.cap_local = kCandCap / (int)chunks;
+    p.cap_local = (kCandCap / (int)chunks) & ~3;  // multiple of 4: 16-byte aligned slices
     c.last_chunks = (int)chunks;
     p.eps_rel = kEpsRel;
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;
