@@ -1,4 +1,4 @@
-// K2 + K3 fused — everything after the tcgen05 scoring pass, one 128-thread CTA per query:
+// K2 + K3 fused — everything after the tcgen05 scoring pass, one 2-warp CTA per query:
 //
 //  A  certified candidates: T_a = k-th best approximate entry score, taken from the union of the
 //     scoring CTAs' final running lists (the global top-k is inside that union), then every
@@ -19,9 +19,27 @@ namespace sw {
 
 namespace {
 
-constexpr int FT = 128;     // threads per query CTA
+constexpr int FT = 64;      // threads per query CTA (2 warps)
 constexpr int NWARP = FT / 32;
-constexpr int SMAXC = 512;  // candidates whose exact results stay in shared memory
+constexpr int SMAXC = 256;  // candidates whose exact results stay in shared memory
+constexpr int SC = 32;      // dims per staged chunk of the rescoring ring
+constexpr int SP = SC + 4;  // 144-byte smem rows: 16 B aligned for cp.async; the 8 lanes of each
+                            // LDS.128 phase read rows l..l+7 -> banks 4l..4l+3, conflict-free
+constexpr int NST = 4;      // ring stages per warp
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 struct FinishParams {
     int B, k, rank, implicit_all, n_chunks, cap_local, do_select;
@@ -61,6 +79,7 @@ struct FinSmem {
     int64_t sel_slot[kMaxTopK];
     int32_t sel_row[kMaxTopK];
     double sel_sim[kMaxTopK];
+    HitRec rec[kMaxTopK];  // mirror of the hit records for the select stage
     float cut;
     int n, ovf, nh, emitted;
 };
@@ -119,7 +138,7 @@ __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
     return s;
 }
 
-__global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
+__global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
     extern __shared__ double qd[];  // query as doubles, Df
     __shared__ FinSmem S;
     const int b = blockIdx.x;
@@ -140,11 +159,25 @@ __global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
         if (warp == 0) {  // T_a over the union of the scoring CTAs' final lists
             const int m = p.n_chunks * p.k;
             const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
+            constexpr int NV = 16;  // m <= 512 held in registers (148 CTAs x 8 = 1184 max)
+            float vals[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int i = lane + 32 * u;
+                vals[u] = i < m ? tk[(i / p.k) * kMaxTopK + (i % p.k)] : -INFINITY;
+            }
             unsigned long long prev = ~0ull;
             float kth = -INFINITY;
             for (int r = 0; r < p.k; ++r) {
                 unsigned long long best = 0;
-                for (int i = lane; i < m; i += 32) {
+#pragma unroll
+                for (int u = 0; u < NV; ++u) {
+                    if (vals[u] == -INFINITY) continue;
+                    const unsigned long long key = ((unsigned long long)f2ord(vals[u]) << 32) |
+                                                   (0xFFFFFFFFu - (uint32_t)(lane + 32 * u));
+                    if (key < prev && key > best) best = key;
+                }
+                for (int i = lane + 32 * NV; i < m; i += 32) {  // rare: very wide grids
                     const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
                     if (v == -INFINITY) continue;
                     const unsigned long long key =
@@ -161,45 +194,88 @@ __global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
             }
             if (lane == 0) S.cut = kth - 2.0f * p.eps_rel * p.q_norm[b] * ord2f(*p.maxnorm);
         }
+        // slice sizes of this warp's chunks c = warp + NWARP * j (lane j), loaded before the cut
+        // is known so the round trip overlaps warp 0's T_a selection
+        const int nloc = (p.n_chunks - warp + NWARP - 1) / NWARP;
         __syncthreads();
         const float cut = S.cut;
-        // warp w filters slices c = w, w+4, ...: 4 scores + 4 slots per lane per load
+        const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
         int emitted = 0;
-        for (int c = warp; c < p.n_chunks; c += NWARP) {
-            const int raw = p.slice_cnt[(int64_t)b * p.n_chunks + c];
-            if (raw > p.cap_local && lane == 0) S.ovf = 1;
-            const int cnt = min(raw, p.cap_local);
-            emitted += cnt;
-            const int64_t src = base + (int64_t)c * p.cap_local;  // cap_local % 4 == 0
-            for (int i0 = 0; i0 < cnt; i0 += 128) {
-                const int i = i0 + 4 * lane;
-                float4 sc = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                int4 sl = make_int4(0, 0, 0, 0);
-                if (i < cnt) {
-                    sc = *reinterpret_cast<const float4*>(p.cand_score + src + i);
-                    sl = *reinterpret_cast<const int4*>(p.cand_slot + src + i);
-                }
-                const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
-                const int slv[4] = {sl.x, sl.y, sl.z, sl.w};
-                int mine = 0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) mine += (i + u < cnt && scv[u] >= cut) ? 1 : 0;
-                int incl = mine;  // warp inclusive scan of per-lane pass counts
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(full, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const int tot = __shfl_sync(full, incl, 31);
-                int wbase = 0;
-                if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
-                wbase = __shfl_sync(full, wbase, 0);
-                int pos = wbase + incl - mine;
+        for (int j0 = 0; j0 < nloc; j0 += 32) {
+            const int cj = warp + NWARP * (j0 + lane);
+            const int raw = j0 + lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + cj] : 0;
+            if (__any_sync(full, raw > p.cap_local) && lane == 0) S.ovf = 1;
+            const int my_cnt = min(raw, p.cap_local);
+            const int jn = min(32, nloc - j0);
+            // 4 chunks x 2 segments of 128 entries in flight per lane
+            for (int jg = 0; jg < jn; jg += 4) {
+                float4 sc[4][2];
+                int4 sl[4][2];
+                int cnt[4];
+                int64_t src[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    if (i + u < cnt && scv[u] >= cut) {
-                        if (pos < SMAXC) S.slot[pos] = slv[u];
-                        p.list[base + pos] = slv[u];
-                        ++pos;
+                    const int j = jg + u;
+                    cnt[u] = __shfl_sync(full, my_cnt, j < jn ? j : 0);
+                    if (j >= jn) cnt[u] = 0;
+                    src[u] = base + (int64_t)(warp + NWARP * (j0 + j)) * p.cap_local;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = 128 * h + 4 * lane;
+                        sc[u][h] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                        sl[u][h] = make_int4(0, 0, 0, 0);
+                        if (i < cnt[u]) {
+                            sc[u][h] = *reinterpret_cast<const float4*>(p.cand_score + src[u] + i);
+                            sl[u][h] = *reinterpret_cast<const int4*>(p.cand_slot + src[u] + i);
+                        }
+                    }
+                }
+                auto consume = [&](int cn, int i0, float4 sv, int4 lv) {
+                    const int i = i0 + 4 * lane;
+                    const float scv[4] = {sv.x, sv.y, sv.z, sv.w};
+                    const int slv[4] = {lv.x, lv.y, lv.z, lv.w};
+                    int mine = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) mine += (i + e < cn && scv[e] >= cut) ? 1 : 0;
+                    int incl = mine;  // warp inclusive scan of per-lane pass counts
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_up_sync(full, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const int tot = __shfl_sync(full, incl, 31);
+                    int wbase = 0;
+                    if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
+                    wbase = __shfl_sync(full, wbase, 0);
+                    int pos = wbase + incl - mine;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (i + e < cn && scv[e] >= cut) {
+                            if (pos < SMAXC) S.slot[pos] = slv[e];
+                            p.list[base + pos] = slv[e];
+                            // pull the candidate's rows into L2 now; phase B stages them
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                             p.rows + (int64_t)slv[e] * p.Rp * p.Df),
+                                         "r"((uint32_t)row_bytes)
+                                         : "memory");
+                            ++pos;
+                        }
+                    }
+                };
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    emitted += cnt[u];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (128 * h < cnt[u]) consume(cnt[u], 128 * h, sc[u][h], sl[u][h]);
+                    for (int i0 = 256; i0 < cnt[u]; i0 += 128) {  // rare: slices > 256 entries
+                        const int i = i0 + 4 * lane;
+                        float4 sv = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                        int4 lv = make_int4(0, 0, 0, 0);
+                        if (i < cnt[u]) {
+                            sv = *reinterpret_cast<const float4*>(p.cand_score + src[u] + i);
+                            lv = *reinterpret_cast<const int4*>(p.cand_slot + src[u] + i);
+                        }
+                        consume(cnt[u], i0, sv, lv);
                     }
                 }
             }
@@ -212,25 +288,68 @@ __global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
     const int64_t n = S.n;
     const long long t_a = clock64();
 
-    // ---------------- B: exact rescoring, thread = (candidate, pyramid row)
+    // ---------------- B: exact rescoring. Warp w takes groups of 32 items (candidate, pyramid
+    // row), g = w, w + NWARP, ...; the 32 rows are staged 32 dims at a time through an NST-deep
+    // cp.async ring (coalesced 128-byte row segments), and lane l runs ITS row's sequential fp64
+    // chain from shared memory.
     const int64_t items = n << p.logRp;
-    for (int64_t w0 = 0; w0 < items; w0 += FT) {
-        const int64_t w = w0 + t;
+    float* ring = reinterpret_cast<float*>(qd + p.Df) + (size_t)warp * NST * 32 * SP;
+    const int nch = (p.Df + SC - 1) / SC;
+    for (int64_t g0 = (int64_t)warp * 32; g0 < items; g0 += FT) {
+        const int64_t w = g0 + lane;
         const int64_t i = w >> p.logRp;
         const int r = (int)(w & (p.Rp - 1));
-        double sim = -DBL_MAX;
-        int rw = 0x7fffffff;
-        int64_t slot = -1;
+        int64_t row = -1, slot = -1;
         if (w < items) {
             slot = p.implicit_all ? i : (i < SMAXC ? (int64_t)S.slot[i] : (int64_t)p.list[base + i]);
-            if (p.valid[slot] && r < p.nrows[slot]) {
-                const double s = chain_dot_any(
-                    reinterpret_cast<const float4*>(p.rows + (slot * p.Rp + r) * p.Df), qd,
-                    p.Df >> 2);
-                sim = fmin(1.0, fmax(-1.0, s));  // core.cpp:35-36
-                rw = r;
-            }
+            if (p.valid[slot] && r < p.nrows[slot]) row = slot * p.Rp + r;
         }
+        // lane l stages float4 (l & 7) of rows (l >> 3) + 4u, u = 0..7
+        const float* src[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t rj = __shfl_sync(full, row, (lane >> 3) + 4 * u);
+            src[u] = rj >= 0 ? p.rows + rj * p.Df + 4 * (lane & 7) : nullptr;
+        }
+        auto issue = [&](int ch) {
+            if (ch < nch) {
+                const int d0 = ch * SC;
+                float* dst = ring + (size_t)(ch % NST) * 32 * SP + 4 * (lane & 7);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (src[u] && d0 + 4 * (lane & 7) < p.Df)
+                        cp_async16(dst + ((lane >> 3) + 4 * u) * SP, src[u] + d0);
+            }
+            cp_async_commit();  // empty groups keep the wait count uniform
+        };
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < NST - 1; ++c) issue(c);
+        double s = 0.0;
+        for (int ch = 0; ch < nch; ++ch) {
+            issue(ch + NST - 1);
+            cp_async_wait<NST - 1>();
+            __syncwarp();
+            if (row >= 0) {
+                const float4* sr4 =
+                    reinterpret_cast<const float4*>(ring + ((size_t)(ch % NST) * 32 + lane) * SP);
+                const double* qq = qd + ch * SC;
+                const int dn4 = min(SC, p.Df - ch * SC) >> 2;
+#pragma unroll
+                for (int d4 = 0; d4 < SC / 4; ++d4) {  // sequential order i = 0..D-1
+                    if (d4 < dn4) {
+                        const float4 x = sr4[d4];
+                        s = fma(qq[4 * d4 + 0], (double)x.x, s);
+                        s = fma(qq[4 * d4 + 1], (double)x.y, s);
+                        s = fma(qq[4 * d4 + 2], (double)x.z, s);
+                        s = fma(qq[4 * d4 + 3], (double)x.w, s);
+                    }
+                }
+            }
+            __syncwarp();  // this ring slot is refilled NST - 1 chunks later
+        }
+        double sim = row >= 0 ? fmin(1.0, fmax(-1.0, s)) : -DBL_MAX;  // core.cpp:35-36
+        int rw = row >= 0 ? r : 0x7fffffff;
         for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest row (index.cpp:311)
             const double os = __shfl_xor_sync(full, sim, o);
             const int orow = __shfl_xor_sync(full, rw, o);
@@ -315,34 +434,48 @@ __global__ void __launch_bounds__(FT, 3) k_finish(const FinishParams p) {
         const int64_t row = S.sel_slot[h] * p.Rp + S.sel_row[h];
         const float* rp = p.rows + row * p.Df;
         const size_t lo = (size_t)j * p.D / 8, hi = (size_t)(j + 1) * p.D / 8;
+        sw_segment sg;
+        double sn = 0.0;
+        uint64_t eid = 0;
+        if (j == 0) {  // issued before the chain so their latency overlaps it
+            sg = p.segs[row];
+            sn = p.sneg[row];
+            eid = p.ids[S.sel_slot[h]];
+        }
         double s = 0.0;
         if ((p.D & 31) == 0 && hi - lo == 64 && (lo & 3) == 0) {
             s = chain_dot<16, 16>(reinterpret_cast<const float4*>(rp + lo), qd + lo);
         } else {
             for (size_t i = lo; i < hi; ++i) s = fma(qd[i], (double)rp[i], s);
         }
-        hb[h].phi[j] = s;
+        S.rec[h].phi[j] = s;
         if (j == 0) {
-            const sw_segment sg = p.segs[row];
-            hb[h].sim = S.sel_sim[h];
-            hb[h].entry_id = p.ids[S.sel_slot[h]];
-            hb[h].level = sg.level;
-            hb[h].slot = (int32_t)S.sel_slot[h];
-            hb[h].start_s = sg.start_s;
-            hb[h].length_s = sg.length_s;
-            hb[h].s_neg = p.sneg[row];
-            hb[h].row = S.sel_row[h];
-            hb[h].owner = p.rank;
+            HitRec& o = S.rec[h];
+            o.sim = S.sel_sim[h];
+            o.entry_id = eid;
+            o.level = sg.level;
+            o.slot = (int32_t)S.sel_slot[h];
+            o.start_s = sg.start_s;
+            o.length_s = sg.length_s;
+            o.s_neg = sn;
+            o.row = S.sel_row[h];
+            o.owner = p.rank;
         }
     }
     const int nh_code = S.ovf ? -nh - 1 : nh;
     if (t == 0) p.nhits[b] = nh_code;
     __syncthreads();
+    {  // copy the smem records out (16-byte words)
+        const int nw = nh * (int)(sizeof(HitRec) / 16);
+        const int4* srcw = reinterpret_cast<const int4*>(S.rec);
+        int4* dstw = reinterpret_cast<int4*>(hb);
+        for (int i = t; i < nw; i += FT) dstw[i] = srcw[i];
+    }
     const long long t_d = clock64();
 
     // ---------------- E: gate + select + Skip Gater + t* (warp 0)
-    if (p.do_select && warp == 0) {
-        const sw_choice c = dev::select_warp(hb, nh_code, p.u_draw[b], p.reqs[b], p.sp, lane);
+    if (p.do_select && warp == 0) {  // (phase D covered 8 hits x 8 block sums in one pass)
+        const sw_choice c = dev::select_warp(S.rec, nh_code, p.u_draw[b], p.reqs[b], p.sp, lane);
         if (lane == 0) p.out[b] = c;
     }
     if (t == 0) {
@@ -419,7 +552,7 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.out = d_out;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
-        const size_t smem = sizeof(double) * c.Df;
+        const size_t smem = sizeof(double) * c.Df + sizeof(float) * NWARP * NST * 32 * SP;
         static size_t attr = 0;
         if (smem > attr) {
             SW_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
