@@ -42,7 +42,7 @@ __global__ void k_insert_rows(int64_t n, const int64_t* __restrict__ slot_of,
                               double* __restrict__ sneg, sw_segment* __restrict__ segs,
                               uint64_t* __restrict__ slot_ids, int32_t* __restrict__ slot_nrows,
                               uint8_t* __restrict__ valid, uint32_t* __restrict__ valid_bits,
-                              uint32_t* __restrict__ maxnorm,
+                              uint32_t* __restrict__ norms,
                               const float* __restrict__ neg, int have_neg, int D, int Df, int Dp,
                               int Rp) {
     int64_t e = blockIdx.x;
@@ -68,10 +68,18 @@ __global__ void k_insert_rows(int64_t n, const int64_t* __restrict__ slot_of,
     for (int r = threadIdx.x; r < nr; r += blockDim.x) {
         const int64_t dst = slot * Rp + base + r;
         const float* df = rows + dst * Df;
-        double nn = 0.0;
-        for (int d = 0; d < D; ++d) nn = fma((double)df[d], (double)df[d], nn);
-        float nf = (float)sqrt(nn) * (1.0f + 1e-6f);
-        atomicMax(maxnorm, f2ord(nf));
+        // |e|, |e - bf16(e)|, |bf16(e)|: the data-dependent terms of the tcgen05 error bound
+        double nn = 0.0, dd = 0.0, bb = 0.0;
+        for (int d = 0; d < D; ++d) {
+            const double x = (double)df[d];
+            const double xb = (double)__bfloat162float(__float2bfloat16_rn(df[d]));
+            nn = fma(x, x, nn);
+            dd = fma(x - xb, x - xb, dd);
+            bb = fma(xb, xb, bb);
+        }
+        atomicMax(&norms[0], f2ord((float)sqrt(nn) * (1.0f + 1e-6f)));
+        atomicMax(&norms[1], f2ord((float)sqrt(dd) * (1.0f + 1e-6f)));
+        atomicMax(&norms[2], f2ord((float)sqrt(bb) * (1.0f + 1e-6f)));
         sneg[dst] = have_neg ? clamp01(clamp_cos(seq_dot(df, neg, D))) : 0.0;
     }
     // pad rows repeat row 0 in the bf16 shadow (approximate per-entry max unaffected)
@@ -245,7 +253,7 @@ void launch_insert_rows_full(Ctx& c, int64_t n, const int64_t* d_slot, const int
         k_insert_rows<<<(unsigned)m, 128, 0, st>>>(
             m, d_slot + off, d_base ? d_base + off : nullptr, d_row_off + off, d_ids + off,
             d_rows, d_segs, c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid,
-            c.valid_bits, c.maxnorm, c.neg, c.have_neg ? 1 : 0, c.D, c.Df, c.Dp, c.Rp);
+            c.valid_bits, c.norms, c.neg, c.have_neg ? 1 : 0, c.D, c.Df, c.Dp, c.Rp);
     }
     SW_CUDA(cudaGetLastError());
 }

@@ -61,7 +61,7 @@ static void default_schedule(std::vector<double>& abar) {
 static void free_ctx(Ctx& c) {
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
                     c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
-                    c.latent, c.maxnorm, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm,
+                    c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
     for (void* p : ptrs)
@@ -109,12 +109,13 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.tsrc, (size_t)c.S);
     if (c.C > 0 && c.Tmax > 0 && c.F > 0)
         dalloc(&c.latent, (size_t)c.Lslots * c.C * c.Tmax * c.F);
-    dalloc(&c.maxnorm, 1);
+    dalloc(&c.norms, 4);
     dalloc(&c.neg, (size_t)c.Df);
     dalloc(&c.theta, kNumArms * kFeatureDim);
     dalloc(&c.psi, kNumArms * kFeatureDim);
     dalloc(&c.q_bf, (size_t)c.BmaxPad * c.Dp);
     dalloc(&c.q_norm, (size_t)c.Bmax);
+    dalloc(&c.q_eps, (size_t)c.Bmax);
     dalloc(&c.thr, (size_t)c.Bmax);
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
     dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
@@ -141,8 +142,8 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     SW_CUDA(cudaMemsetAsync(c.neg, 0, sizeof(float) * c.Df, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.theta, 0, sizeof(float) * kNumArms * kFeatureDim, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.psi, 0, sizeof(float) * kNumArms * kFeatureDim, c.mstream));
-    const uint32_t zero_norm = f2ord(0.0f);
-    SW_CUDA(cudaMemcpyAsync(c.maxnorm, &zero_norm, 4, cudaMemcpyHostToDevice, c.mstream));
+    const uint32_t zero_norm[4] = {f2ord(0.0f), f2ord(0.0f), f2ord(0.0f), f2ord(0.0f)};
+    SW_CUDA(cudaMemcpyAsync(c.norms, zero_norm, 16, cudaMemcpyHostToDevice, c.mstream));
     std::vector<double> ab;
     default_schedule(ab);
     dalloc(&c.abar, ab.size());

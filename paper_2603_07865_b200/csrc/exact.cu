@@ -22,31 +22,48 @@ __device__ __forceinline__ double clamp_cos(double v) {
 
 __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
                        __nv_bfloat16* __restrict__ q_bf, float* __restrict__ q_norm,
-                       uint32_t* __restrict__ thr, int32_t* __restrict__ cand_n,
-                       const sw_request* __restrict__ req, uint64_t seed,
-                       double* __restrict__ u_draw) {
+                       float* __restrict__ q_eps, const uint32_t* __restrict__ norms,
+                       uint32_t* __restrict__ thr, const sw_request* __restrict__ req,
+                       uint64_t seed, double* __restrict__ u_draw) {
     const int b = blockIdx.x;
     if (b >= B) return;
     // the request's selector draw Rng(derive_seed(seed, id, 2)).uniform() (pipeline.cpp:211),
     // computed here by one lane of warp 1 so its 156-step MT seeding overlaps the conversion
     if (req && threadIdx.x == 32) u_draw[b] = dev::uniform_draw(dev::derive_seed(seed, req[b].id, 2, 0));
-    __shared__ double red[32];
+    __shared__ double red[3][32];
     const float* qb = q + (int64_t)b * D;
-    double s = 0.0;
+    double nn = 0.0, dd = 0.0, bb = 0.0;
     for (int d = threadIdx.x; d < Dp; d += blockDim.x) {
-        float v = d < D ? qb[d] : 0.0f;
-        q_bf[(int64_t)b * Dp + d] = __float2bfloat16_rn(v);
-        s += (double)v * v;
+        const float v = d < D ? qb[d] : 0.0f;
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        q_bf[(int64_t)b * Dp + d] = h;
+        const double x = v, xb = (double)__bfloat162float(h);
+        nn += x * x;
+        dd += (x - xb) * (x - xb);
+        bb += xb * xb;
     }
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    for (int o = 16; o; o >>= 1) {
+        nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        dd += __shfl_xor_sync(0xffffffffu, dd, o);
+        bb += __shfl_xor_sync(0xffffffffu, bb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = nn;
+        red[1][threadIdx.x >> 5] = dd;
+        red[2][threadIdx.x >> 5] = bb;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        q_norm[b] = (float)sqrt(t) * (1.0f + 1e-6f);
+        double t[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            for (int j = 0; j < 3; ++j) t[j] += red[j][w];
+        const double qn = sqrt(t[0]), qd = sqrt(t[1]), qbn = sqrt(t[2]);
+        const double en = ord2f(norms[0]), ed = ord2f(norms[1]), ebn = ord2f(norms[2]);
+        (void)en;
+        const double eps = (qn * ed + qd * ebn + (double)kAccSlack * qbn * ebn) * (1.0 + 1e-5) + 1e-12;
+        q_norm[b] = (float)qn * (1.0f + 1e-6f);
+        q_eps[b] = (float)eps * (1.0f + 1e-6f);
         thr[b] = f2ord(-INFINITY);
-        cand_n[b] = 0;
     }
 }
 
@@ -76,8 +93,8 @@ __global__ void k_hits_to_public(int B, int k, const HitRec* __restrict__ hits,
 int launch_prep(Ctx& c, const float* d_q, int B, const sw_request* d_req, uint64_t seed,
                 cudaStream_t st) {
     StageScope sc(c, SW_STAGE_PREP, st);
-    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.thr, c.cand_n, d_req, seed,
-                              c.u_draw);
+    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.q_eps, c.norms, c.thr, d_req,
+                              seed, c.u_draw);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

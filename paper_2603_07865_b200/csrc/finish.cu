@@ -48,9 +48,7 @@ struct FinishParams {
     const int32_t* cand_slot;
     const float* cand_score;
     const float* cta_topk;
-    const float* q_norm;
-    const uint32_t* maxnorm;
-    float eps_rel;
+    const float* q_eps;
     const float* q;
     int D, Df, Rp, logRp;
     const float* rows;
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                 prev = best;
                 kth = ord2f((uint32_t)(best >> 32));
             }
-            if (lane == 0) S.cut = kth - 2.0f * p.eps_rel * p.q_norm[b] * ord2f(*p.maxnorm);
+            if (lane == 0) S.cut = kth - 2.0f * p.q_eps[b];
         }
         // slice sizes of this warp's chunks c = warp + NWARP * j (lane j), loaded before the cut
         // is known so the round trip overlaps warp 0's T_a selection
@@ -526,9 +524,7 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.cand_slot = c.cand_slot;
     p.cand_score = c.cand_score;
     p.cta_topk = c.cta_topk;
-    p.q_norm = c.q_norm;
-    p.maxnorm = c.maxnorm;
-    p.eps_rel = kEpsRel;
+    p.q_eps = c.q_eps;
     p.q = d_q;
     p.D = c.D;
     p.Df = c.Df;

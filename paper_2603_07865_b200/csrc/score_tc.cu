@@ -40,8 +40,7 @@ struct TcParams {
     int64_t tiles_per_cta;
     int64_t n_slots;  // high-water slot count
     const uint32_t* valid_bits;  // one bit per slot
-    const float* q_norm;
-    const uint32_t* maxnorm;
+    const float* q_eps;
     uint32_t* thr;
     int32_t* slice_cnt;  // [B][n_chunks] emissions per (query, CTA)
     float* cta_topk;     // [B][n_chunks][32] final running lists
@@ -49,7 +48,6 @@ struct TcParams {
     float* cand_score;
     int n_chunks;
     int cap_local;
-    float eps_rel;
 };
 
 // Emission + running top-list update for the entries of one 32-column chunk whose approximate
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int q = qblock * BM + quarter * 32 + lane;
         const bool qvalid = q < p.B;
         float eps2 = 0.0f;
-        if (qvalid) eps2 = 2.0f * p.eps_rel * p.q_norm[q] * ord2f(*p.maxnorm);
+        if (qvalid) eps2 = 2.0f * p.q_eps[q];
         float theta = -INFINITY, kth = -INFINITY, published = -INFINITY;
         // descending list; the top KL - k slots are +inf so list[KL-1] is always the k-th best
         float list[KL];
@@ -368,8 +366,7 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     chunks = (p.n_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
     p.n_slots = c.high_water;
     p.valid_bits = c.valid_bits;
-    p.q_norm = c.q_norm;
-    p.maxnorm = c.maxnorm;
+    p.q_eps = c.q_eps;
     p.thr = c.thr;
     p.slice_cnt = c.slice_cnt;
     p.cta_topk = c.cta_topk;
@@ -378,7 +375,6 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.n_chunks = (int)chunks;
     p.cap_local = (kCandCap / (int)chunks) & ~3;  // multiple of 4: 16-byte aligned slices
     c.last_chunks = (int)chunks;
-    p.eps_rel = kEpsRel;
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;
     dim3 grid((unsigned)qblocks, (unsigned)chunks);
     switch (c.Rp) {

@@ -47,9 +47,10 @@ constexpr int kFeatureDim = 11;       // gater.hpp:28
 constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep running list
 constexpr int kCandCap = 16384;       // emitted candidates per query (split over the CTAs)
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
-// |bf16 dot - fp64 dot| <= kEpsRel * |q| * max|row|: bf16 rounding of both operands
-// (2u + u^2, u = 2^-8) plus fp32 tensor-core accumulation slack over K <= 512
-constexpr float kEpsRel = 0.0081f;
+// Certified error of a tcgen05 score: |q.e - q~.e~| <= |q| |e - e~| + |q - q~| |e~|
+// (Cauchy-Schwarz on q.e - q~.e~ = q.(e - e~) + (q - q~).e~, ~ = bf16) plus the fp32 tensor-core
+// accumulation slack kAccSlack * |q~| |e~| (K <= 512 additions at <= 2^-23 relative each, x2).
+constexpr float kAccSlack = 0x1.0p-12f;
 
 // Per-shard top-k record (SW_HIT_RECORD_BYTES = 128): everything the replicated select /
 // gater stage needs, so the all-gather carries no embeddings.
@@ -108,7 +109,7 @@ struct Ctx {
     uint32_t* valid_bits = nullptr;   // [S/32 + pad] one bit per slot (read by the tcgen05 epilogue)
     int32_t* tsrc = nullptr;          // [S]
     float* latent = nullptr;          // [Lslots][C][Tmax][F]
-    uint32_t* maxnorm = nullptr;      // ordered float bits, max row L2 norm
+    uint32_t* norms = nullptr;        // ordered floats: max |e|, max |e - bf16(e)|, max |bf16(e)|
     float* neg = nullptr;             // [Df]
     float* theta = nullptr;           // [14*11]
     float* psi = nullptr;
@@ -121,6 +122,7 @@ struct Ctx {
     // batch scratch
     __nv_bfloat16* q_bf = nullptr;  // [BmaxPad][Dp]
     float* q_norm = nullptr;        // [Bmax]
+    float* q_eps = nullptr;         // [Bmax] certified |bf16 score - fp64 score| bound per query
     uint32_t* thr = nullptr;        // [Bmax] shared running k-th best (ordered)
     int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
     int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)

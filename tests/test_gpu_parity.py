@@ -50,6 +50,25 @@ def test_search_matches_oracle(orc, mode, dim, delta, clustered, n):
         _check_hits(hits, cnt, _arena(c), orc, q, k)
 
 
+@pytest.mark.parametrize("scale", [0.25, 3.7])
+def test_search_nonunit_and_near_ties_tc(orc, scale):
+    """Certified over-fetch with non-unit rows/queries (the error bound scales with the norms)
+    and near-tied entries (tiny perturbations of one vector)."""
+    rng = np.random.default_rng(5)
+    c = SynthCache(2000, 128, 1.0, seed=12, clustered=True)
+    base = c.rows[0].astype(np.float64)
+    for e in range(1, 200):  # 200 near-duplicates of row 0 at distance ~1e-4
+        v = base + 1e-4 * rng.standard_normal(128)
+        c.rows[e] = (v / np.linalg.norm(v)).astype(np.float32)
+    c.rows *= np.float32(scale)
+    wc = _cache(c, max_batch=64, tc_always=True)
+    q = perturbed_queries(c, 64, scale=0.01) * np.float32(1.0 / scale)
+    q[:8] = c.rows[:8] / np.float32(scale)
+    hits, cnt = wc.search(q, 8)
+    assert wc.launch_info()["tensor_cores"]
+    _check_hits(hits, cnt, _arena(c), orc, q, 8)
+
+
 def test_search_tc_default_large(orc):
     # 40K entries x 1 row: default mode picks the tcgen05 pre-filter
     c = SynthCache(40000, 512, 1.0, seed=8, clustered=True)
