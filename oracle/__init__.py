@@ -44,7 +44,7 @@ def build(force: bool = False) -> None:
     import subprocess
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "dropin"]  # dropin links the freshly built libsemwarm_b200.so
     subprocess.check_call(["make", "-s", "-C", HERE] + (["-B"] if force else []) + targets)
 
 
