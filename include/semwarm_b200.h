@@ -249,6 +249,51 @@ int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats);
 int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
                         int32_t* candidates_max);
 
+/* ---------------------------------------------------------------- Cache Manager (host policy)
+ * CacheManager (cache.hpp:45-106) over a context's arena: the policy stays on the host exactly
+ * as in the reference; admit / evict / refine land in the arena through sw_arena_*. */
+typedef struct swcm_cache swcm_cache;
+typedef struct swcm_config { /* CacheConfig (cache.hpp:31-42) */
+    uint64_t capacity;
+    double decay_per_hour;
+    double grace_hours;
+    double quality_floor;
+    double pyramid_delta;
+    uint64_t embedding_seed;  /* derive_seed(seed, "SEGM") in the reference (pipeline.cpp:76-78) */
+    int32_t refine_regenerations;
+    int32_t refine_attempt_cap;
+    int32_t refine_window;
+    int32_t reserved;
+    double refine_skip_threshold;
+    int64_t latent_capacity;  /* floats the regenerate callback may write (0: no latents) */
+} swcm_config;
+/* RegenerateFn (cache.hpp:47-49): fill embedding (dim floats), quality, optional latent. */
+typedef int (*swcm_regenerate_fn)(void* user, const float* prompt, int32_t dim, double duration_s,
+                                  uint64_t seed, float* embedding_out, double* quality_out,
+                                  float* latent_out, int32_t* t_src_out);
+int swcm_create(sw_ctx* ctx, int32_t dim, const swcm_config* cfg, swcm_cache** out);
+int swcm_destroy(swcm_cache* cache);
+/* CacheManager::admit (cache.cpp:30-52): returns 1 admitted (*id_out set), 0 rejected. */
+int swcm_admit(swcm_cache* cache, const float* clip_embedding, double duration_s,
+               const float* prompt_embedding, double quality, double now_h, const float* latent,
+               int32_t t_src, uint64_t* id_out);
+int swcm_last_evicted(const swcm_cache* cache, uint64_t* out, int32_t cap);
+/* CacheManager::record_reuse (cache.cpp:54-68) */
+int swcm_record_reuse(swcm_cache* cache, uint64_t entry_id, int32_t steps_skipped,
+                      double duration_s, double now_h, double skip_fraction);
+/* CacheManager::evict_if_full (cache.cpp:70-105): returns the number evicted */
+int swcm_evict_if_full(swcm_cache* cache, double now_h, uint64_t* out, int32_t cap);
+/* CacheManager::refinement_candidates (cache.cpp:142-154) */
+int swcm_refinement_candidates(const swcm_cache* cache, uint64_t* out, int32_t cap);
+/* CacheManager::refine (cache.cpp:107-140) with Rng(rng_seed); *replaced = 1 if the stored
+ * entry was replaced. SW_WARN_UNKNOWN_ID for an unknown id (warn + no-op). */
+int swcm_refine(swcm_cache* cache, uint64_t entry_id, uint64_t rng_seed, swcm_regenerate_fn regen,
+                void* user, int32_t* replaced);
+int swcm_importance(const swcm_cache* cache, uint64_t entry_id, double now_h, double* out);
+int swcm_size(const swcm_cache* cache);
+int swcm_ids(const swcm_cache* cache, uint64_t* out, int32_t cap);
+int swcm_check_consistent(const swcm_cache* cache);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,10 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
 
 
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    cu = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu")]
+    host = os.path.join(CSRC, "host")
+    cpp = [os.path.join(host, f) for f in os.listdir(host) if f.endswith(".cpp")]
+    return sorted(cu) + sorted(cpp)
 
 
 def _stale(target, deps):
@@ -43,7 +46,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
             cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]

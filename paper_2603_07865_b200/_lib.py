@@ -49,6 +49,20 @@ class SwPolicy(C.Structure):
                 ("rule_similarity_threshold", C.c_double), ("rule_skip_fraction", C.c_double)]
 
 
+class SwcmConfig(C.Structure):
+    _fields_ = [("capacity", C.c_uint64), ("decay_per_hour", C.c_double),
+                ("grace_hours", C.c_double), ("quality_floor", C.c_double),
+                ("pyramid_delta", C.c_double), ("embedding_seed", C.c_uint64),
+                ("refine_regenerations", C.c_int32), ("refine_attempt_cap", C.c_int32),
+                ("refine_window", C.c_int32), ("reserved", C.c_int32),
+                ("refine_skip_threshold", C.c_double), ("latent_capacity", C.c_int64)]
+
+
+REGEN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_uint64,
+                       C.POINTER(C.c_float), C.POINTER(C.c_double), C.POINTER(C.c_float),
+                       C.POINTER(C.c_int32))
+
+
 # numpy mirrors of the array-of-struct types
 SEGMENT_DTYPE = np.dtype([("level", "<i4"), ("reserved", "<i4"), ("start_s", "<f8"),
                           ("length_s", "<f8")])
@@ -118,6 +132,18 @@ def lib() -> C.CDLL:
         "sw_last_launch_info": ([vp, vp, vp, vp], C.c_int),
         "sw_profile_enable": ([vp, i32], C.c_int),
         "sw_debug_query_stats": ([vp, i32, vp], C.c_int),
+        "swcm_create": ([vp, i32, C.POINTER(SwcmConfig), C.POINTER(vp)], C.c_int),
+        "swcm_destroy": ([vp], C.c_int),
+        "swcm_admit": ([vp, vp, f64, vp, f64, f64, vp, i32, C.POINTER(u64)], C.c_int),
+        "swcm_last_evicted": ([vp, vp, i32], C.c_int),
+        "swcm_record_reuse": ([vp, u64, i32, f64, f64, f64], C.c_int),
+        "swcm_evict_if_full": ([vp, f64, vp, i32], C.c_int),
+        "swcm_refinement_candidates": ([vp, vp, i32], C.c_int),
+        "swcm_refine": ([vp, u64, u64, REGEN_FN, vp, C.POINTER(i32)], C.c_int),
+        "swcm_importance": ([vp, u64, f64, C.POINTER(f64)], C.c_int),
+        "swcm_size": ([vp], C.c_int),
+        "swcm_ids": ([vp, vp, i32], C.c_int),
+        "swcm_check_consistent": ([vp], C.c_int),
         "sw_profile_reset": ([vp], C.c_int),
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
     }
@@ -137,6 +163,9 @@ EXPORTED = [
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host", "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
+    "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",
+    "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
+    "swcm_size", "swcm_ids", "swcm_check_consistent",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

@@ -294,3 +294,98 @@ class WarmStartCache:
         check(_lib.lib().sw_gater_host(self._h, ptr(p), ptr(s), ptr(T), B, int(explore),
                                        ptr(phi), ptr(arm)), "gater")
         return phi, arm
+
+
+class CacheManager:
+    """CacheManager (cache.hpp:45-106): host policy in libsemwarm_b200 (csrc/host), data plane in
+    the WarmStartCache's device arena. Method names follow the reference."""
+
+    def __init__(self, cache: WarmStartCache, capacity: int = 1024, decay_per_hour: float = 0.9,
+                 grace_hours: float = 1.0, quality_floor: float = 0.3, pyramid_delta: float = 0.25,
+                 embedding_seed: int = 0, refine_regenerations: int = 3,
+                 refine_attempt_cap: int = 5, refine_window: int = 10,
+                 refine_skip_threshold: float = 0.10, latent_capacity: int = 0):
+        self.cache = cache
+        cfg = _lib.SwcmConfig(capacity, decay_per_hour, grace_hours, quality_floor,
+                              pyramid_delta, embedding_seed, refine_regenerations,
+                              refine_attempt_cap, refine_window, 0, refine_skip_threshold,
+                              latent_capacity)
+        h = C.c_void_p()
+        check(_lib.lib().swcm_create(cache._h, cache.dim, C.byref(cfg), C.byref(h)),
+              "swcm_create")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib().swcm_destroy(self._h)
+            self._h = None
+
+    def admit(self, clip_embedding, duration_s, prompt_embedding, quality, now_h, latent=None):
+        e = np.ascontiguousarray(clip_embedding, np.float32)
+        pr = None if prompt_embedding is None else np.ascontiguousarray(prompt_embedding, np.float32)
+        lat = None if latent is None else np.ascontiguousarray(latent, np.float32)
+        out = C.c_uint64()
+        rc = check(_lib.lib().swcm_admit(self._h, ptr(e), duration_s, ptr(pr), quality, now_h,
+                                         ptr(lat), 0 if lat is None else lat.shape[1],
+                                         C.byref(out)), "admit")
+        return int(out.value) if rc == 1 else None
+
+    def last_evicted(self):
+        buf = np.zeros(4096, np.uint64)
+        n = check(_lib.lib().swcm_last_evicted(self._h, ptr(buf), 4096), "last_evicted")
+        return buf[:n].tolist()
+
+    def record_reuse(self, entry_id, steps_skipped, duration_s, now_h, skip_fraction):
+        rc = check(_lib.lib().swcm_record_reuse(self._h, entry_id, steps_skipped, duration_s,
+                                                now_h, skip_fraction), "record_reuse")
+        if rc == _lib.SW_WARN_UNKNOWN_ID:
+            warnings.warn(f"record_reuse for unknown entry id {entry_id}")
+
+    def evict_if_full(self, now_h):
+        buf = np.zeros(4096, np.uint64)
+        n = check(_lib.lib().swcm_evict_if_full(self._h, now_h, ptr(buf), 4096), "evict")
+        return buf[:n].tolist()
+
+    def refinement_candidates(self):
+        buf = np.zeros(65536, np.uint64)
+        n = check(_lib.lib().swcm_refinement_candidates(self._h, ptr(buf), 65536), "candidates")
+        return buf[:n].tolist()
+
+    def refine(self, entry_id, rng_seed, regenerate):
+        """regenerate(prompt, duration_s, seed) -> (embedding, quality[, latent])."""
+        dim = self.cache.dim
+
+        def cb(user, prompt, d, duration, seed, emb_out, q_out, lat_out, t_out):
+            pr = None if not prompt else np.ctypeslib.as_array(
+                C.cast(prompt, C.POINTER(C.c_float)), (dim,)).copy()
+            res = regenerate(pr, duration, int(seed))
+            e = np.ascontiguousarray(res[0], np.float32)
+            for i in range(dim):
+                emb_out[i] = float(e[i])
+            q_out[0] = float(res[1])
+            t_out[0] = 0
+            return 0
+
+        fn = _lib.REGEN_FN(cb)
+        replaced = C.c_int32()
+        rc = check(_lib.lib().swcm_refine(self._h, entry_id, rng_seed, fn, None,
+                                          C.byref(replaced)), "refine")
+        if rc == _lib.SW_WARN_UNKNOWN_ID:
+            warnings.warn(f"refine for unknown entry id {entry_id}")
+        return bool(replaced.value)
+
+    def current_importance(self, entry_id, now_h):
+        out = C.c_double()
+        check(_lib.lib().swcm_importance(self._h, entry_id, now_h, C.byref(out)), "importance")
+        return out.value
+
+    def size(self):
+        return _lib.lib().swcm_size(self._h)
+
+    def ids(self):
+        buf = np.zeros(max(1, self.size()), np.uint64)
+        n = _lib.lib().swcm_ids(self._h, ptr(buf), buf.shape[0])
+        return buf[:n].tolist()
+
+    def check_consistent(self):
+        return bool(_lib.lib().swcm_check_consistent(self._h))
