@@ -373,6 +373,27 @@ def main():
                "d2h_bytes_per_step": B * CHOICE_DTYPE.itemsize, "ms_per_step": round(e2e_ms, 4),
                "path": "sw_warmstart_host (pinned host prompts/requests -> choices)"}
 
+    # ---- align + noise timed alone on the same choices, both noise modes (device events)
+    align_alone = {}
+    if world == 1:
+        eps_t = torch.randn((B, C_, T_, F_), dtype=torch.float32, device=dev)
+        for mode, dptr in (("philox", None), ("eps", eps_t.data_ptr())):
+            def al():
+                _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+                                             .data_ptr(), B, dptr, 1234, out.data_ptr(), T_, sp),
+                           "sw_align_noise")
+            for _ in range(3):
+                al()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 50
+            a0.record(stream)
+            for _ in range(reps):
+                al()
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            align_alone[mode] = a0.elapsed_time(a1) / reps
+        del eps_t
+
     # ---- p50 selector latency (search through select, pipeline.cpp:93-143's selector_ms span)
     lat = {}
     if not args.no_latency and world == 1:
@@ -408,6 +429,7 @@ def main():
     t_seg = (fr(ch["start_s"] + ch["length_s"]) - fr(ch["start_s"]))[hits]
     al_bytes = float(np.sum(4 * C_ * F_ * (np.minimum(t_out, T_) + np.minimum(t_seg, t_out))))
     al_gbs = al_bytes / (al_ms / max(1, al_n) / 1000.0) / 1e9 if al_n else None
+    eps_bytes = al_bytes + float(np.sum(4 * C_ * F_ * np.minimum(t_out, T_)))
     total_ms_step = ms / steps
     value = B * steps / (ms / 1000.0)
     stage_ms = {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items() if v[1]}
@@ -454,7 +476,12 @@ def main():
         "align_roofline": {"bound": "hbm", "achieved": round(al_gbs, 1) if al_gbs else None,
                            "peak": hbm, "unit": "GB/s",
                            "frac": round(al_gbs / hbm, 4) if al_gbs else None,
-                           "bytes_per_launch": al_bytes},
+                           "bytes_per_launch": al_bytes,
+                           "alone_ms": {k: round(v, 4) for k, v in align_alone.items()},
+                           "alone_frac": {
+                               "philox": round(al_bytes / (align_alone["philox"] / 1e3) / 1e9 / hbm, 4),
+                               "eps": round(eps_bytes / (align_alone["eps"] / 1e3) / 1e9 / hbm, 4)}
+                           if align_alone else None},
         "stage_ms": stage_ms,
         "selector_p50_ms": lat,
         "hit_rate": round(float(hits.mean()), 4),

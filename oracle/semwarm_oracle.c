@@ -344,16 +344,45 @@ void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* u in (0,1): odd 24-bit numerator, exact in float */
-static float u01(uint32_t x) { return (float)((x >> 8) | 1u) * 0x1.0p-24f; }
+static float as_f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t as_u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
-/* Box-Muller: r = sqrt(-2 ln u1) in fp32; cos/sin(2 pi u2) correctly rounded to fp32 (the
- * device evaluates sincospif(2 u2), exact argument, <= 1 ulp). */
+/* Box-Muller, our definition, every fp32 rounding spelled out
+ * exactly as the device evaluates it (paper_2603_07865_b200/csrc/align.cu box_muller):
+ * v = 2 - asfloat(0x3f800000 | a>>9) in (0,1]; ln v = e ln2 + ln(1+f) with
+ * ln(1+f) = f - f^2/2 + f^3 q(f) (degree-6 minimax q); r = sqrt(-2 ln v);
+ * theta = 2 pi (b>>8) 2^-24 split into the nearest quadrant and phi in [-pi/4, pi/4);
+ * minimax sin (odd, deg 7) / cos (even, deg 8) of phi; (z0, z1) = (r cos, r sin). */
 static void box_muller(uint32_t a, uint32_t b, float* z0, float* z1) {
-    float r = sqrtf(-2.0f * logf(u01(a)));
-    double th = 2.0 * M_PI * (double)u01(b);
-    *z0 = r * (float)cos(th);
-    *z1 = r * (float)sin(th);
+    float v = 2.0f - as_f(0x3f800000u | (a >> 9));
+    uint32_t iv = as_u(v);
+    int e = ((int32_t)(iv - 0x3f3504f3u)) >> 23;
+    float f = as_f(iv - ((uint32_t)e << 23)) - 1.0f;
+    float f2 = f * f, f3 = f2 * f;
+    float q = 0x1.644d8ap-4f;
+    q = fmaf(q, f, -0x1.24291cp-3f);
+    q = fmaf(q, f, 0x1.317306p-3f);
+    q = fmaf(q, f, -0x1.53836p-3f);
+    q = fmaf(q, f, 0x1.98d828p-3f);
+    q = fmaf(q, f, -0x1.00037ep-2f);
+    q = fmaf(q, f, 0x1.5556d8p-2f);
+    float l1p = fmaf(f3, q, fmaf(f2, -0.5f, f));
+    float lnv = fmaf((float)e, 0x1.62e43p-1f, l1p);
+    float r = sqrtf(-2.0f * lnv);
+    uint32_t j = b >> 8;
+    uint32_t n = (j + (1u << 21)) >> 22;
+    float ph = (float)((int32_t)j - (int32_t)(n << 22)) * 0x1.921fb6p-22f;
+    float p2 = ph * ph;
+    float sp = fmaf(ph * p2, fmaf(p2, fmaf(p2, -0x1.994522p-13f, 0x1.11073ep-7f), -0x1.555546p-3f),
+                    ph);
+    float cp = fmaf(p2, fmaf(p2, fmaf(p2, fmaf(p2, 0x1.99177ap-16f, -0x1.6c07f6p-10f),
+                                      0x1.55553cp-5f), -0.5f), 1.0f);
+    /* quadrant n: swap on odd n; sin negative for n mod 4 in {2,3}, cos for {1,2} */
+    float sn = (n & 1u) ? cp : sp, cs = (n & 1u) ? sp : cp;
+    if (n & 2u) sn = -sn;
+    if ((n + 1u) & 2u) cs = -cs;
+    *z0 = r * cs;
+    *z1 = r * sn;
 }
 
 void so_philox_normals(uint64_t seed, uint64_t rid, int64_t n, float* out) {
