@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-latency", action="store_true")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: validation of the N>1 script on ONE GPU (all ranks share cuda:0, "
+                        "records all-gathered through host memory); never a bench number")
     return p.parse_args()
 
 
@@ -224,9 +227,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    staged = args.dist_backend == "gloo"
+    if staged:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if staged:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     B, K = args.batch, args.top_k
     R = rows_per_entry(args.delta)
@@ -263,7 +272,12 @@ def main():
     else:
         qpool = torch.empty((n_pool, B, D), dtype=torch.float32, device=dev)
     if world > 1:
-        dist.broadcast(qpool, 0)
+        if staged:
+            qc = qpool.cpu()
+            dist.broadcast(qc, 0)
+            qpool.copy_(qc)
+        else:
+            dist.broadcast(qpool, 0)
     L = np.random.default_rng(11).uniform(2.5, 10.0, B)
     req_np = [requests(np.arange(s * B + 1, (s + 1) * B + 1, dtype=np.uint64), L,
                        np.full(B, 200, np.int32)) for s in range(n_pool)]
@@ -292,9 +306,17 @@ def main():
         else:
             _lib.check(L_.sw_local_topk(wc._h, q.data_ptr(), B, K, rank, rec_local.data_ptr(),
                                         n_local_t.data_ptr(), sp), "sw_local_topk")
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(rec_all, rec_local)
-                dist.all_gather_into_tensor(n_all, n_local_t)
+            if staged:  # host-staged gather (gloo validation mode only)
+                stream.synchronize()
+                for src, dst in ((rec_local, rec_all), (n_local_t, n_all)):
+                    parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
+                    dist.all_gather(parts, src.cpu())
+                    dst.copy_(torch.cat(parts).to(dev))
+                torch.cuda.synchronize(dev)
+            else:
+                with torch.cuda.stream(stream):
+                    dist.all_gather_into_tensor(rec_all, rec_local)
+                    dist.all_gather_into_tensor(n_all, n_local_t)
             _lib.check(L_.sw_merge_select(wc._h, rec_all.data_ptr(), n_all.data_ptr(), world,
                                           q.data_ptr(), r.data_ptr(), B, K, 1, Cc.byref(csel),
                                           Cc.byref(cpol), choices.data_ptr(), sp),
@@ -326,7 +348,7 @@ def main():
     wc.profile(False)
     ms = ev0.elapsed_time(ev1)
     prof = wc.profile_read()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cpu" if staged else dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -424,9 +446,10 @@ def main():
     achieved = flops / (score_ms / 1000.0) / 1e12 if sc_n else None
     al_ms, al_n = prof["align"]
     hits = ch["hit"].astype(bool)
-    t_out = ch["t_out"][hits].astype(np.int64)
+    owned = hits & ((ch["owner"] == rank) if world > 1 else True)  # owner-computes align
+    t_out = ch["t_out"][owned].astype(np.int64)
     fr = lambda x: np.floor(x * 25.0 + 0.5)
-    t_seg = (fr(ch["start_s"] + ch["length_s"]) - fr(ch["start_s"]))[hits]
+    t_seg = (fr(ch["start_s"] + ch["length_s"]) - fr(ch["start_s"]))[owned]
     al_bytes = float(np.sum(4 * C_ * F_ * (np.minimum(t_out, T_) + np.minimum(t_seg, t_out))))
     al_gbs = al_bytes / (al_ms / max(1, al_n) / 1000.0) / 1e9 if al_n else None
     eps_bytes = al_bytes + float(np.sum(4 * C_ * F_ * np.minimum(t_out, T_)))
@@ -465,6 +488,7 @@ def main():
                    "l2": "inputs larger than L2 (bf16 arena %.0f MB streamed per step)"
                          % (n_rows * D * 2 / 1e6),
                    "latent_slots": min(args.latent_slots, n_local)},
+        **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
         "roofline": {"bound": "tensor", "kernel": "k_score_tc (tcgen05.mma M128 N256 K16, TMA)",
                      "achieved": round(achieved, 1) if achieved else None, "peak": pk_burst,
                      "unit": "TFLOP/s", "frac": round(achieved / pk_burst, 4) if achieved else None,
