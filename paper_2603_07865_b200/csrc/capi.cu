@@ -62,7 +62,7 @@ static void free_ctx(Ctx& c) {
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
                     c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
-                    c.thr, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
+                    c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -117,9 +117,10 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.q_norm, (size_t)c.Bmax);
     dalloc(&c.q_eps, (size_t)c.Bmax);
     dalloc(&c.thr, (size_t)c.Bmax);
+    dalloc(&c.top1, (size_t)c.Bmax * kMaxSlices);
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
-    dalloc(&c.slice_cnt, (size_t)c.Bmax * 148);
-    dalloc(&c.cta_topk, (size_t)c.Bmax * 148 * kMaxTopK);
+    dalloc(&c.slice_cnt, (size_t)c.Bmax * kMaxSlices);
+    dalloc(&c.cta_topk, (size_t)c.Bmax * kMaxSlices * kMaxTopK);
     dalloc(&c.u_draw, (size_t)c.Bmax);
     dalloc(&c.dbg, (size_t)c.Bmax * 8);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);

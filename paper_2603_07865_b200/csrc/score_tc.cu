@@ -6,9 +6,12 @@
 //               one 256x64 bf16 cache chunk per pipeline stage
 //   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=256, K=16 per instruction),
 //               double-buffered fp32 accumulators (2 x 256 TMEM columns)
-//   warps 2-5   epilogue: TMEM lane == query, so each thread walks ITS query's 256 scores with
-//               tcgen05.ld, takes the per-entry max over the entry's Rp pyramid rows, and keeps
-//               a running 32-deep top list in registers.
+//   warps 2-9   epilogue, two groups of 4 warps: group g drains accumulator g, i.e. the tiles
+//               lt = g, g+2, ... (each group gets two MMA tile-times per tile, so the TMEM read
+//               of 128 KB per tile never paces the tensor core). TMEM lane == query, so each
+//               thread walks ITS query's 256 scores with tcgen05.ld, takes the per-entry max
+//               over the entry's Rp pyramid rows, and keeps a running top list in registers.
+//               Each (CTA, group) is one emission slice of the query's candidate buffer.
 //
 // The 1M x 1024 score matrix is never written. Instead the epilogue emits a CERTIFIED candidate
 // set: with eps_q >= |bf16 score - exact score| (bf16 rounding of both operands, 2u + u^2 with
@@ -28,8 +31,11 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int A_CHUNK = BM * 128;  // bytes: 128 rows x 64 bf16
 constexpr int B_STAGE = BN * 128;  // bytes: 256 rows x 64 bf16
-constexpr int THREADS = 192;
+constexpr int B_HALF = B_STAGE / 2;  // CTA-pair mode: each CTA of the pair stages 128 rows
+constexpr int THREADS = 320;
+constexpr int EPI_GROUPS = 2;
 constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
+constexpr uint32_t IDESC_PAIR = ptx::idesc_bf16_f32(2 * BM, BN);
 
 struct TcParams {
     int B;
@@ -42,12 +48,15 @@ struct TcParams {
     const uint32_t* valid_bits;  // one bit per slot
     const float* q_eps;
     uint32_t* thr;
+    uint32_t* top1;  // [B][kMaxSlices] each slice's running best approximate entry score
     int32_t* slice_cnt;  // [B][n_chunks] emissions per (query, CTA)
     float* cta_topk;     // [B][n_chunks][32] final running lists
     int32_t* cand_slot;  // [B][kCandCap], CTA y owns [y * cap_local, (y + 1) * cap_local)
     float* cand_score;
     int n_chunks;
     int cap_local;
+    int experiment;  // 0 normal; profiling only (SW_SCORE_EXPERIMENT): 1 = epilogue skipped,
+                     // 2 = also no cache TMA (pure MMA rate)
 };
 
 // Emission + running top-list update for the entries of one 32-column chunk whose approximate
@@ -55,7 +64,7 @@ struct TcParams {
 // (usually 0 or 1). Emissions go to this (query, CTA)'s private slice with a register counter:
 // no atomics and no loads on the emission path.
 template <int RP, int KL>
-__device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t mask,
+__device__ __forceinline__ void emit_chunk(const uint32_t (&r)[32], uint32_t mask,
                                            int64_t slot_c, float& theta, float (&list)[KL],
                                            float& kth, float eps2, int& cnt, int64_t slice,
                                            const TcParams& p) {
@@ -63,15 +72,20 @@ __device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t 
     while (mask) {
         const int e = __ffs(mask) - 1;
         mask &= mask - 1;
-        // em[e] through a binary mux tree (a dynamic register index would spill to local)
+        // entry e's max over its RP pyramid rows, selected through a binary mux tree (a
+        // dynamic register index would spill to local memory), clamped like core.cpp:35-36
         float t[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) t[j] = em[j];
+        for (int j = 0; j < E; ++j) {
+            t[j] = __uint_as_float(r[j * RP]);
+#pragma unroll
+            for (int i = 1; i < RP; ++i) t[j] = fmaxf(t[j], __uint_as_float(r[j * RP + i]));
+        }
 #pragma unroll
         for (int w = E / 2, b = 1; w >= 1; w >>= 1, b <<= 1)
 #pragma unroll
             for (int j = 0; j < w; ++j) t[j] = (e & b) ? t[2 * j + 1] : t[2 * j];
-        const float m = t[0];
+        const float m = fminf(1.0f, fmaxf(-1.0f, t[0]));
         if (m < theta) continue;  // theta may have risen within this chunk
         if (cnt < p.cap_local) {
             p.cand_slot[slice + cnt] = (int32_t)(slot_c + e);
@@ -90,16 +104,22 @@ __device__ __forceinline__ void emit_chunk(const float (&em)[32 / RP], uint32_t 
     }
 }
 
-template <int RP, int KL>
+// PAIR: a 2-CTA cluster (the two CTAs of one TPC) runs the MMA as cta_group::2 with M = 256:
+// each CTA keeps its own 128 queries resident and stages HALF of every 256-row cache tile
+// (128 rows), so the per-SM L2 -> SM operand feed halves; the leader CTA issues the MMA for
+// both and its commits multicast to both CTAs' barriers. The epilogue is unchanged: TMEM lane
+// == query in each CTA. TEMPTY lives in the leader and counts both CTAs' epilogue warps.
+template <int RP, int KL, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     k_score_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmE,
                const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
+    constexpr int BSTG = PAIR ? B_HALF : B_STAGE;
     uint8_t* sA = smem;
     uint8_t* sB = smem + p.kch * A_CHUNK;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * B_STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * BSTG);
     const int S = p.n_stages;
     // full[S] | empty[S] | a_full | tfull[2] | tempty[2]
     auto bar = [&](int i) { return ptx::smem_u32(&bars[i]); };
@@ -111,8 +131,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int qblock = blockIdx.x;
     const int64_t t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
     const int64_t t1 = min(p.n_tiles, t0 + p.tiles_per_cta);
-    if (t0 >= t1) return;  // uniform for the whole CTA
+    if (t0 >= t1) return;  // uniform for the whole CTA (and for both CTAs of a pair)
     const int ntiles = (int)(t1 - t0);
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -122,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::mbar_init(bar(AFULL), 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar(TFULL + i), 1);
-            ptx::mbar_init(bar(TEMPTY + i), 4);
+            ptx::mbar_init(bar(TEMPTY + i), PAIR ? 8 : 4);  // one group of 4 warps per acc
         }
         ptx::fence_barrier_init();
     }
@@ -131,62 +153,111 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::tma_prefetch_desc(&tmE);
     }
     if (warp == 1) {
-        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
-        ptx::tmem_relinquish();
+        if (PAIR) {
+            ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), 512);
+            ptx::tmem_relinquish_pair();
+        } else {
+            ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+            ptx::tmem_relinquish();
+        }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (PAIR)
+        ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer
-            ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
-            for (int kc = 0; kc < p.kch; ++kc)
-                ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
-                                 qblock * BM);
-            uint32_t it = 0;
+            if (PAIR) {
+                // both CTAs load their own queries / their half of each tile; the bytes
+                // complete on the leader's barriers, whose expectation covers both halves
+                if (leader) ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(2 * p.kch * A_CHUNK));
+                for (int kc = 0; kc < p.kch; ++kc)
+                    ptx::tma_load_2d_pair(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL),
+                                          kc * 64, qblock * BM);
+            } else {
+                ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
+                for (int kc = 0; kc < p.kch; ++kc)
+                    ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
+                                     qblock * BM);
+            }
+            int s = 0;  // ring stage and its phase, advanced incrementally (no division)
+            uint32_t ph = 0;
             for (int lt = 0; lt < ntiles; ++lt) {
                 const int64_t tile = t0 + lt;
-                for (int kc = 0; kc < p.kch; ++kc, ++it) {
-                    const int s = (int)(it % S);
-                    const uint32_t ph = (it / S) & 1u;
+                for (int kc = 0; kc < p.kch; ++kc, s = (s + 1 == S) ? 0 : s + 1,
+                         ph ^= (s == 0) ? 1u : 0u) {
                     ptx::mbar_wait_sleep(bar(EMPTY + s), ph ^ 1u);
-                    ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
-                    ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
-                                     kc * 64, (int32_t)(tile * BN));
+                    if (p.experiment == 2) {
+                        if (leader) ptx::mbar_arrive(bar(FULL + s));
+                        continue;
+                    }
+                    if (PAIR) {
+                        if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
+                        ptx::tma_load_2d_pair(ptx::smem_u32(sB + s * BSTG), &tmE, bar(FULL + s),
+                                              kc * 64, (int32_t)(tile * BN + rank * (BN / 2)));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
+                        ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
+                                         kc * 64, (int32_t)(tile * BN));
+                    }
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (one thread issues for the whole CTA)
+        if (leader) {
+            // ---------------- MMA issuer: the converged warp waits, one elected lane issues
+            // for the whole CTA / pair. Descriptors advance by constants (K16 step = 32 B =
+            // 2 in the >>4 address field), keeping the per-chunk issue path short.
             ptx::mbar_wait(bar(AFULL), 0);
             ptx::tc_fence_after();
-            uint32_t it = 0;
+            const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sA));
+            const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sB));
+            int s = 0;
+            uint32_t ph = 0;
             for (int lt = 0; lt < ntiles; ++lt) {
                 const int acc = lt & 1;
                 const uint32_t aph = (lt >> 1) & 1u;
                 ptx::mbar_wait_sleep(bar(TEMPTY + acc), aph ^ 1u);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kc = 0; kc < p.kch; ++kc, ++it) {
-                    const int s = (int)(it % S);
-                    const uint32_t ph = (it / S) & 1u;
+                for (int kc = 0; kc < p.kch; ++kc, s = (s + 1 == S) ? 0 : s + 1,
+                         ph ^= (s == 0) ? 1u : 0u) {
                     ptx::mbar_wait_sleep(bar(FULL + s), ph);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + kc * A_CHUNK);
-                    const uint32_t b0 = ptx::smem_u32(sB + s * B_STAGE);
+                    const uint64_t ad = adesc0 + (uint64_t)(kc * (A_CHUNK >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(s * (BSTG >> 4));
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(a0 + k * 32),
-                                      ptx::umma_desc_sw128(b0 + k * 32), IDESC,
-                                      (kc | k) != 0 ? 1u : 0u);
-                    ptx::mma_commit(bar(EMPTY + s));  // frees the smem stage when MMAs finish
+                        for (int k = 0; k < 4; ++k) {
+                            if (PAIR)
+                                ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, IDESC_PAIR,
+                                                   (kc | k) != 0 ? 1u : 0u);
+                            else
+                                ptx::mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, IDESC,
+                                              (kc | k) != 0 ? 1u : 0u);
+                        }
+                        // frees the smem stage (both CTAs' halves) when the MMAs finish
+                        if (PAIR)
+                            ptx::mma_commit_pair(bar(EMPTY + s));
+                        else
+                            ptx::mma_commit(bar(EMPTY + s));
+                    }
+                    __syncwarp();
                 }
-                ptx::mma_commit(bar(TFULL + acc));  // accumulator ready for the epilogue
+                // accumulator ready for the epilogue (of both CTAs)
+                if (ptx::elect_one()) {
+                    if (PAIR)
+                        ptx::mma_commit_pair(bar(TFULL + acc));
+                    else
+                        ptx::mma_commit(bar(TFULL + acc));
+                }
+                __syncwarp();
             }
         }
         __syncwarp();
@@ -194,8 +265,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ---------------- epilogue: TMEM lane == query
         constexpr int E = 32 / RP;          // entries per 32-column chunk
         constexpr int SPT = BN / RP;        // slots per tile
-        constexpr int NW = SPT >= 32 ? SPT / 32 : 1;
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
+        const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
+        const int vchunk = blockIdx.y * EPI_GROUPS + grp;
         const int q = qblock * BM + quarter * 32 + lane;
         const bool qvalid = q < p.B;
         float eps2 = 0.0f;
@@ -206,11 +278,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int i = 0; i < KL; ++i) list[i] = (i < KL - p.k) ? INFINITY : -INFINITY;
         const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
-        const int64_t slice = (int64_t)q * kCandCap + (int64_t)blockIdx.y * p.cap_local;
+        const int64_t slice = (int64_t)q * kCandCap + (int64_t)vchunk * p.cap_local;
         int cnt = 0;
         uint32_t g_next = qvalid ? __ldcg(&p.thr[q]) : 0u;  // shared k-th best, one tile ahead
+        float pub_top1 = -INFINITY;
+        int done = 0;  // tiles drained by this group
 
-        for (int lt = 0; lt < ntiles; ++lt) {
+        for (int lt = grp; lt < ntiles; lt += EPI_GROUPS) {
             const int acc = lt & 1;
             const uint32_t aph = (lt >> 1) & 1u;
             const int64_t tile = t0 + lt;
@@ -218,72 +292,132 @@ __global__ void __launch_bounds__(THREADS, 1)
                 theta = fmaxf(theta, ord2f(g_next) - eps2);
                 g_next = __ldcg(&p.thr[q]);
             }
-            // validity bits of this tile's slots, fetched before waiting on the accumulator
             const int64_t slot0 = tile * SPT;
-            const int boff = (int)(slot0 & 31);
-            uint32_t vw[NW];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) vw[w] = __ldg(p.valid_bits + (slot0 >> 5) + w);
-            ptx::mbar_wait(bar(TFULL + acc), aph);
+            ptx::mbar_wait_sleep(bar(TFULL + acc), aph);  // no spinning on the MMA's SMSPs
             ptx::tc_fence_after();
-#pragma unroll
+            if (done == 0 && p.k <= BN / 32 && p.experiment == 0) {
+                // First tile of this slice: the threshold is still -inf, so a one-pass scan
+                // would emit the whole record sequence of the tile (~k + k ln(256/k)). A
+                // pre-pass takes each fully valid chunk's best entry; the k-th largest of
+                // those k+ distinct entries' scores (their minimum over >= k chunks, taken as
+                // the min over all 8) lower-bounds T_a, and the emitting pass starts from it.
+                float lo_best = INFINITY;
+                int n_full = 0;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
+                    const int64_t sc = slot0 + c * E;
+                    uint32_t vb = __ldg(p.valid_bits + (sc >> 5)) >> (int)(sc & 31);
+                    if (E < 32) vb &= (1u << (E & 31)) - 1u;
+                    ptx::tmem_ld_wait();
+                    const float cmax = ptx::max32(r);
+                    if (vb == (E < 32 ? (1u << (E & 31)) - 1u : 0xFFFFFFFFu)) {
+                        lo_best = fminf(lo_best, fminf(1.0f, fmaxf(-1.0f, cmax)));
+                        ++n_full;
+                    }
+                }
+                if (qvalid && n_full == BN / 32) {
+                    theta = fmaxf(theta, lo_best - eps2);
+                    if (lo_best > published) {
+                        atomicMax(&p.thr[q], f2ord(lo_best));
+                        published = lo_best;
+                    }
+                }
+            }
+            // Hot loop kept compact (not unrolled: the rare emission path is instantiated once,
+            // so the epilogue stays resident in the instruction cache). Per 32-column chunk:
+            // one tcgen05.ld, a 16-op FMNMX3 max tree over the raw scores, one compare; max and clamp
+            // commute, so the per-entry clamped maxima are only formed on the rare path.
+#pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
+                if (p.experiment == 1 || p.experiment == 2) break;  // profiling: no epilogue
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                 ptx::tmem_ld_wait();
-                // per-entry max over the entry's RP pyramid rows (adjacent columns), clamped
-                // to [-1, 1] like cosine_similarity (core.cpp:35-36)
-                float em[E];
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    float m = __uint_as_float(r[e * RP]);
-#pragma unroll
-                    for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[e * RP + j]));
-                    em[e] = fminf(1.0f, fmaxf(-1.0f, m));
-                }
-                // tree max (short dependency chain), then a bitmask only when needed
-                float t[E];
-#pragma unroll
-                for (int e = 0; e < E; ++e) t[e] = em[e];
-#pragma unroll
-                for (int w = E / 2; w >= 1; w >>= 1)
-#pragma unroll
-                    for (int e = 0; e < w; ++e) t[e] = fmaxf(t[e], t[e + w]);
-                if (qvalid && t[0] >= theta) {
+                if (qvalid && fminf(1.0f, fmaxf(-1.0f, ptx::max32(r))) >= theta) {
+                    // clamp(x) >= theta  <=>  x >= theta'  (theta' = -inf when theta <= -1;
+                    // theta > 1 cannot reach here), so the mask needs no per-entry clamp
+                    const float th = theta > -1.0f ? theta : -INFINITY;
                     uint32_t mask = 0;
 #pragma unroll
-                    for (int e = 0; e < E; ++e) mask |= (em[e] >= theta ? 1u : 0u) << e;
-                    const int bb = boff + c * E;
-                    uint32_t vbits = (NW > 1 ? vw[(c * E) >> 5] : vw[0]) >> (bb & 31);
-                    if (E < 32) vbits &= (1u << E) - 1u;
+                    for (int e = 0; e < E; ++e) {
+                        float m = __uint_as_float(r[e * RP]);
+#pragma unroll
+                        for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[e * RP + j]));
+                        mask |= (m >= th ? 1u : 0u) << e;
+                    }
+                    const int64_t sc = slot0 + c * E;  // E-slot group never straddles a word
+                    uint32_t vbits = __ldg(p.valid_bits + (sc >> 5)) >> (int)(sc & 31);
+                    if (E < 32) vbits &= (1u << (E & 31)) - 1u;
                     mask &= vbits;
                     if (mask)
-                        emit_chunk<RP, KL>(em, mask, slot0 + c * E, theta, list, kth, eps2, cnt,
-                                           slice, p);
+                        emit_chunk<RP, KL>(r, mask, sc, theta, list, kth, eps2, cnt, slice, p);
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar(TEMPTY + acc));
-            if (qvalid && kth > published) {
-                atomicMax(&p.thr[q], f2ord(kth));
-                published = kth;
+            if (lane == 0) {
+                if (PAIR)
+                    ptx::mbar_arrive_cluster(ptx::mapa(bar(TEMPTY + acc), 0));
+                else
+                    ptx::mbar_arrive(bar(TEMPTY + acc));
+            }
+            if (qvalid) {
+                // Union bound on T_a: the slices partition the entries, so the k-th largest of
+                // their running bests is the k-th best of k distinct entries, <= T_a. It tracks
+                // the whole scanned prefix of the cache (a slice's own k-th best tracks only
+                // its 1/n_chunks share), so the emission threshold converges tiles earlier.
+                const float best = list[KL - p.k];
+                if (best > pub_top1) {
+                    __stcg(&p.top1[(int64_t)q * kMaxSlices + vchunk], f2ord(best));
+                    pub_top1 = best;
+                }
+                ++done;
+                float bound = kth;
+                if ((done & (done - 1)) == 0 && p.n_chunks >= p.k) {  // tiles 1, 2, 4, 8, ...
+                    float sel[KL];
+#pragma unroll
+                    for (int i = 0; i < KL; ++i) sel[i] = (i < KL - p.k) ? INFINITY : -INFINITY;
+                    const uint32_t* t1 = p.top1 + (int64_t)q * kMaxSlices;
+                    for (int j = 0; j < p.n_chunks; ++j) {
+                        float x = ord2f(__ldcg(t1 + j));
+#pragma unroll
+                        for (int i = 0; i < KL; ++i) {
+                            const float hi = fmaxf(sel[i], x);
+                            x = fminf(sel[i], x);
+                            sel[i] = hi;
+                        }
+                    }
+                    bound = fmaxf(bound, sel[KL - 1]);
+                    theta = fmaxf(theta, bound - eps2);
+                }
+                if (bound > published) {
+                    atomicMax(&p.thr[q], f2ord(bound));
+                    published = bound;
+                }
             }
         }
         if (qvalid) {
-            p.slice_cnt[(int64_t)q * p.n_chunks + blockIdx.y] = cnt;
-            // this CTA's exact local top-k (every entry below it was below the running k-th)
-            float* tk = p.cta_topk + ((int64_t)q * p.n_chunks + blockIdx.y) * kMaxTopK;
+            p.slice_cnt[(int64_t)q * p.n_chunks + vchunk] = cnt;
+            // this slice's exact local top-k (every entry below it was below the running k-th)
+            float* tk = p.cta_topk + ((int64_t)q * p.n_chunks + vchunk) * kMaxTopK;
 #pragma unroll
             for (int i = 0; i < KL; ++i)
                 if (i >= KL - p.k) tk[i - (KL - p.k)] = list[i];
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (PAIR)
+        ptx::cluster_sync();  // neither CTA frees TMEM (or exits) while the pair still uses it
+    else
+        __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 512);
+        if (PAIR)
+            ptx::tmem_dealloc_pair(tmem_base, 512);
+        else
+            ptx::tmem_dealloc(tmem_base, 512);
     }
 }
 
@@ -319,23 +453,53 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32
     return r == CUDA_SUCCESS;
 }
 
-template <int RP, int KL>
+template <int RP, int KL, bool PAIR>
 void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     static bool attr_set = false;
+    auto kern = k_score_tc<RP, KL, PAIR>;
     if (!attr_set) {
-        SW_CUDA(cudaFuncSetAttribute(k_score_tc<RP, KL>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem_optin));
+        SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     c.smem_optin));
         attr_set = true;
     }
-    k_score_tc<RP, KL><<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+    if (PAIR) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SW_CUDA(cudaLaunchKernelEx(&cfg, kern, c.tm_q, c.tm_rows_half, p));
+    } else {
+        kern<<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+    }
 }
 
-template <int RP>
+template <int RP, bool PAIR>
 void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     if (p.k <= 8)
-        launch_tc_kl<RP, 8>(c, p, grid, smem, st);
+        launch_tc_kl<RP, 8, PAIR>(c, p, grid, smem, st);
     else
-        launch_tc_kl<RP, 32>(c, p, grid, smem, st);
+        launch_tc_kl<RP, 32, PAIR>(c, p, grid, smem, st);
+}
+
+template <bool PAIR>
+void launch_tc(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+    switch (c.Rp) {
+        case 1: launch_tc_rp<1, PAIR>(c, p, grid, smem, st); break;
+        case 2: launch_tc_rp<2, PAIR>(c, p, grid, smem, st); break;
+        case 4: launch_tc_rp<4, PAIR>(c, p, grid, smem, st); break;
+        case 8: launch_tc_rp<8, PAIR>(c, p, grid, smem, st); break;
+        case 16: launch_tc_rp<16, PAIR>(c, p, grid, smem, st); break;
+        case 32: launch_tc_rp<32, PAIR>(c, p, grid, smem, st); break;
+        default: throw Error(SW_EINVAL, "rows per entry pad must be a power of two <= 32");
+    }
 }
 
 }  // namespace
@@ -343,6 +507,7 @@ void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_
 bool encode_tensor_maps(Ctx& c) {
     if (c.Dp > 512) return false;
     bool ok = encode_2d(&c.tm_rows, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN);
+    ok = ok && encode_2d(&c.tm_rows_half, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN / 2);
     ok = ok && encode_2d(&c.tm_q, c.q_bf, (uint64_t)c.Dp, (uint64_t)c.BmaxPad, BM);
     return ok;
 }
@@ -357,6 +522,14 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_STAGE);
     SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
     p.k = k;
+    const int qb = (B + BM - 1) / BM;
+    // CTA pairs need an even number of 128-query blocks; SW_SCORE_PAIR=0 forces single CTAs
+    static const bool pair_ok = [] {
+        const char* e = getenv("SW_SCORE_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    const bool pair = pair_ok && qb >= 2 && qb % 2 == 0;
+    if (pair) p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_HALF);
     const int64_t rows_hw = c.high_water * c.Rp;
     p.n_tiles = (rows_hw + BN - 1) / BN;
     const int qblocks = (B + BM - 1) / BM;
@@ -368,24 +541,27 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.valid_bits = c.valid_bits;
     p.q_eps = c.q_eps;
     p.thr = c.thr;
+    p.top1 = c.top1;
     p.slice_cnt = c.slice_cnt;
     p.cta_topk = c.cta_topk;
     p.cand_slot = c.cand_slot;
     p.cand_score = c.cand_score;
-    p.n_chunks = (int)chunks;
-    p.cap_local = (kCandCap / (int)chunks) & ~3;  // multiple of 4: 16-byte aligned slices
-    c.last_chunks = (int)chunks;
-    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 256;
+    p.n_chunks = (int)chunks * EPI_GROUPS;  // emission slices: (CTA, epilogue group)
+    p.cap_local = (kCandCap / p.n_chunks) & ~3;  // multiple of 4: 16-byte aligned slices
+    c.last_chunks = p.n_chunks;
+    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK +
+                        (size_t)p.n_stages * (pair ? B_HALF : B_STAGE) + 256;
+    c.last_score_pair = pair;
+    static const int experiment = [] {
+        const char* e = getenv("SW_SCORE_EXPERIMENT");
+        return e ? atoi(e) : 0;
+    }();
+    p.experiment = experiment;
     dim3 grid((unsigned)qblocks, (unsigned)chunks);
-    switch (c.Rp) {
-        case 1: launch_tc_rp<1>(c, p, grid, smem, st); break;
-        case 2: launch_tc_rp<2>(c, p, grid, smem, st); break;
-        case 4: launch_tc_rp<4>(c, p, grid, smem, st); break;
-        case 8: launch_tc_rp<8>(c, p, grid, smem, st); break;
-        case 16: launch_tc_rp<16>(c, p, grid, smem, st); break;
-        case 32: launch_tc_rp<32>(c, p, grid, smem, st); break;
-        default: throw Error(SW_EINVAL, "rows per entry pad must be a power of two <= 32");
-    }
+    if (pair)
+        launch_tc<true>(c, p, grid, smem, st);
+    else
+        launch_tc<false>(c, p, grid, smem, st);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

@@ -46,6 +46,7 @@ constexpr int kNumArms = 14;          // gater.hpp:13
 constexpr int kFeatureDim = 11;       // gater.hpp:28
 constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep running list
 constexpr int kCandCap = 16384;       // emitted candidates per query (split over the CTAs)
+constexpr int kMaxSlices = 2 * 148;   // (scoring CTA, epilogue group) emission slices per query
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
 // Certified error of a tcgen05 score: |q.e - q~.e~| <= |q| |e - e~| + |q - q~| |e~|
 // (Cauchy-Schwarz on q.e - q~.e~ = q.(e - e~) + (q - q~).e~, ~ = bf16) plus the fp32 tensor-core
@@ -124,12 +125,14 @@ struct Ctx {
     float* q_norm = nullptr;        // [Bmax]
     float* q_eps = nullptr;         // [Bmax] certified |bf16 score - fp64 score| bound per query
     uint32_t* thr = nullptr;        // [Bmax] shared running k-th best (ordered)
+    uint32_t* top1 = nullptr;       // [Bmax][kMaxSlices] each slice's running best (ordered)
     int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
-    int32_t* slice_cnt = nullptr;   // [Bmax][148] emissions per (query, scoring CTA)
-    float* cta_topk = nullptr;      // [Bmax][148][32] each scoring CTA's final top-k (approx)
+    int32_t* slice_cnt = nullptr;   // [Bmax][kMaxSlices] emissions per (query, CTA, group)
+    float* cta_topk = nullptr;      // [Bmax][kMaxSlices][32] each slice's final top-k (approx)
     double* u_draw = nullptr;       // [Bmax] per-request selector draw
     int32_t* dbg = nullptr;         // [Bmax][8] per-query finish stats (sw_debug_query_stats)
     int last_chunks = 1;
+    bool last_score_pair = false;  // last scoring launch ran as tcgen05 CTA pairs
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
     double* cand_exact = nullptr;   // [Bmax][kCandCap]
@@ -145,6 +148,7 @@ struct Ctx {
 
     // TMA descriptors (encoded once at creation; cover the full capacity)
     CUtensorMap tm_rows{};
+    CUtensorMap tm_rows_half{};  // 128-row boxes for the CTA-pair scoring kernel
     CUtensorMap tm_q{};
     bool tc_ok = false;
     int smem_optin = 0;

@@ -75,7 +75,8 @@ def test_search_tc_default_large(orc):
     wc = _cache(c, max_batch=1024)
     q = perturbed_queries(c, 1024, frac_random=0.1)
     hits, cnt = wc.search(q, 8)
-    assert wc.launch_info()["tensor_cores"]
+    info = wc.launch_info()
+    assert info["tensor_cores"] and info["cta_pair"]  # 8 query blocks -> cta_group::2 pairs
     sel = np.arange(0, 1024, 16)
     _check_hits(hits[sel], cnt[sel], _arena(c), orc, q[sel], 8)
 
