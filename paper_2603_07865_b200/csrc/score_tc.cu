@@ -6,12 +6,11 @@
 //               one 256x64 bf16 cache chunk per pipeline stage
 //   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=256, K=16 per instruction),
 //               double-buffered fp32 accumulators (2 x 256 TMEM columns)
-//   warps 2-9   epilogue, two groups of 4 warps: group g drains accumulator g, i.e. the tiles
-//               lt = g, g+2, ... (each group gets two MMA tile-times per tile, so the TMEM read
-//               of 128 KB per tile never paces the tensor core). TMEM lane == query, so each
-//               thread walks ITS query's 256 scores with tcgen05.ld, takes the per-entry max
-//               over the entry's Rp pyramid rows, and keeps a running top list in registers.
-//               Each (CTA, group) is one emission slice of the query's candidate buffer.
+//   warps 2-5   epilogue (EPI_GROUPS groups of 4 warps; group g drains the tiles lt = g mod
+//               EPI_GROUPS). TMEM lane == query, so each thread walks ITS query's 256 scores
+//               with tcgen05.ld, takes the per-entry max over the entry's Rp pyramid rows, and
+//               keeps a running top list in registers. Each (CTA, group) is one emission slice
+//               of the query's candidate buffer.
 //
 // The 1M x 1024 score matrix is never written. Instead the epilogue emits a CERTIFIED candidate
 // set: with eps_q >= |bf16 score - exact score| (bf16 rounding of both operands, 2u + u^2 with
@@ -23,6 +22,13 @@
 #include "ptx.cuh"
 #include "sw_internal.cuh"
 
+#ifndef SW_EPI_GROUPS_
+// Epilogue warp groups draining the two accumulators. 2 (group g drains accumulator g) was
+// measured SLOWER once the epilogue hot loop became compact: the extra warps compete for the
+// issue slots of the SMSPs that host the TMA producer and the MMA issuer (0.765 vs 0.724 ms).
+#define SW_EPI_GROUPS_ 1
+#endif
+
 namespace sw {
 
 namespace {
@@ -32,8 +38,9 @@ constexpr int BN = 256;
 constexpr int A_CHUNK = BM * 128;  // bytes: 128 rows x 64 bf16
 constexpr int B_STAGE = BN * 128;  // bytes: 256 rows x 64 bf16
 constexpr int B_HALF = B_STAGE / 2;  // CTA-pair mode: each CTA of the pair stages 128 rows
-constexpr int THREADS = 320;
-constexpr int EPI_GROUPS = 2;
+constexpr int EPI_GROUPS = SW_EPI_GROUPS_;
+constexpr int THREADS = 64 + 128 * EPI_GROUPS;
+
 constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
 constexpr uint32_t IDESC_PAIR = ptx::idesc_bf16_f32(2 * BM, BN);
 
