@@ -156,6 +156,19 @@ def reference_sample(n_entries, n_queries, nthreads, seed=1, cache=None):
     return run, idx
 
 
+def ncu_traffic(prefix):
+    """DRAM bytes per launch of a kernel from the committed ncu summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+            t = json.load(f)["traffic_bytes"]
+        for k, v in t.items():
+            if k.startswith(prefix):
+                return v, k
+    except Exception:
+        pass
+    return None, None
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -489,11 +502,16 @@ def main():
                          % (n_rows * D * 2 / 1e6),
                    "latent_slots": min(args.latent_slots, n_local)},
         **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
-        "roofline": {"bound": "tensor", "kernel": "k_score_tc (tcgen05.mma M128 N256 K16, TMA)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "k_score_tc (tcgen05.mma %s, TMA)" % (
+                         "cta_group::2 M256 N256 K16" if wc.launch_info()["cta_pair"]
+                         else "M128 N256 K16"),
                      "achieved": round(achieved, 1) if achieved else None, "peak": pk_burst,
                      "unit": "TFLOP/s", "frac": round(achieved / pk_burst, 4) if achieved else None,
                      "frac_of_sustained": round(achieved / pk_sust, 4) if achieved and pk_sust else None,
-                     "peak_source": pk_src, "traffic": None,
+                     "peak_source": pk_src,
+                     "traffic": ncu_traffic("k_score_tc")[0],
+                     "traffic_source": "profiles/ncu_latest.json (ncu --set full, one launch)",
                      "algorithmic": f"2*B*N*D = {flops:.4g} flop per launch",
                      "kernel_ms": round(score_ms, 4),
                      "share_of_step": round(score_ms / total_ms_step, 3)},

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
+                    __syncwarp();
                     ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                     const int64_t sc = slot0 + c * E;
                     uint32_t vb = __ldg(p.valid_bits + (sc >> 5)) >> (int)(sc & 31);
@@ -340,6 +341,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < BN / 32; ++c) {
                 if (p.experiment == 1 || p.experiment == 2) break;  // profiling: no epilogue
                 uint32_t r[32];
+                // tcgen05.ld is .sync.aligned: reconverge lanes that diverged on the previous
+                // chunk's emission path before it (a partially valid warp, B % 32 != 0, hangs
+                // otherwise)
+                __syncwarp();
                 ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                 ptx::tmem_ld_wait();
                 if (qvalid && fminf(1.0f, fmaxf(-1.0f, ptx::max32(r))) >= theta) {
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 else
                     ptx::mbar_arrive(bar(TEMPTY + acc));
             }
+            ++done;  // warp-uniform (all lanes): it gates the .sync.aligned pre-pass
             if (qvalid) {
                 // Union bound on T_a: the slices partition the entries, so the k-th largest of
                 // their running bests is the k-th best of k distinct entries, <= T_a. It tracks
@@ -380,7 +386,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                     __stcg(&p.top1[(int64_t)q * kMaxSlices + vchunk], f2ord(best));
                     pub_top1 = best;
                 }
-                ++done;
                 float bound = kth;
                 if ((done & (done - 1)) == 0 && p.n_chunks >= p.k) {  // tiles 1, 2, 4, 8, ...
                     float sel[KL];

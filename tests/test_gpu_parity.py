@@ -81,6 +81,20 @@ def test_search_tc_default_large(orc):
     _check_hits(hits[sel], cnt[sel], _arena(c), orc, q[sel], 8)
 
 
+@pytest.mark.parametrize("B", [1, 33, 130])
+def test_search_tc_partial_warps(orc, B):
+    """Batches that leave a warp partially valid (B % 32 != 0) with several tiles per scoring
+    CTA: every warp-collective tcgen05.ld must stay converged (regression: a per-lane gate on
+    the first-tile pre-pass hung the epilogue)."""
+    c = SynthCache(120000, 512, 1.0, seed=21, clustered=False)
+    wc = _cache(c, max_batch=256)
+    q = perturbed_queries(c, B, frac_random=0.1)
+    hits, cnt = wc.search(q, 8)
+    assert wc.launch_info()["tensor_cores"]
+    sel = np.arange(0, B, max(1, B // 8))
+    _check_hits(hits[sel], cnt[sel], _arena(c), orc, q[sel], 8)
+
+
 def test_search_host_entry_point(orc):
     c = SynthCache(200, 64, 0.25, seed=1)
     wc = _cache(c)
