@@ -168,6 +168,31 @@ int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t 
 /* Copy stored fp32 rows of an entry back to host (n_rows_cap x D); returns rows copied. */
 int sw_arena_read_rows(sw_ctx* ctx, uint64_t entry_id, float* rows, int32_t n_rows_cap);
 
+/* ---------------------------------------------------------------- IVF coarse quantiser
+ * IvfIndex (index.hpp:47-101) in its reference-default mode (pipeline.cpp:28-31: 64 centroids,
+ * nprobe 8, rebuild every 1024 mutations). Without sw_ivf_configure a context is in exhaustive
+ * parity mode (one list). */
+/* IvfIndex::build({}, centroids, seed, nprobe) + set_rebuild_interval (index.cpp:186-208).
+ * Empty arena only. centroids < 1 -> SW_EINVAL (index.cpp:191); at most 256 lists. */
+int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t rebuild_interval,
+                     uint64_t seed);
+/* IvfIndex::set_nprobe (index.hpp:74). */
+int sw_ivf_set_nprobe(sw_ctx* ctx, int32_t nprobe);
+/* IvfIndex::rebuild (index.cpp:257-283): k-means++ and Lloyd over every stored row in
+ * (id, level, start) order with seed derive_seed(seed, ++rebuild_count), bit-identical to the
+ * reference; dot products, member sums and reseeding searches run on the GPU. Also the bulk
+ * path after sw_arena_fill_synthetic. */
+int sw_ivf_rebuild(sw_ctx* ctx);
+/* centroid_count() (index.hpp:69), mutations since the last rebuild, rebuild count. */
+int sw_ivf_info(sw_ctx* ctx, int32_t* n_centroids, uint64_t* mutations, uint64_t* rebuilds);
+/* Host copy of the centroids (C x D fp32); returns C. */
+int sw_ivf_centroids(sw_ctx* ctx, float* centroids_out, int32_t cap);
+/* Installs centroids (e.g. from a SWIX snapshot, index.cpp:345-408) and reassigns every stored
+ * row to its nearest one. */
+int sw_ivf_set_centroids(sw_ctx* ctx, const float* centroids, int32_t n_centroids);
+/* The list of each of an entry's rows (test / debug); returns the row count. */
+int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t entry_id, int16_t* lists, int32_t cap);
+
 /* ---------------------------------------------------------------- batched hot path
  * IvfIndex::search (index.cpp:289-326) in exhaustive mode for B queries: exact fp64 cosine,
  * best segment per entry, (sim desc, id asc), truncated to k. d_out: B x k, d_n: B. */

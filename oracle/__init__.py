@@ -216,6 +216,12 @@ class Ref:
         L.ref_index_new.restype = C.c_void_p
         L.ref_index_new.argtypes = [C.c_int]
         L.ref_index_free.argtypes = [C.c_void_p]
+        L.ref_ivf_new.restype = C.c_void_p
+        L.ref_ivf_new.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64]
+        L.ref_index_save.restype = C.c_int
+        L.ref_index_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_index_check_consistent.restype = C.c_int
+        L.ref_index_check_consistent.argtypes = [C.c_void_p]
         L.ref_index_insert_many.restype = C.c_int
         L.ref_index_insert_many.argtypes = [C.c_void_p, C.c_int, u64p, i64p, f32p, i32p, f64p, f64p]
         L.ref_index_remove.argtypes = [C.c_void_p, C.c_uint64]
@@ -300,8 +306,8 @@ class Ref:
         return rows[:n].copy(), lv[:n].copy(), st[:n].copy(), ln[:n].copy()
 
     # -- index
-    def index(self, ar: Arena):
-        return RefIndex(self, ar)
+    def index(self, ar: Arena, ivf=None):
+        return RefIndex(self, ar, ivf)
 
     def context_features(self, p, c, T):
         phi = np.zeros(11, np.float64)
@@ -316,16 +322,66 @@ class Ref:
                                        np.ascontiguousarray(phi, np.float64), int(explore))
 
 
-class RefIndex:
-    """Reference IvfIndex in exhaustive parity mode over an Arena (kept alive here)."""
+def parse_swix(path: str):
+    """SWIX snapshot (index.cpp:347-369) -> (centroids [C][D] f32, nprobe, lists) where lists[j]
+    is the list's records in order: (entry_id, level, start_s f32, length_s f32)."""
+    import struct
+    b = open(path, "rb").read()
+    assert b[:4] == b"SWIX", "bad magic"
+    C_, nprobe, D = struct.unpack_from("<III", b, 4)
+    o = 16
+    cent = np.frombuffer(b, np.float32, C_ * D, o).reshape(C_, D).copy()
+    o += 4 * C_ * D
+    lists = []
+    for _ in range(C_):
+        (cnt,) = struct.unpack_from("<Q", b, o)
+        o += 8
+        recs = []
+        for _ in range(cnt):
+            eid, lvl = struct.unpack_from("<QB", b, o)
+            st, ln = struct.unpack_from("<ff", b, o + 9)
+            recs.append((eid, lvl, st, ln))
+            o += 17 + 4 * D
+        lists.append(recs)
+    assert o == len(b)
+    return cent, nprobe, lists
 
-    def __init__(self, ref: Ref, ar: Arena):
+
+class RefIndex:
+    """Reference IvfIndex over an Arena (kept alive here): exhaustive parity mode by default,
+    or IVF mode (ivf = (centroids, seed, nprobe, rebuild_interval)) as CacheManager builds it."""
+
+    def __init__(self, ref: Ref, ar: Arena, ivf=None):
         self.ref, self.ar = ref, ar
-        self.h = ref.lib.ref_index_new(ar.dim)
-        rc = ref.lib.ref_index_insert_many(self.h, ar.n_entries, ar.ids, ar.off, ar.rows,
-                                           ar.levels, ar.starts, ar.lengths)
+        if ivf is None:
+            self.h = ref.lib.ref_index_new(ar.dim)
+        else:
+            c, seed, nprobe, interval = ivf
+            self.h = ref.lib.ref_ivf_new(ar.dim, c, seed, nprobe, interval)
+        if ar.n_entries:
+            rc = ref.lib.ref_index_insert_many(self.h, ar.n_entries, ar.ids, ar.off, ar.rows,
+                                               ar.levels, ar.starts, ar.lengths)
+            if rc != 0:
+                raise RuntimeError("reference insert failed")
+
+    def insert(self, ar: Arena):
+        """Inserts more entries (the arena must stay alive: candidate assembly reads it)."""
+        self._keep = getattr(self, "_keep", []) + [ar]
+        rc = self.ref.lib.ref_index_insert_many(self.h, ar.n_entries, ar.ids, ar.off, ar.rows,
+                                                ar.levels, ar.starts, ar.lengths)
         if rc != 0:
             raise RuntimeError("reference insert failed")
+
+    def snapshot(self):
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".swix") as f:
+            n = self.ref.lib.ref_index_save(self.h, f.name.encode())
+            if n < 0:
+                raise RuntimeError("save failed")
+            return parse_swix(f.name)
+
+    def consistent(self) -> bool:
+        return bool(self.ref.lib.ref_index_check_consistent(self.h))
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -127,6 +127,27 @@ void* ref_index_new(int dim) {
     return h;
 }
 void ref_index_free(void* p) { delete static_cast<RefIndex*>(p); }
+// IVF mode exactly as CacheManager creates it (cache.cpp:17, pipeline.cpp:79-81):
+// IvfIndex::build({}, C, seed, nprobe) + set_rebuild_interval.
+void* ref_ivf_new(int dim, int centroids, uint64_t seed, int nprobe, uint64_t interval) {
+    auto* h = new RefIndex;
+    h->dim = (size_t)dim;
+    h->idx = IvfIndex::build({}, (uint32_t)centroids, seed, (uint32_t)nprobe);
+    h->idx.set_rebuild_interval(interval);
+    return h;
+}
+// SWIX snapshot of the index (index.cpp:347-369): the only view of its centroids and lists.
+int ref_index_save(void* p, const char* path) {
+    try {
+        static_cast<RefIndex*>(p)->idx.save(path);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return (int)static_cast<RefIndex*>(p)->idx.centroid_count();
+}
+int ref_index_check_consistent(void* p) {
+    return static_cast<RefIndex*>(p)->idx.check_consistent() ? 1 : 0;
+}
 
 // Inserts n_entries entries; entry e owns rows [off[e], off[e+1]) of `rows` (caller keeps the
 // buffer alive for the index lifetime: candidate assembly reads segment rows from it).

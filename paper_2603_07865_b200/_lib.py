@@ -145,6 +145,13 @@ def lib() -> C.CDLL:
         "swcm_ids": ([vp, vp, i32], C.c_int),
         "swcm_check_consistent": ([vp], C.c_int),
         "sw_profile_reset": ([vp], C.c_int),
+        "sw_ivf_configure": ([vp, i32, i32, u64, u64], C.c_int),
+        "sw_ivf_set_nprobe": ([vp, i32], C.c_int),
+        "sw_ivf_rebuild": ([vp], C.c_int),
+        "sw_ivf_info": ([vp, C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)], C.c_int),
+        "sw_ivf_centroids": ([vp, vp, i32], C.c_int),
+        "sw_ivf_set_centroids": ([vp, vp, i32], C.c_int),
+        "sw_ivf_entry_lists": ([vp, u64, vp, i32], C.c_int),
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -165,7 +172,9 @@ EXPORTED = [
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
     "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",
     "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
-    "swcm_size", "swcm_ids", "swcm_check_consistent",
+    "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",
+    "sw_ivf_rebuild", "sw_ivf_info", "sw_ivf_centroids", "sw_ivf_set_centroids",
+    "sw_ivf_entry_lists",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

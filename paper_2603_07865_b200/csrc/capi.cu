@@ -63,7 +63,8 @@ static void free_ctx(Ctx& c) {
                     c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
-                    c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage};
+                    c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
+                    c.cent, c.row_list, c.prank, c.pmask};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
@@ -133,6 +134,11 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.d_q_stage, (size_t)c.Bmax * c.D);
     dalloc(&c.d_req_stage, (size_t)c.Bmax);
     dalloc(&c.d_choice_stage, (size_t)c.Bmax);
+    dalloc(&c.cent, (size_t)kMaxCentroids * c.Df);
+    dalloc(&c.row_list, (size_t)nrow);
+    dalloc(&c.prank, (size_t)c.Bmax * kMaxCentroids);
+    dalloc(&c.pmask, (size_t)c.Bmax * 4);
+    c.ivf_rows.assign((size_t)c.S, 0);
     SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
     SW_CUDA(cudaMemsetAsync(c.valid, 0, (size_t)c.S, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.valid_bits, 0, sizeof(uint32_t) * (size_t)(c.S / 32 + 16), c.mstream));
@@ -270,6 +276,11 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
         launch_copy_latents(c, n, d_slot, d_lat, d_latoff, d_tsrc, st);
     }
     SW_CUDA(cudaStreamSynchronize(st));
+    if (c.ivf) {  // IvfIndex::insert per entry, in order (index.cpp:224-234)
+        std::vector<int32_t> nr((size_t)n);
+        for (int64_t e = 0; e < n; ++e) nr[(size_t)e] = (int32_t)(h_off[e + 1] - h_off[e]);
+        ivf_on_insert(c, pl.slot, pl.base, nr);
+    }
     cudaFree(d_slot);
     cudaFree(d_base);
     if (!on_device) {
@@ -297,6 +308,7 @@ static void do_remove(Ctx& c, uint64_t id, bool* found) {
     c.h_nrows[(size_t)s] = 0;
     launch_clear_slot(c, s, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
+    if (c.ivf) ivf_on_remove(c, s);  // IvfIndex::remove (index.cpp:236-255)
     if (s == c.high_water - 1) {
         --c.high_water;
         // trim trailing free slots so the scan range stays tight
@@ -455,6 +467,9 @@ int sw_arena_replace(sw_ctx* ctx, uint64_t id, int32_t n_rows, const float* rows
         }
         SW_REQUIRE(n_rows <= c.Rp, "entry has more rows than the arena's rows_per_entry");
         // in place: same slot, rows rewritten from row 0 (CacheManager::refine, cache.cpp:129-139)
+        // The reference re-indexes with remove + insert; in IVF mode both count as mutations
+        // and either may trigger a rebuild (the remove's without this entry).
+        if (c.ivf) ivf_on_remove(c, it->second);
         c.h_nrows[(size_t)it->second] = 0;
         int64_t off[2] = {0, n_rows};
         int64_t loff = 0;
@@ -491,9 +506,108 @@ int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t 
         for (int64_t i = 0; i < n; ++i) {
             c.slot_of[first_id + (uint64_t)i] = slot0 + i;
             c.h_nrows[(size_t)(slot0 + i)] = c.R;
+            c.ivf_rows[(size_t)(slot0 + i)] = c.R;
         }
         c.high_water += n;
+        // IVF mode: a bulk load like IvfIndex::build(vecs) — no mutation counting; rows join the
+        // current centroids' lists (sw_ivf_rebuild re-clusters)
+        if (c.ivf && c.ivf_C > 0) ivf_set_centroids(c, c.h_cent.data(), c.ivf_C);
         return SW_OK;
+    });
+}
+
+// ---------------------------------------------------------------- IVF coarse quantiser
+int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t rebuild_interval,
+                     uint64_t seed) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        SW_REQUIRE(centroids >= 1, "centroid count must be >= 1");  // index.cpp:191
+        SW_REQUIRE(centroids <= kMaxCentroids, "at most 256 centroids are supported");
+        SW_REQUIRE(nprobe >= 1, "nprobe must be >= 1");
+        SW_REQUIRE(rebuild_interval >= 1, "rebuild interval must be >= 1");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_REQUIRE(c.slot_of.empty(), "configure the IVF index on an empty arena");
+        c.ivf = true;
+        c.ivf_target = centroids;
+        c.ivf_nprobe = nprobe;
+        c.ivf_interval = rebuild_interval;
+        c.ivf_seed = seed;
+        c.ivf_C = 0;
+        c.ivf_mutations = 0;
+        c.ivf_rebuilds = 0;
+        c.h_cent.clear();
+        return SW_OK;
+    });
+}
+
+int sw_ivf_set_nprobe(sw_ctx* ctx, int32_t nprobe) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && nprobe >= 1, "bad argument");
+        std::unique_lock lk(ctx->c.mu);
+        ctx->c.ivf_nprobe = nprobe;
+        return SW_OK;
+    });
+}
+
+int sw_ivf_rebuild(sw_ctx* ctx) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_REQUIRE(c.ivf, "the context is not in IVF mode (sw_ivf_configure)");
+        SW_CUDA(cudaSetDevice(c.device));
+        ivf_rebuild(c);
+        return SW_OK;
+    });
+}
+
+int sw_ivf_info(sw_ctx* ctx, int32_t* n_centroids, uint64_t* mutations, uint64_t* rebuilds) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        std::shared_lock lk(ctx->c.mu);
+        if (n_centroids) *n_centroids = ctx->c.ivf ? ctx->c.ivf_C : 1;
+        if (mutations) *mutations = ctx->c.ivf_mutations;
+        if (rebuilds) *rebuilds = ctx->c.ivf_rebuilds;
+        return SW_OK;
+    });
+}
+
+int sw_ivf_centroids(sw_ctx* ctx, float* out, int32_t cap) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (out || cap == 0), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        const int n = std::min(cap, c.ivf_C);
+        std::memcpy(out, c.h_cent.data(), sizeof(float) * (size_t)n * c.D);
+        return c.ivf_C;
+    });
+}
+
+int sw_ivf_set_centroids(sw_ctx* ctx, const float* centroids, int32_t n) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (centroids || n == 0), "null argument");
+        SW_REQUIRE(n >= 0 && n <= kMaxCentroids, "at most 256 centroids are supported");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_REQUIRE(c.ivf, "the context is not in IVF mode (sw_ivf_configure)");
+        SW_CUDA(cudaSetDevice(c.device));
+        ivf_set_centroids(c, centroids, n);
+        return SW_OK;
+    });
+}
+
+int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t id, int16_t* lists, int32_t cap) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && lists, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        auto it = c.slot_of.find(id);
+        if (it == c.slot_of.end()) return 0;
+        const int nr = std::min(cap, c.ivf_rows[(size_t)it->second]);
+        SW_CUDA(cudaMemcpy(lists, c.row_list + it->second * c.Rp, sizeof(int16_t) * nr,
+                           cudaMemcpyDeviceToHost));
+        return nr;
     });
 }
 

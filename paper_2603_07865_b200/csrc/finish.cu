@@ -67,6 +67,9 @@ struct FinishParams {
     dev::SelParams sp;
     const sw_request* reqs;
     sw_choice* out;
+    int ivf;                  // IVF mode: rows outside the query's probed lists do not count
+    const int16_t* row_list;  // [rows] list of each stored row
+    const uint8_t* prank;     // [B][kMaxCentroids] probe rank of each list (255: not probed)
 };
 
 struct FinSmem {
@@ -298,9 +301,21 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
         const int64_t i = w >> p.logRp;
         const int r = (int)(w & (p.Rp - 1));
         int64_t row = -1, slot = -1;
+        int key = r;  // tie order among an entry's rows (index.cpp:306-311)
         if (w < items) {
             slot = p.implicit_all ? i : (i < SMAXC ? (int64_t)S.slot[i] : (int64_t)p.list[base + i]);
             if (p.valid[slot] && r < p.nrows[slot]) row = slot * p.Rp + r;
+            if (row >= 0 && p.ivf) {
+                // only rows of probed lists are scanned; lists are visited in probe order and
+                // an entry's rows sit in pyramid order inside a list, so the first maximum in
+                // scan order is the lowest (probe rank, row)
+                const int l = p.row_list[row];
+                const int pr = l >= 0 ? p.prank[(int64_t)b * kMaxCentroids + l] : kNotProbed;
+                if (pr == kNotProbed)
+                    row = -1;
+                else
+                    key = (pr << 6) | r;
+            }
         }
         // lane l stages float4 (l & 7) of rows (l >> 3) + 4u, u = 0..7
         const float* src[8];
@@ -347,8 +362,8 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
             __syncwarp();  // this ring slot is refilled NST - 1 chunks later
         }
         double sim = row >= 0 ? fmin(1.0, fmax(-1.0, s)) : -DBL_MAX;  // core.cpp:35-36
-        int rw = row >= 0 ? r : 0x7fffffff;
-        for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest row (index.cpp:311)
+        int rw = row >= 0 ? key : 0x7fffffff;
+        for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest key (index.cpp:311)
             const double os = __shfl_xor_sync(full, sim, o);
             const int orow = __shfl_xor_sync(full, rw, o);
             if (os > sim || (os == sim && orow < rw)) {
@@ -356,6 +371,7 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                 rw = orow;
             }
         }
+        if (rw != 0x7fffffff) rw &= 63;  // key -> row index
         if (w < items && r == 0) {
             if (i < SMAXC) {
                 S.ex[i] = sim;
@@ -489,7 +505,8 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
 
 }  // namespace
 
-int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st);
+int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st);
+bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
 
 // Search (+ optionally select) for B queries. Results land in c.hits / c.nhits (and d_out).
 int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
@@ -507,9 +524,11 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
         SW_REQUIRE(c.high_water <= kCandCap,
                    "exact-only search is limited to 16384 slots; enable the tcgen05 path");
     kernels += launch_prep(c, d_q, B, d_req, sp ? sp->seed : 0, st);
+    const bool ivf = launch_probe_rank(c, d_q, B, st);  // IvfIndex probe lists (nprobe < C)
+    kernels += ivf ? 1 : 0;
     if (tc) {
         StageScope sc(c, SW_STAGE_SCORE_TC, st);
-        kernels += launch_score_tc(c, B, k, st);
+        kernels += launch_score_tc(c, B, k, ivf, st);
     }
     FinishParams p{};
     p.B = B;
@@ -546,6 +565,10 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     if (sp) p.sp = *sp;
     p.reqs = d_req;
     p.out = d_out;
+    p.ivf = ivf ? 1 : 0;
+    p.row_list = c.row_list;
+    p.prank = c.prank;
+    c.last_ivf = ivf;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
         const size_t smem = sizeof(double) * c.Df + sizeof(float) * NWARP * NST * 32 * SP;

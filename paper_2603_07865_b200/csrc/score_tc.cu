@@ -62,6 +62,9 @@ struct TcParams {
     float* cand_score;
     int n_chunks;
     int cap_local;
+    int ivf;                      // IVF mode: only rows of the query's probed lists count
+    const int16_t* row_list;      // [rows] list of every stored row
+    const uint64_t* pmask;        // [B][4] probed-list bitmask per query
     int experiment;  // 0 normal; profiling only (SW_SCORE_EXPERIMENT): 1 = epilogue skipped,
                      // 2 = also no cache TMA (pure MMA rate)
 };
@@ -279,6 +282,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool qvalid = q < p.B;
         float eps2 = 0.0f;
         if (qvalid) eps2 = 2.0f * p.q_eps[q];
+        uint64_t pm0 = 0, pm1 = 0, pm2 = 0, pm3 = 0;  // probed lists (IVF mode)
+        if (p.ivf && qvalid) {
+            pm0 = p.pmask[(int64_t)q * 4 + 0];
+            pm1 = p.pmask[(int64_t)q * 4 + 1];
+            pm2 = p.pmask[(int64_t)q * 4 + 2];
+            pm3 = p.pmask[(int64_t)q * 4 + 3];
+        }
         float theta = -INFINITY, kth = -INFINITY, published = -INFINITY;
         // descending list; the top KL - k slots are +inf so list[KL-1] is always the k-th best
         float list[KL];
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t slot0 = tile * SPT;
             ptx::mbar_wait_sleep(bar(TFULL + acc), aph);  // no spinning on the MMA's SMSPs
             ptx::tc_fence_after();
-            if (done == 0 && p.k <= BN / 32 && p.experiment == 0) {
+            if (done == 0 && p.k <= BN / 32 && p.experiment == 0 && !p.ivf) {
                 // First tile of this slice: the threshold is still -inf, so a one-pass scan
                 // would emit the whole record sequence of the tile (~k + k ln(256/k)). A
                 // pre-pass takes each fully valid chunk's best entry; the k-th largest of
@@ -348,6 +358,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
                 ptx::tmem_ld_wait();
                 if (qvalid && fminf(1.0f, fmaxf(-1.0f, ptx::max32(r))) >= theta) {
+                    if (p.ivf) {
+                        // IVF: a row counts only if its list is among the query's probed lists
+                        // (index.cpp:306-307); the hot max above may include other rows, which
+                        // only makes this rare path run more often, never changes a result
+                        const uint4* rl4 = reinterpret_cast<const uint4*>(
+                            p.row_list + tile * BN + c * 32);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const uint4 w = __ldg(rl4 + v);
+                            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                            for (int h = 0; h < 8; ++h) {
+                                const int l = (int)(int16_t)(ww[h >> 1] >> (16 * (h & 1)));
+                                const uint64_t pm = (l >> 6) == 0 ? pm0 : (l >> 6) == 1 ? pm1
+                                                  : (l >> 6) == 2 ? pm2 : pm3;
+                                if (l < 0 || !((pm >> (l & 63)) & 1ull))
+                                    r[8 * v + h] = __float_as_uint(-INFINITY);
+                            }
+                        }
+                    }
                     // clamp(x) >= theta  <=>  x >= theta'  (theta' = -inf when theta <= -1;
                     // theta > 1 cannot reach here), so the mask needs no per-entry clamp
                     const float th = theta > -1.0f ? theta : -INFINITY;
@@ -357,7 +387,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         float m = __uint_as_float(r[e * RP]);
 #pragma unroll
                         for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[e * RP + j]));
-                        mask |= (m >= th ? 1u : 0u) << e;
+                        mask |= (m >= th && m != -INFINITY ? 1u : 0u) << e;
                     }
                     const int64_t sc = slot0 + c * E;  // E-slot group never straddles a word
                     uint32_t vbits = __ldg(p.valid_bits + (sc >> 5)) >> (int)(sc & 31);
@@ -525,7 +555,7 @@ bool encode_tensor_maps(Ctx& c) {
 }
 
 // Returns the number of kernels launched (1).
-int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
+int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     // grid: x = 128-query block, y = contiguous range of 256-row tiles (<= 148 CTAs per block row)
     TcParams p{};
     p.B = B;
@@ -554,6 +584,9 @@ int launch_score_tc(Ctx& c, int B, int k, cudaStream_t st) {
     p.q_eps = c.q_eps;
     p.thr = c.thr;
     p.top1 = c.top1;
+    p.ivf = ivf ? 1 : 0;
+    p.row_list = c.row_list;
+    p.pmask = c.pmask;
     p.slice_cnt = c.slice_cnt;
     p.cta_topk = c.cta_topk;
     p.cand_slot = c.cand_slot;

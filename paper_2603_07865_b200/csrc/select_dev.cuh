@@ -7,14 +7,14 @@
 namespace sw {
 namespace dev {
 
-__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // core.cpp:58-63
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // core.cpp:58-63
     x += 0x9e3779b97f4a7c15ULL;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
     return x ^ (x >> 31);
 }
-__device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b,
-                                                uint64_t c) {  // core.cpp:65-71
+__host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b,
+                                                         uint64_t c) {  // core.cpp:65-71
     uint64_t s = splitmix64(base ^ 0x53454d5741524dULL);
     s = splitmix64(s ^ a);
     s = splitmix64(s ^ b);

@@ -48,6 +48,8 @@ constexpr int kMaxTopK = 32;          // tcgen05 epilogue keeps a 32-deep runnin
 constexpr int kCandCap = 16384;       // emitted candidates per query (split over the CTAs)
 constexpr int kMaxSlices = 2 * 148;   // (scoring CTA, epilogue group) emission slices per query
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
+constexpr int kMaxCentroids = 256;    // IVF lists (index.centroids; reference default 64)
+constexpr uint8_t kNotProbed = 255;   // probe-rank sentinel
 // Certified error of a tcgen05 score: |q.e - q~.e~| <= |q| |e - e~| + |q - q~| |e~|
 // (Cauchy-Schwarz on q.e - q~.e~ = q.(e - e~) + (q - q~).e~, ~ = bf16) plus the fp32 tensor-core
 // accumulation slack kAccSlack * |q~| |e~| (K <= 512 additions at <= 2^-23 relative each, x2).
@@ -132,6 +134,7 @@ struct Ctx {
     double* u_draw = nullptr;       // [Bmax] per-request selector draw
     int32_t* dbg = nullptr;         // [Bmax][8] per-query finish stats (sw_debug_query_stats)
     int last_chunks = 1;
+    bool last_ivf = false;         // last search probed IVF lists (nprobe < C)
     bool last_score_pair = false;  // last scoring launch ran as tcgen05 CTA pairs
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
@@ -152,6 +155,22 @@ struct Ctx {
     CUtensorMap tm_q{};
     bool tc_ok = false;
     int smem_optin = 0;
+
+    // IVF coarse quantiser (IvfIndex, index.hpp:47-101). ivf == false: exhaustive (one list).
+    bool ivf = false;
+    int ivf_target = 1;               // target_centroids_
+    int ivf_nprobe = 8;               // nprobe_
+    int ivf_C = 0;                    // centroids_.size()
+    uint64_t ivf_seed = 0;            // seed_
+    uint64_t ivf_interval = 1024;     // rebuild_interval_
+    uint64_t ivf_mutations = 0;       // mutations_since_rebuild_
+    uint64_t ivf_rebuilds = 0;        // rebuild_count_
+    float* cent = nullptr;            // [kMaxCentroids][Df] centroids (device)
+    std::vector<float> h_cent;        // [ivf_C][D] host mirror
+    int16_t* row_list = nullptr;      // [S*Rp] list (nearest centroid) of every stored row
+    uint8_t* prank = nullptr;         // [Bmax][kMaxCentroids] probe rank per list, 255 = not probed
+    uint64_t* pmask = nullptr;        // [Bmax][4] probed-list bitmask (read by the tcgen05 epilogue)
+    std::vector<int32_t> ivf_rows;    // [S] rows of each slot the index has seen (insert order)
 
     // host bookkeeping (mirrors the reference's entry_vector_counts_, index.hpp:92)
     std::unordered_map<uint64_t, int64_t> slot_of;
@@ -230,5 +249,12 @@ void launch_gater(Ctx& c, const float* d_p, const float* d_s, const int32_t* d_T
                   int explore, double* d_phi, int32_t* d_arm, cudaStream_t st);
 
 bool encode_tensor_maps(Ctx& c);
+// IVF coarse quantiser (ivf.cu)
+void ivf_rebuild(Ctx& c);
+void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<int32_t>& base,
+                   const std::vector<int32_t>& nr);
+void ivf_on_remove(Ctx& c, int64_t slot);
+void ivf_set_centroids(Ctx& c, const float* h, int C);
+bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
 
 }  // namespace sw

@@ -172,6 +172,40 @@ class WarmStartCache:
         n = check(_lib.lib().sw_arena_read_rows(self._h, entry_id, ptr(out), cap), "read_rows")
         return out[:n]
 
+    # ------------------------------------------------------------------ IVF coarse quantiser
+    def ivf_configure(self, centroids: int = 64, nprobe: int = 8, rebuild_interval: int = 1024,
+                      seed: int = 0):
+        """IvfIndex::build({}, centroids, seed, nprobe) + set_rebuild_interval (index.cpp:186,
+        pipeline.cpp:28-31 defaults). Empty arena only."""
+        check(_lib.lib().sw_ivf_configure(self._h, centroids, nprobe, rebuild_interval, seed),
+              "sw_ivf_configure")
+
+    def ivf_set_nprobe(self, nprobe: int):
+        check(_lib.lib().sw_ivf_set_nprobe(self._h, nprobe), "sw_ivf_set_nprobe")
+
+    def ivf_rebuild(self):
+        check(_lib.lib().sw_ivf_rebuild(self._h), "sw_ivf_rebuild")
+
+    def ivf_info(self) -> dict:
+        n, m, r = C.c_int32(), C.c_uint64(), C.c_uint64()
+        check(_lib.lib().sw_ivf_info(self._h, C.byref(n), C.byref(m), C.byref(r)), "sw_ivf_info")
+        return {"centroids": n.value, "mutations": m.value, "rebuilds": r.value}
+
+    def ivf_centroids(self) -> np.ndarray:
+        out = np.zeros((256, self.dim), np.float32)
+        n = check(_lib.lib().sw_ivf_centroids(self._h, ptr(out), 256), "sw_ivf_centroids")
+        return out[:n]
+
+    def ivf_set_centroids(self, cent: np.ndarray):
+        cent = np.ascontiguousarray(cent, np.float32)
+        check(_lib.lib().sw_ivf_set_centroids(self._h, ptr(cent), cent.shape[0]),
+              "sw_ivf_set_centroids")
+
+    def ivf_entry_lists(self, entry_id: int) -> np.ndarray:
+        out = np.zeros(32, np.int16)
+        n = check(_lib.lib().sw_ivf_entry_lists(self._h, entry_id, ptr(out), 32), "entry_lists")
+        return out[:n]
+
     def profile(self, on: bool = True):
         check(_lib.lib().sw_profile_enable(self._h, int(on)), "profile")
 

@@ -211,3 +211,24 @@ def test_box_muller_definition_tracks_libm(orc):
     # the tail: v = 2^-23 gives r = sqrt(46 ln 2) = 5.647
     assert abs(z).max() <= 5.65
     assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
+
+
+def test_reference_ivf_harness(ref):
+    """The IVF reference shims (ref_ivf_new + SWIX snapshot) used by the GPU IVF parity tests:
+    a 300-entry index with 16 lists rebuilt during the inserts is self-consistent, its snapshot
+    holds every row exactly once, and probing every list gives the exhaustive similarities."""
+    import oracle
+    from paper_2603_07865_b200.synth import SynthCache, perturbed_queries
+    c = SynthCache(300, 32, 0.25, seed=41, clustered=True)
+    ar = oracle.Arena(c.ids, c.off, c.rows, c.levels, c.starts, c.lengths)
+    ri = ref.index(ar, ivf=(16, 3, 16, 256))
+    assert ri.consistent()
+    cent, nprobe, lists = ri.snapshot()
+    assert cent.shape == (16, 32) and nprobe == 16
+    assert sum(len(x) for x in lists) == len(c.rows)
+    assert np.allclose(np.linalg.norm(cent, axis=1), 1.0, atol=1e-5)  # spherical k-means
+    ex = ref.index(ar)
+    for q in perturbed_queries(c, 16, frac_random=0.2):
+        a, b = ri.search(q, 8), ex.search(q, 8)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[4], b[4])
