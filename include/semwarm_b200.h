@@ -193,6 +193,19 @@ int sw_ivf_set_centroids(sw_ctx* ctx, const float* centroids, int32_t n_centroid
 /* The list of each of an entry's rows (test / debug); returns the row count. */
 int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t entry_id, int16_t* lists, int32_t cap);
 
+/* ---------------------------------------------------------------- snapshots
+ * IvfIndex::load (index.cpp:371-406) straight into an EMPTY context's device arena: entries,
+ * centroids, nprobe and every row's stored list; the context switches to IVF mode. Malformed
+ * files -> SW_ERUNTIME (the reference throws std::runtime_error). */
+int sw_swix_load(sw_ctx* ctx, const char* path);
+/* IvfIndex::save (index.cpp:347-369) of the context's index; rows inside a list in rebuild
+ * order (id, level, start). */
+int sw_swix_save(sw_ctx* ctx, const char* path);
+/* load_embeddings (core.cpp:201-220): reads a SWEM file into `out` (up to cap floats); returns
+ * count * dim and the shape, or a negative status. */
+int64_t sw_swem_read(const char* path, float* out, int64_t cap_floats, int32_t* count,
+                     int32_t* dim);
+
 /* ---------------------------------------------------------------- batched hot path
  * IvfIndex::search (index.cpp:289-326) in exhaustive mode for B queries: exact fp64 cosine,
  * best segment per entry, (sim desc, id asc), truncated to k. d_out: B x k, d_n: B. */

@@ -220,6 +220,10 @@ class Ref:
         L.ref_ivf_new.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64]
         L.ref_index_save.restype = C.c_int
         L.ref_index_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_index_load.restype = C.c_void_p
+        L.ref_index_load.argtypes = [C.c_char_p, C.c_int]
+        L.ref_save_embeddings.restype = C.c_int
+        L.ref_save_embeddings.argtypes = [C.c_char_p, f32p, C.c_int, C.c_int]
         L.ref_index_check_consistent.restype = C.c_int
         L.ref_index_check_consistent.argtypes = [C.c_void_p]
         L.ref_index_insert_many.restype = C.c_int
@@ -308,6 +312,20 @@ class Ref:
     # -- index
     def index(self, ar: Arena, ivf=None):
         return RefIndex(self, ar, ivf)
+
+    def load_index(self, path: str, dim: int):
+        """IvfIndex::load of a SWIX snapshot (search / save / consistency only)."""
+        ri = RefIndex.__new__(RefIndex)
+        ri.ref, ri.ar = self, None
+        ri.h = self.lib.ref_index_load(path.encode(), dim)
+        if not ri.h:
+            raise RuntimeError("reference failed to load " + path)
+        return ri
+
+    def save_embeddings(self, path: str, v: np.ndarray):
+        v = np.ascontiguousarray(v, np.float32)
+        if self.lib.ref_save_embeddings(path.encode(), v, v.shape[0], v.shape[1]) != 0:
+            raise RuntimeError("save_embeddings failed")
 
     def context_features(self, p, c, T):
         phi = np.zeros(11, np.float64)

@@ -145,6 +145,27 @@ int ref_index_save(void* p, const char* path) {
     }
     return (int)static_cast<RefIndex*>(p)->idx.centroid_count();
 }
+void* ref_index_load(const char* path, int dim) {
+    auto* h = new RefIndex;
+    h->dim = (size_t)dim;
+    try {
+        h->idx = IvfIndex::load(path);
+    } catch (const std::exception&) {
+        delete h;
+        return nullptr;
+    }
+    return h;
+}
+int ref_save_embeddings(const char* path, const float* v, int n, int dim) {
+    std::vector<EmbeddingVector> vs;
+    for (int i = 0; i < n; ++i) vs.push_back(vec(v + (size_t)i * dim, dim));
+    try {
+        save_embeddings(path, vs);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return 0;
+}
 int ref_index_check_consistent(void* p) {
     return static_cast<RefIndex*>(p)->idx.check_consistent() ? 1 : 0;
 }

@@ -323,6 +323,11 @@ static void do_remove(Ctx& c, uint64_t id, bool* found) {
 
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static void bulk_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* off,
+                        const float* rows, const sw_segment* segs) {
+    do_insert(c, n, ids, off, rows, segs, nullptr, nullptr, nullptr, false);
+}
+
 }  // namespace sw
 
 using namespace sw;
@@ -609,6 +614,43 @@ int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t id, int16_t* lists, int32_t cap) {
                            cudaMemcpyDeviceToHost));
         return nr;
     });
+}
+
+// ---------------------------------------------------------------- snapshots
+int sw_swix_load(sw_ctx* ctx, const char* path) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && path, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        swix_load(c, path, &bulk_insert);
+        return SW_OK;
+    });
+}
+
+int sw_swix_save(sw_ctx* ctx, const char* path) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && path, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        swix_save(c, path);
+        return SW_OK;
+    });
+}
+
+int64_t sw_swem_read(const char* path, float* out, int64_t cap_floats, int32_t* count,
+                     int32_t* dim) {
+    try {
+        SW_REQUIRE(path, "null argument");
+        return swem_read(path, out, cap_floats, count, dim);
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SW_ERUNTIME;
+    }
 }
 
 int sw_arena_read_rows(sw_ctx* ctx, uint64_t id, float* rows, int32_t cap) {

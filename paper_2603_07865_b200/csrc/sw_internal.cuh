@@ -256,5 +256,11 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
 void ivf_on_remove(Ctx& c, int64_t slot);
 void ivf_set_centroids(Ctx& c, const float* h, int C);
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
+// snapshots (host/snapshot.cpp)
+void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uint64_t*,
+                                                        const int64_t*, const float*,
+                                                        const sw_segment*));
+void swix_save(Ctx& c, const char* path);
+int64_t swem_read(const char* path, float* out, int64_t cap_floats, int32_t* count, int32_t* dim);
 
 }  // namespace sw

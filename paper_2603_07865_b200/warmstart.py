@@ -206,6 +206,15 @@ class WarmStartCache:
         n = check(_lib.lib().sw_ivf_entry_lists(self._h, entry_id, ptr(out), 32), "entry_lists")
         return out[:n]
 
+    # ------------------------------------------------------------------ snapshots
+    def load_swix(self, path: str):
+        """IvfIndex::load (index.cpp:371-406) into this (empty) cache's device arena."""
+        check(_lib.lib().sw_swix_load(self._h, path.encode()), "sw_swix_load")
+
+    def save_swix(self, path: str):
+        """IvfIndex::save (index.cpp:347-369) of this cache's index."""
+        check(_lib.lib().sw_swix_save(self._h, path.encode()), "sw_swix_save")
+
     def profile(self, on: bool = True):
         check(_lib.lib().sw_profile_enable(self._h, int(on)), "profile")
 
@@ -423,3 +432,13 @@ class CacheManager:
 
     def check_consistent(self):
         return bool(_lib.lib().swcm_check_consistent(self._h))
+
+
+def read_swem(path: str) -> np.ndarray:
+    """load_embeddings (core.cpp:201-220): a SWEM file as a [count, dim] float32 array."""
+    n, d = C.c_int32(), C.c_int32()
+    nf = check(_lib.lib().sw_swem_read(path.encode(), None, 0, C.byref(n), C.byref(d)),
+               "sw_swem_read")
+    out = np.zeros(max(nf, 0), np.float32)
+    check(_lib.lib().sw_swem_read(path.encode(), ptr(out), nf, None, None), "sw_swem_read")
+    return out.reshape(n.value, d.value)

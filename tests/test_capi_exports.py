@@ -4,6 +4,7 @@ import ctypes as C
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_2603_07865_b200 as pkg
@@ -53,3 +54,12 @@ def test_sass_contains_tcgen05_and_tma():
     sass = subprocess.run(["cuobjdump", "-sass", pkg.LIB_PATH], capture_output=True,
                           text=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_swem_reader_matches_reference_writer(ref, tmp_path):
+    """SWEM (core.cpp:183-220) written by the reference, read by the C-ABI (host-only call)."""
+    from paper_2603_07865_b200.warmstart import read_swem
+    v = np.random.default_rng(0).standard_normal((37, 24)).astype(np.float32)
+    p = str(tmp_path / "e.swem")
+    ref.save_embeddings(p, v)
+    np.testing.assert_array_equal(read_swem(p), v)
