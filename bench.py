@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-latency", action="store_true")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
+    p.add_argument("--ivf", default=None, metavar="C,NPROBE",
+                   help="IVF mode (the reference's default index: 64,8): GPU k-means rebuild of "
+                        "the synthetic cache, then probe-restricted warm starts")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 script on ONE GPU (all ranks share cuda:0, "
                         "records all-gathered through host memory); never a bench number")
@@ -123,13 +126,16 @@ def make_host_cache(n, seed=1):
     for i in range(0, n, 65536):
         m = min(65536, n - i)
         rows[i:i + m] = normalize_rows(rng.standard_normal((m, D), dtype=np.float32))
-    dur = rng.uniform(4.0, 12.0, n)
+    dur = rng.uniform(4.0, 12.0, n).astype(np.float32).astype(np.float64)  # SWIX-exact (f32)
     return rows, dur
 
 
-def reference_sample(n_entries, n_queries, nthreads, seed=1, cache=None):
-    """Builds the reference IvfIndex (exhaustive) over n_entries and returns a callable that
-    runs n_queries requests through the reference plan flow with nthreads host threads."""
+def reference_sample(n_entries, n_queries, nthreads, seed=1, cache=None, ivf=None, device=0):
+    """Builds the reference IvfIndex over n_entries (exhaustive, or IVF: ivf = (C, nprobe)) and
+    returns a callable that runs n_queries requests through the reference plan flow with
+    nthreads host threads. IVF: the lists come from our GPU k-means of the same rows, written as
+    a SWIX snapshot and loaded by the reference's own IvfIndex::load (a 1M-row host k-means
+    would not finish in a bench run)."""
     import oracle
     from paper_2603_07865_b200.synth import normalize_rows, trained_like_gater
     rows, dur = cache if cache is not None else make_host_cache(n_entries, seed)
@@ -137,7 +143,21 @@ def reference_sample(n_entries, n_queries, nthreads, seed=1, cache=None):
                       np.arange(n_entries + 1, dtype=np.int64), rows,
                       np.zeros(n_entries, np.int32), np.zeros(n_entries), dur)
     ref = oracle.Ref()
-    idx = ref.index(ar)
+    if ivf is None:
+        idx = ref.index(ar)
+    else:
+        import tempfile
+        from paper_2603_07865_b200.warmstart import WarmStartCache
+        tmp = WarmStartCache(D, rows_per_entry=1, max_entries=n_entries, max_batch=8,
+                             latent_shape=None, device=device)
+        tmp.ivf_configure(ivf[0], ivf[1], 1 << 62, 0)
+        tmp.insert_batch(ar.ids, ar.off, ar.rows, ar.levels, ar.starts, ar.lengths)
+        tmp.ivf_rebuild()
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "cache.swix")
+            tmp.save_swix(path)
+            tmp.close()
+            idx = ref.load_index_with_arena(path, ar)
     rng = np.random.default_rng(seed + 1)
     src = rows[rng.integers(0, n_entries, n_queries)].astype(np.float64)
     g = rng.standard_normal((n_queries, D))
@@ -264,8 +284,17 @@ def main():
     th, ps = trained_like_gater()
     wc.set_negative(neg)
     wc.set_gater(th, ps, 1.0)
+    ivf = tuple(int(x) for x in args.ivf.split(",")) if args.ivf else None
+    if ivf:
+        wc.ivf_configure(ivf[0], ivf[1], 1 << 62, 0)
     wc.fill_synthetic(n_local, first_id=first + 1, seed=1, delta=args.delta)
+    torch.cuda.synchronize(dev)
     setup_s = time.time() - t_setup
+    rebuild_s = None
+    if ivf:
+        t = time.perf_counter()
+        wc.ivf_rebuild()  # GPU k-means++ + Lloyd, bit-identical to the reference's kmeans
+        rebuild_s = time.perf_counter() - t
 
     # ---- prompts: perturbed copies of cached rows (hits) + 10% unrelated prompts
     n_pool = 4
@@ -474,14 +503,15 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         try:
             nt = cpu_threads()
-            run, _idx = reference_sample(args.entries, 2 * nt, nt)
+            run, _idx = reference_sample(args.entries, 2 * nt, nt, ivf=ivf, device=local)
             t = time.perf_counter()
             run()
             el = time.perf_counter() - t
             cpu = {"value": round(2 * nt / el, 3), "unit": "requests/s", "cores": nt,
                    "kind": "reference",
                    "sample": f"{2 * nt} requests ({nt} host threads, {cpu_model()}) through the "
-                             f"unmodified reference (oracle/_ref: IvfIndex::search exhaustive + "
+                             f"unmodified reference (oracle/_ref: IvfIndex::search "
+                             f"{'IVF C=%d nprobe=%d (SWIX-loaded lists)' % ivf if ivf else 'exhaustive'} + "
                              f"score_candidates + select + context_features + choose_arm + t*) "
                              f"over a host copy of a {args.entries}-entry x {D}-d cache"}
         except Exception as e:
@@ -495,7 +525,8 @@ def main():
         "data": "synthetic (device Philox iid unit embeddings; N(0,1) latents)",
         "config": {"workload": f"config3: {args.entries}-entry cache x {D}-d (delta={args.delta},"
                                f" {R} row/entry), batch {B}, top-{K} exact, exploit gater, "
-                               f"align+noise {C_}x{T_}x{F_} Philox",
+                               f"align+noise {C_}x{T_}x{F_} Philox"
+                               + (f", IVF C={ivf[0]} nprobe={ivf[1]}" if ivf else ""),
                    "entries": args.entries, "rows_per_gpu": n_rows, "global_batch": B,
                    "parallelism": f"entry-sharded x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (bf16 arena %.0f MB streamed per step)"
@@ -524,6 +555,9 @@ def main():
                                "philox": round(al_bytes / (align_alone["philox"] / 1e3) / 1e9 / hbm, 4),
                                "eps": round(eps_bytes / (align_alone["eps"] / 1e3) / 1e9 / hbm, 4)}
                            if align_alone else None},
+        **({"ivf": {"centroids": ivf[0], "nprobe": ivf[1], "rebuild_s": round(rebuild_s, 3),
+                    "rebuild": "GPU k-means++ + Lloyd over %d rows (fp64, bit-identical to "
+                               "index.cpp:59-184)" % n_rows}} if ivf else {}),
         "stage_ms": stage_ms,
         "selector_p50_ms": lat,
         "hit_rate": round(float(hits.mean()), 4),

@@ -222,6 +222,9 @@ class Ref:
         L.ref_index_save.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_index_load.restype = C.c_void_p
         L.ref_index_load.argtypes = [C.c_char_p, C.c_int]
+        L.ref_index_new_loaded.restype = C.c_void_p
+        L.ref_index_new_loaded.argtypes = [C.c_char_p, C.c_int, C.c_int, u64p, i64p, f32p, i32p,
+                                           f64p, f64p]
         L.ref_save_embeddings.restype = C.c_int
         L.ref_save_embeddings.argtypes = [C.c_char_p, f32p, C.c_int, C.c_int]
         L.ref_index_check_consistent.restype = C.c_int
@@ -318,6 +321,16 @@ class Ref:
         ri = RefIndex.__new__(RefIndex)
         ri.ref, ri.ar = self, None
         ri.h = self.lib.ref_index_load(path.encode(), dim)
+        if not ri.h:
+            raise RuntimeError("reference failed to load " + path)
+        return ri
+
+    def load_index_with_arena(self, path: str, ar: Arena):
+        """SWIX index + arena rows for candidate assembly (plan_batch works on it)."""
+        ri = RefIndex.__new__(RefIndex)
+        ri.ref, ri.ar = self, ar
+        ri.h = self.lib.ref_index_new_loaded(path.encode(), ar.dim, ar.n_entries, ar.ids, ar.off,
+                                             ar.rows, ar.levels, ar.starts, ar.lengths)
         if not ri.h:
             raise RuntimeError("reference failed to load " + path)
         return ri

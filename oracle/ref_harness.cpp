@@ -156,6 +156,23 @@ void* ref_index_load(const char* path, int dim) {
     }
     return h;
 }
+// IvfIndex::load(path) for the index, the caller's arena (kept alive) for candidate assembly:
+// the CPU baseline of an IVF-mode cache whose lists were built elsewhere (a 1M-row k-means
+// does not finish on the host in a bench run).
+void* ref_index_new_loaded(const char* path, int dim, int n_entries, const uint64_t* ids,
+                           const int64_t* off, const float* rows, const int* levels,
+                           const double* starts, const double* lengths) {
+    auto* h = static_cast<RefIndex*>(ref_index_load(path, dim));
+    if (!h) return nullptr;
+    for (int e = 0; e < n_entries; ++e) {
+        EntryRows er;
+        er.rows = rows + (size_t)off[e] * h->dim;
+        for (int64_t r = off[e]; r < off[e + 1]; ++r)
+            er.segs.push_back(PyramidDescriptor{levels[r], starts[r], lengths[r]});
+        h->entries[ids[e]] = std::move(er);
+    }
+    return h;
+}
 int ref_save_embeddings(const char* path, const float* v, int n, int dim) {
     std::vector<EmbeddingVector> vs;
     for (int i = 0; i < n; ++i) vs.push_back(vec(v + (size_t)i * dim, dim));

@@ -524,7 +524,11 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
         SW_REQUIRE(c.high_water <= kCandCap,
                    "exact-only search is limited to 16384 slots; enable the tcgen05 path");
     kernels += launch_prep(c, d_q, B, d_req, sp ? sp->seed : 0, st);
-    const bool ivf = launch_probe_rank(c, d_q, B, st);  // IvfIndex probe lists (nprobe < C)
+    bool ivf;
+    {
+        StageScope sc(c, SW_STAGE_PREP, st);
+        ivf = launch_probe_rank(c, d_q, B, st);  // IvfIndex probe lists (nprobe < C)
+    }
     kernels += ivf ? 1 : 0;
     if (tc) {
         StageScope sc(c, SW_STAGE_SCORE_TC, st);
