@@ -193,6 +193,19 @@ int sw_ivf_set_centroids(sw_ctx* ctx, const float* centroids, int32_t n_centroid
 /* The list of each of an entry's rows (test / debug); returns the row count. */
 int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t entry_id, int16_t* lists, int32_t cap);
 
+/* ---------------------------------------------------------------- phase vocoder
+ * time_stretch (vocoder.cpp:128-207; StftConfig{window, hop}, pipeline.hpp:36 uses {128, 32})
+ * of B 1-D clips on the GPU, one CTA per clip. d_in: device, clip b = d_in[in_off[b] ..
+ * + in_len[b]) at sample_rate; target_s[b] host. Outputs are packed into d_out (out_cap floats)
+ * at out_off[b] (host, written), out_len[b] = llround(target_s * rate) samples. status[b]
+ * (host): 0, or SW_EINVAL where the reference throws (empty clip, target <= 0, stretch ratio
+ * outside [0.4, 2.5]). A bad window / hop fails the call with SW_EINVAL (StftConfig::validate).
+ * Stream-ordered; host arrays may be reused once the call returns. */
+int sw_time_stretch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int32_t B,
+                    int32_t sample_rate, const double* target_s, int32_t window, int32_t hop,
+                    float* d_out, int64_t out_cap, int64_t* out_off, int32_t* out_len,
+                    int32_t* status, void* stream);
+
 /* ---------------------------------------------------------------- snapshots
  * IvfIndex::load (index.cpp:371-406) straight into an EMPTY context's device arena: entries,
  * centroids, nprobe and every row's stored list; the context switches to IVF mode. Malformed

@@ -225,6 +225,11 @@ class Ref:
         L.ref_index_new_loaded.restype = C.c_void_p
         L.ref_index_new_loaded.argtypes = [C.c_char_p, C.c_int, C.c_int, u64p, i64p, f32p, i32p,
                                            f64p, f64p]
+        L.ref_time_stretch.restype = C.c_int
+        L.ref_time_stretch.argtypes = [f32p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                       f32p, C.c_int]
+        L.ref_synth_latent.restype = C.c_int
+        L.ref_synth_latent.argtypes = [f32p, C.c_int, C.c_double, C.c_int, f32p, C.c_int]
         L.ref_save_embeddings.restype = C.c_int
         L.ref_save_embeddings.argtypes = [C.c_char_p, f32p, C.c_int, C.c_int]
         L.ref_index_check_consistent.restype = C.c_int
@@ -334,6 +339,21 @@ class Ref:
         if not ri.h:
             raise RuntimeError("reference failed to load " + path)
         return ri
+
+    def time_stretch(self, x, rate, target_s, window=128, hop=32):
+        """vocoder.cpp:128-207; None when the reference throws."""
+        x = np.ascontiguousarray(x, np.float32)
+        cap = max(0, int(round(target_s * rate))) + 8
+        out = np.zeros(cap, np.float32)
+        n = self.lib.ref_time_stretch(x, x.shape[0], rate, target_s, window, hop, out, cap)
+        return None if n < 0 else out[:n].copy()
+
+    def synth_latent(self, emb, duration_s, rate=200):
+        emb = np.ascontiguousarray(emb, np.float32)
+        cap = int(round(duration_s * rate)) + 8
+        out = np.zeros(cap, np.float32)
+        n = self.lib.ref_synth_latent(emb, emb.shape[0], duration_s, rate, out, cap)
+        return out[:n].copy()
 
     def save_embeddings(self, path: str, v: np.ndarray):
         v = np.ascontiguousarray(v, np.float32)

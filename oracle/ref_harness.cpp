@@ -21,6 +21,7 @@
 #include "semwarm/core.hpp"
 #include "semwarm/gater.hpp"
 #include "semwarm/index.hpp"
+#include "semwarm/vocoder.hpp"
 #include "semwarm/selector.hpp"
 #include "semwarm/simgen.hpp"
 
@@ -172,6 +173,31 @@ void* ref_index_new_loaded(const char* path, int dim, int n_entries, const uint6
         h->entries[ids[e]] = std::move(er);
     }
     return h;
+}
+// time_stretch (vocoder.cpp:128-207) of one 1-D clip; returns the output length, or -1 when
+// the reference throws (empty clip, ratio outside [0.4, 2.5], bad config).
+int ref_time_stretch(const float* in, int n, int rate, double target_s, int window, int hop,
+                     float* out, int cap) {
+    AudioClip c;
+    c.samples.assign(in, in + n);
+    c.sample_rate = rate;
+    StftConfig cfg;
+    cfg.window_size = window;
+    cfg.analysis_hop = hop;
+    try {
+        AudioClip o = time_stretch(c, target_s, cfg);
+        const int m = (int)o.samples.size();
+        std::memcpy(out, o.samples.data(), sizeof(float) * (size_t)std::min(m, cap));
+        return m;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+// synth_latent (simgen.cpp:19-50): the simulated backend's 1-D latent of an embedding.
+int ref_synth_latent(const float* emb, int dim, double duration_s, int rate, float* out, int cap) {
+    auto v = synth_latent(vec(emb, dim), duration_s, rate);
+    std::memcpy(out, v.data(), sizeof(float) * (size_t)std::min<int>((int)v.size(), cap));
+    return (int)v.size();
 }
 int ref_save_embeddings(const char* path, const float* v, int n, int dim) {
     std::vector<EmbeddingVector> vs;

@@ -153,6 +153,8 @@ def lib() -> C.CDLL:
         "sw_ivf_set_centroids": ([vp, vp, i32], C.c_int),
         "sw_ivf_entry_lists": ([vp, u64, vp, i32], C.c_int),
         "sw_swix_load": ([vp, C.c_char_p], C.c_int),
+        "sw_time_stretch": ([vp, vp, vp, i32, i32, vp, i32, i32, vp, i64, vp, vp, vp, vp],
+                            C.c_int),
         "sw_swix_save": ([vp, C.c_char_p], C.c_int),
         "sw_swem_read": ([C.c_char_p, vp, i64, C.POINTER(i32), C.POINTER(i32)], i64),
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
@@ -177,7 +179,7 @@ EXPORTED = [
     "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
     "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",
     "sw_ivf_rebuild", "sw_ivf_info", "sw_ivf_centroids", "sw_ivf_set_centroids",
-    "sw_ivf_entry_lists", "sw_swix_load", "sw_swix_save", "sw_swem_read",
+    "sw_ivf_entry_lists", "sw_swix_load", "sw_swix_save", "sw_swem_read", "sw_time_stretch",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

@@ -616,6 +616,21 @@ int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t id, int16_t* lists, int32_t cap) {
     });
 }
 
+// ---------------------------------------------------------------- phase vocoder
+int sw_time_stretch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int32_t B,
+                    int32_t sample_rate, const double* target_s, int32_t window, int32_t hop,
+                    float* d_out, int64_t out_cap, int64_t* out_off, int32_t* out_len,
+                    int32_t* status, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(B >= 0 && (B == 0 || (d_in && in_off && in_len && target_s && d_out &&
+                                         out_off && out_len && status)),
+                   "null argument");
+        time_stretch_batch(d_in, in_off, in_len, B, sample_rate, target_s, window, hop, d_out,
+                           out_cap, out_off, out_len, status, as_stream(stream));
+        return SW_OK;
+    });
+}
+
 // ---------------------------------------------------------------- snapshots
 int sw_swix_load(sw_ctx* ctx, const char* path) {
     return guarded([&] {

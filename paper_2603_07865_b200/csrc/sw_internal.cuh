@@ -256,6 +256,11 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
 void ivf_on_remove(Ctx& c, int64_t slot);
 void ivf_set_centroids(Ctx& c, const float* h, int C);
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
+// phase-vocoder time stretch (vocoder.cu)
+int time_stretch_batch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int B,
+                       int rate, const double* target_s, int n, int hop_a, float* d_out,
+                       int64_t out_cap, int64_t* out_off, int32_t* out_len, int32_t* status,
+                       cudaStream_t st);
 // snapshots (host/snapshot.cpp)
 void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uint64_t*,
                                                         const int64_t*, const float*,

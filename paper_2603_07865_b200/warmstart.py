@@ -442,3 +442,29 @@ def read_swem(path: str) -> np.ndarray:
     out = np.zeros(max(nf, 0), np.float32)
     check(_lib.lib().sw_swem_read(path.encode(), ptr(out), nf, None, None), "sw_swem_read")
     return out.reshape(n.value, d.value)
+
+
+def time_stretch(clips, sample_rate: int, target_s, window: int = 128, hop: int = 32,
+                 device: int = 0, stream=None):
+    """time_stretch (vocoder.cpp:128-207) of a list of 1-D float32 clips on the GPU. Returns a
+    list of float32 arrays (None where the reference would throw)."""
+    torch = _torch()
+    clips = [np.ascontiguousarray(c, np.float32) for c in clips]
+    B = len(clips)
+    in_len = np.array([c.shape[0] for c in clips], np.int32)
+    in_off = np.concatenate([[0], np.cumsum(in_len)[:-1]]).astype(np.int64) if B else np.zeros(0, np.int64)
+    flat = np.concatenate(clips) if B and in_len.sum() else np.zeros(1, np.float32)
+    tgt = np.ascontiguousarray(target_s, np.float64)
+    cap = int(sum(max(0, round(t * sample_rate)) for t in tgt)) + 1
+    d_in = torch.from_numpy(flat).to(f"cuda:{device}")
+    d_out = torch.zeros(cap, dtype=torch.float32, device=f"cuda:{device}")
+    out_off = np.zeros(B, np.int64)
+    out_len = np.zeros(B, np.int32)
+    status = np.zeros(B, np.int32)
+    st = stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
+    check(_lib.lib().sw_time_stretch(ptr(d_in), ptr(in_off), ptr(in_len), B, sample_rate,
+                                     ptr(tgt), window, hop, ptr(d_out), cap, ptr(out_off),
+                                     ptr(out_len), ptr(status), st), "sw_time_stretch")
+    host = d_out.cpu().numpy()
+    return [None if status[b] else host[out_off[b]:out_off[b] + out_len[b]].copy()
+            for b in range(B)]
