@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--latent-slots", type=int, default=65536)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-latency", action="store_true")
+    p.add_argument("--no-vocoder", action="store_true",
+                   help="skip the phase-vocoder (time_stretch) side measurement")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
     p.add_argument("--ivf", default=None, metavar="C,NPROBE",
                    help="IVF mode (the reference's default index: 64,8): GPU k-means rebuild of "
@@ -458,6 +460,52 @@ def main():
             align_alone[mode] = a0.elapsed_time(a1) / reps
         del eps_t
 
+    # ---- phase-vocoder time_stretch (the reference's alignment, vocoder.cpp:128-207) side
+    # measurement: 1024 clips of the simulated 200 Hz 1-D latent, segment 4-12 s stretched to a
+    # served duration (ratio inside the duration gate's [2/3, 2]), STFT {128, 32}
+    vocoder = None
+    if world == 1 and not args.no_vocoder:
+        from paper_2603_07865_b200.warmstart import time_stretch
+        vr = np.random.default_rng(5)
+        nclip = 1024
+        clips, tg = [], []
+        for _ in range(nclip):
+            L_in = int(vr.integers(800, 2400))
+            t = np.arange(L_in) / 200.0
+            clips.append((0.5 * np.sin(2 * np.pi * vr.uniform(1, 20) * t)
+                          + 0.1 * vr.standard_normal(L_in)).astype(np.float32))
+            tg.append(L_in / 200.0 * float(vr.uniform(2 / 3, 2.0)))
+        for _ in range(2):
+            time_stretch(clips, 200, tg, device=local)
+        torch.cuda.synchronize(dev)
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        v0.record()
+        for _ in range(reps):
+            time_stretch(clips, 200, tg, device=local)
+        v1.record()
+        torch.cuda.synchronize(dev)
+        g_ms = v0.elapsed_time(v1) / reps
+        vocoder = {"clips": nclip, "config": "STFT window 128 hop 32 (pipeline.hpp:36), 200 Hz",
+                   "ms_per_batch_e2e": round(g_ms, 3),
+                   "clips_per_s": round(nclip / (g_ms / 1e3), 1),
+                   "note": "through the C-ABI with host clips (H2D + D2H inside)"}
+        if not args.no_cpu_baseline:
+            try:
+                import oracle
+                from concurrent.futures import ThreadPoolExecutor
+                ref = oracle.Ref()
+                nt = cpu_threads()
+                sample = list(range(0, nclip, 4))
+                t = time.perf_counter()
+                with ThreadPoolExecutor(nt) as ex:
+                    list(ex.map(lambda i: ref.time_stretch(clips[i], 200, tg[i]), sample))
+                el = time.perf_counter() - t
+                vocoder["cpu_ref_clips_per_s"] = round(len(sample) / el, 1)
+                vocoder["cpu_ref_cores"] = nt
+            except Exception as e:  # pragma: no cover
+                vocoder["cpu_ref_clips_per_s"] = f"unavailable: {e}"
+
     # ---- p50 selector latency (search through select, pipeline.cpp:93-143's selector_ms span)
     lat = {}
     if not args.no_latency and world == 1:
@@ -558,6 +606,7 @@ def main():
         **({"ivf": {"centroids": ivf[0], "nprobe": ivf[1], "rebuild_s": round(rebuild_s, 3),
                     "rebuild": "GPU k-means++ + Lloyd over %d rows (fp64, bit-identical to "
                                "index.cpp:59-184)" % n_rows}} if ivf else {}),
+        "vocoder": vocoder,
         "stage_ms": stage_ms,
         "selector_p50_ms": lat,
         "hit_rate": round(float(hits.mean()), 4),
