@@ -130,6 +130,10 @@ int sw_ctx_create(const sw_config* cfg, int device, sw_ctx** out);
 int sw_ctx_destroy(sw_ctx* ctx);
 const char* sw_last_error(void);
 int sw_version(void);
+/* Shape of a context: embedding dim, latent C / T_max / F (C = 0 without a latent arena),
+ * max batch, CUDA device. Any output may be NULL. */
+int sw_ctx_info(sw_ctx* ctx, int32_t* dim, int32_t* latent_c, int32_t* latent_t_max,
+                int32_t* latent_f, int32_t* max_batch, int32_t* device);
 
 /* SelectorConfig::negative_embedding (selector.hpp:31, make_negative_embedding selector.cpp:16-20).
  * Host pointer, D floats. Recomputes every stored row's s_neg. */
@@ -205,6 +209,23 @@ int sw_time_stretch(const float* d_in, const int64_t* in_off, const int32_t* in_
                     int32_t sample_rate, const double* target_s, int32_t window, int32_t hop,
                     float* d_out, int64_t out_cap, int64_t* out_off, int32_t* out_len,
                     int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- request batching (§8f)
+ * Aggregates concurrent single-request callers (the reference's per-connection
+ * Pipeline::handle_request, server.cpp:83,149) into device batches. swb_submit is thread-safe
+ * and blocks until its request's batch has run; a worker takes up to max_batch queued requests,
+ * waiting at most max_wait_us after the oldest for the batch to fill. Results equal one sw_plan
+ * (or sw_warmstart) over the same requests: draws and noise are keyed by request id. latent
+ * (optional, C x t_out_max x F floats) receives the aligned + noised latent when the batcher was
+ * created with_latent. */
+typedef struct swb_batcher swb_batcher;
+int swb_create(sw_ctx* ctx, int32_t max_batch, int32_t max_wait_us, uint64_t seed,
+               const sw_selector_config* sel, const sw_policy* policy, uint64_t philox_seed,
+               int32_t t_out_max, int32_t with_latent, swb_batcher** out);
+int swb_destroy(swb_batcher* b);
+int swb_submit(swb_batcher* b, const float* prompt, const sw_request* req, sw_choice* choice,
+               float* latent);
+int swb_stats(swb_batcher* b, int64_t* batches, int64_t* requests);
 
 /* ---------------------------------------------------------------- snapshots
  * IvfIndex::load (index.cpp:371-406) straight into an EMPTY context's device arena: entries,

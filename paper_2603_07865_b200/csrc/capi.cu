@@ -69,6 +69,7 @@ static void free_ctx(Ctx& c) {
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
     for (cudaEvent_t e : c.prof_ev) cudaEventDestroy(e);
+    if (c.scratch_ev) cudaEventDestroy(c.scratch_ev);
     if (c.mstream) cudaStreamDestroy(c.mstream);
 }
 
@@ -166,6 +167,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     SW_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
     SW_CUDA(cudaDeviceGetAttribute(&c.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     c.tc_ok = major == 10 && minor == 0 && encode_tensor_maps(c);
+    SW_CUDA(cudaEventCreateWithFlags(&c.scratch_ev, cudaEventDisableTiming));
 }
 
 // Reserve slots for n new entries (lowest free slot first) and update host bookkeeping.
@@ -335,6 +337,19 @@ using namespace sw;
 extern "C" {
 
 int sw_version(void) { return 1; }
+
+int sw_ctx_info(sw_ctx* ctx, int32_t* dim, int32_t* latent_c, int32_t* latent_t_max,
+                int32_t* latent_f, int32_t* max_batch, int32_t* device) {
+    if (!ctx) return SW_EINVAL;
+    const Ctx& c = ctx->c;
+    if (dim) *dim = c.D;
+    if (latent_c) *latent_c = c.latent ? c.C : 0;
+    if (latent_t_max) *latent_t_max = c.Tmax;
+    if (latent_f) *latent_f = c.F;
+    if (max_batch) *max_batch = c.Bmax;
+    if (device) *device = c.device;
+    return SW_OK;
+}
 
 const char* sw_last_error(void) { return g_last_error.c_str(); }
 
@@ -688,7 +703,7 @@ int sw_search(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, sw_hit* d_out
     return guarded([&] {
         SW_REQUIRE(ctx && (B == 0 || (d_q && d_out && d_n)), "null argument");
         Ctx& c = ctx->c;
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         int kn = launch_search(c, d_q, B, k, 0, st);
@@ -712,7 +727,7 @@ int sw_search_host(sw_ctx* ctx, const float* q, int32_t B, int32_t k, sw_hit* ou
         SW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         int rc;
         {
-            std::shared_lock lk(c.mu);
+            HotGuard lk(c, st);
             SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
                                     cudaMemcpyHostToDevice, st));
             int kn = launch_search(c, c.d_q_stage, B, k, 0, st);
@@ -755,7 +770,7 @@ int sw_plan(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, u
     return guarded([&] {
         SW_REQUIRE(ctx && (B == 0 || (d_q && d_req && d_out)), "null argument");
         Ctx& c = ctx->c;
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         c.last_kernels = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_out, as_stream(stream));
         return SW_OK;
@@ -798,7 +813,7 @@ int sw_warmstart(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t
     return guarded([&] {
         SW_REQUIRE(ctx && (B == 0 || (d_q && d_req && d_ch && d_out)), "null argument");
         Ctx& c = ctx->c;
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, st);
@@ -816,7 +831,7 @@ int sw_warmstart_host(sw_ctx* ctx, const float* q, const sw_request* reqs, int32
         SW_REQUIRE(ctx && (B == 0 || (q && reqs && choices && d_out)), "null argument");
         Ctx& c = ctx->c;
         SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
@@ -840,7 +855,7 @@ int sw_local_topk(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, int32_t r
         SW_REQUIRE(ctx && (B == 0 || (d_q && d_records && d_n)), "null argument");
         SW_REQUIRE(k >= 1 && k <= kMaxTopK, "k must be in [1, 32]");
         Ctx& c = ctx->c;
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         int kn = launch_search(c, d_q, B, k, rank, st);
@@ -862,7 +877,7 @@ int sw_merge_select(sw_ctx* ctx, const void* d_gathered, const int32_t* d_gn, in
         check_sel(sel, pol);
         SW_REQUIRE(k == sel->top_k, "merge k must equal the selector top_k");
         Ctx& c = ctx->c;
-        std::shared_lock lk(c.mu);
+        HotGuard lk(c, as_stream(stream));
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         launch_merge(c, reinterpret_cast<const HitRec*>(d_gathered), d_gn, world, B, k, st);

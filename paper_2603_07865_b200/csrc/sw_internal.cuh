@@ -91,6 +91,7 @@ __host__ __device__ __forceinline__ uint64_t d2ord(double d) {
 }
 
 // --------------------------------------------------------------------------- context
+struct Ctx;
 struct Ctx {
     sw_config cfg{};
     int device = 0;
@@ -180,6 +181,11 @@ struct Ctx {
     mutable std::shared_mutex mu;
 
     cudaStream_t mstream = nullptr;   // mutation stream
+    // Hot-path calls share the context's batch scratch (q_bf, thresholds, candidate buffers,
+    // staging): their enqueue is serialised on the host and their GPU work chained through
+    // scratch_ev, so concurrent readers on different streams never overlap on it.
+    std::mutex scratch_mu;
+    cudaEvent_t scratch_ev = nullptr;
     // stage profiling (CUDA events on the launching stream; single-threaded use)
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;   // pool, pairs (start, stop)
@@ -189,6 +195,23 @@ struct Ctx {
     int64_t prof_n[SW_NUM_STAGES] = {};
     // last launch info
     int last_kernels = 0, last_tc = 0, last_cand_max = 0;
+};
+
+// Reader guard of the hot path: shared with other readers against arena mutations, exclusive
+// with them on the batch scratch (host enqueue under scratch_mu, device work after the previous
+// reader's via scratch_ev).
+struct HotGuard {
+    std::shared_lock<std::shared_mutex> rd;
+    std::unique_lock<std::mutex> sc;
+    Ctx& c;
+    cudaStream_t st;
+    HotGuard(Ctx& c_, cudaStream_t st_) : rd(c_.mu), sc(c_.scratch_mu), c(c_), st(st_) {
+        cudaSetDevice(c.device);
+        if (c.scratch_ev) cudaStreamWaitEvent(st, c.scratch_ev, 0);
+    }
+    ~HotGuard() {
+        if (c.scratch_ev) cudaEventRecord(c.scratch_ev, st);
+    }
 };
 
 // RAII stage timer: records a (start, stop) event pair around the enclosed launches.

@@ -468,3 +468,49 @@ def time_stretch(clips, sample_rate: int, target_s, window: int = 128, hop: int 
     host = d_out.cpu().numpy()
     return [None if status[b] else host[out_off[b]:out_off[b] + out_len[b]].copy()
             for b in range(B)]
+
+
+class Batcher:
+    """swb_* (csrc/host/batcher.cpp): concurrent single-request callers -> device batches.
+    submit() is thread-safe and blocking (ctypes releases the GIL while it waits)."""
+
+    def __init__(self, cache: WarmStartCache, max_batch: int = 1024, max_wait_us: int = 200,
+                 seed: int = 1, sel: SelectorConfig = None, policy: Policy = None,
+                 philox_seed: int = 0, t_out_max: int = 0, with_latent: bool = False):
+        self.cache = cache
+        self._sel = (sel or SelectorConfig()).c()
+        self._pol = (policy or Policy()).c()
+        h = C.c_void_p()
+        check(_lib.lib().swb_create(cache._h, max_batch, max_wait_us, seed, C.byref(self._sel),
+                                    C.byref(self._pol), philox_seed, t_out_max, int(with_latent),
+                                    C.byref(h)), "swb_create")
+        self._h = h
+        self.latent_shape = (cache.latent_shape[0], t_out_max, cache.latent_shape[2]) \
+            if with_latent and cache.latent_shape else None
+
+    def submit(self, prompt: np.ndarray, req: np.ndarray, want_latent: bool = False):
+        """One request: prompt [D] float32, req a 1-element requests() record. Returns the
+        choice record (and the aligned latent when the batcher was built with_latent)."""
+        prompt = np.ascontiguousarray(prompt, np.float32)
+        req = np.ascontiguousarray(req)
+        ch = np.zeros(1, CHOICE_DTYPE)
+        lat = np.zeros(self.latent_shape, np.float32) if (want_latent and self.latent_shape) else None
+        check(_lib.lib().swb_submit(self._h, ptr(prompt), ptr(req), ptr(ch), ptr(lat)),
+              "swb_submit")
+        return (ch[0], lat) if want_latent else ch[0]
+
+    def stats(self):
+        b, r = C.c_int64(), C.c_int64()
+        check(_lib.lib().swb_stats(self._h, C.byref(b), C.byref(r)), "swb_stats")
+        return {"batches": b.value, "requests": r.value}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().swb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
