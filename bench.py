@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--latent-slots", type=int, default=65536)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-latency", action="store_true")
+    p.add_argument("--no-batcher", action="store_true",
+                   help="skip the request-batcher (swb_*) side measurement")
     p.add_argument("--no-vocoder", action="store_true",
                    help="skip the phase-vocoder (time_stretch) side measurement")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
@@ -390,6 +392,7 @@ def main():
         ev1.record(stream)
         barrier()
     wc.profile(False)
+    step_info = wc.launch_info()  # of the timed steps (later side measurements launch others)
     ms = ev0.elapsed_time(ev1)
     prof = wc.profile_read()
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cpu" if staged else dev)
@@ -506,6 +509,45 @@ def main():
             except Exception as e:  # pragma: no cover
                 vocoder["cpu_ref_clips_per_s"] = f"unavailable: {e}"
 
+    # ---- request batcher (swb_*): concurrent single-request clients (the
+    # reference's per-connection handle_request) grouped into device batches
+    batcher = None
+    if world == 1 and not args.no_batcher:
+        from concurrent.futures import ThreadPoolExecutor
+        from paper_2603_07865_b200.warmstart import Batcher
+        qh = qpool[0].cpu().numpy()
+        rq = reqs[0].cpu().numpy().view(req_np[0].dtype)
+        nclient, per = 256, 8
+        bt = Batcher(wc, max_batch=B, max_wait_us=300, seed=1, sel=sel, policy=pol,
+                     philox_seed=1234, t_out_max=T_)
+
+        def client(t):
+            lat = []
+            for j in range(per):
+                i = (t * per + j) % B
+                t0 = time.perf_counter()
+                bt.submit(qh[i], rq[i:i + 1])
+                lat.append(time.perf_counter() - t0)
+            return lat
+
+        with ThreadPoolExecutor(nclient) as ex:
+            list(ex.map(client, range(16)))  # warm-up
+            s0 = bt.stats()
+            t0 = time.perf_counter()
+            lats = sum(ex.map(client, range(nclient)), [])
+            wall = time.perf_counter() - t0
+        s1 = bt.stats()
+        bt.close()
+        nb = s1["batches"] - s0["batches"]
+        nr = s1["requests"] - s0["requests"]
+        lats.sort()
+        batcher = {"clients": nclient, "requests": nr, "requests_per_s": round(nr / wall, 1),
+                   "mean_batch": round(nr / max(1, nb), 1),
+                   "p50_ms": round(1e3 * lats[len(lats) // 2], 3),
+                   "p99_ms": round(1e3 * lats[int(len(lats) * 0.99)], 3),
+                   "note": "Python client threads, one blocking swb_submit per request "
+                           "(plan + align+noise), wall clock"}
+
     # ---- p50 selector latency (search through select, pipeline.cpp:93-143's selector_ms span)
     lat = {}
     if not args.no_latency and world == 1:
@@ -583,7 +625,7 @@ def main():
         **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
         "roofline": {"bound": "tensor",
                      "kernel": "k_score_tc (tcgen05.mma %s, TMA)" % (
-                         "cta_group::2 M256 N256 K16" if wc.launch_info()["cta_pair"]
+                         "cta_group::2 M256 N256 K16" if step_info["cta_pair"]
                          else "M128 N256 K16"),
                      "achieved": round(achieved, 1) if achieved else None, "peak": pk_burst,
                      "unit": "TFLOP/s", "frac": round(achieved / pk_burst, 4) if achieved else None,
@@ -607,6 +649,7 @@ def main():
                     "rebuild": "GPU k-means++ + Lloyd over %d rows (fp64, bit-identical to "
                                "index.cpp:59-184)" % n_rows}} if ivf else {}),
         "vocoder": vocoder,
+        "batcher": batcher,
         "stage_ms": stage_ms,
         "selector_p50_ms": lat,
         "hit_rate": round(float(hits.mean()), 4),
