@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--ivf", default=None, metavar="C,NPROBE",
                    help="IVF mode (the reference's default index: 64,8): GPU k-means rebuild of "
                         "the synthetic cache, then probe-restricted warm starts")
+    p.add_argument("--sharded-path", action="store_true",
+                   help="run the entry-sharded step (local top-k -> gather -> merge+select -> "
+                        "owner align) even at N=1: config 4's per-GPU work at --entries/GPU")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 script on ONE GPU (all ranks share cuda:0, "
                         "records all-gathered through host memory); never a bench number")
@@ -342,17 +345,23 @@ def main():
     rec_all = torch.empty((world * B * K * _lib.HIT_RECORD_BYTES,), dtype=torch.uint8, device=dev)
     n_all = torch.empty((world * B,), dtype=torch.int32, device=dev)
 
+    sharded = world > 1 or args.sharded_path
+
     def step(i):
         q = qpool[i % n_pool]
         r = reqs[i % n_pool]
-        if world == 1:
+        if not sharded:
             _lib.check(L_.sw_warmstart(wc._h, q.data_ptr(), r.data_ptr(), B, 1, Cc.byref(csel),
                                        Cc.byref(cpol), None, 1234, choices.data_ptr(),
                                        out.data_ptr(), T_, sp), "sw_warmstart")
         else:
             _lib.check(L_.sw_local_topk(wc._h, q.data_ptr(), B, K, rank, rec_local.data_ptr(),
                                         n_local_t.data_ptr(), sp), "sw_local_topk")
-            if staged:  # host-staged gather (gloo validation mode only)
+            if world == 1:  # --sharded-path at N=1: the gather of one rank is a copy
+                with torch.cuda.stream(stream):
+                    rec_all.copy_(rec_local)
+                    n_all.copy_(n_local_t)
+            elif staged:  # host-staged gather (gloo validation mode only)
                 stream.synchronize()
                 for src, dst in ((rec_local, rec_all), (n_local_t, n_all)):
                     parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
@@ -618,7 +627,7 @@ def main():
                                f"align+noise {C_}x{T_}x{F_} Philox"
                                + (f", IVF C={ivf[0]} nprobe={ivf[1]}" if ivf else ""),
                    "entries": args.entries, "rows_per_gpu": n_rows, "global_batch": B,
-                   "parallelism": f"entry-sharded x{world}" if world > 1 else "single",
+                   "parallelism": f"entry-sharded x{world}" if sharded else "single",
                    "l2": "inputs larger than L2 (bf16 arena %.0f MB streamed per step)"
                          % (n_rows * D * 2 / 1e6),
                    "latent_slots": min(args.latent_slots, n_local)},
