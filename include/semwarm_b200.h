@@ -318,7 +318,8 @@ int sw_profile_read(sw_ctx* ctx, int32_t stage, double* total_ms, int64_t* launc
  * enrichment, select). Synchronizes the device. */
 int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats);
 /* Launch statistics of the last sw_plan/sw_search on this context (kernels launched; scoring
- * mode: 0 exact fp64 only, 1 tcgen05 single CTAs, 2 tcgen05 CTA pairs (cta_group::2)). */
+ * mode: 0 exact fp64 only, 1 tcgen05 single CTAs, 2 tcgen05 CTA pairs (cta_group::2), 3 CTA
+ * pairs with the queries resident in TMEM). */
 int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
                         int32_t* candidates_max);
 

@@ -585,7 +585,7 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
         k_finish<<<B, FT, smem, st>>>(p);
     }
     SW_CUDA(cudaGetLastError());
-    c.last_tc = tc ? (c.last_score_pair ? 2 : 1) : 0;  // 2: tcgen05 CTA pairs
+    c.last_tc = tc ? (c.last_score_ts ? 3 : c.last_score_pair ? 2 : 1) : 0;  // 2: pairs, 3: +TS
     return kernels + 1;
 }
 

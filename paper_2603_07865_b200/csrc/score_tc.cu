@@ -43,6 +43,11 @@ constexpr int THREADS = 64 + 128 * EPI_GROUPS;
 
 constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
 constexpr uint32_t IDESC_PAIR = ptx::idesc_bf16_f32(2 * BM, BN);
+// TS mode (CTA pairs, A operand in TMEM): 128-column tiles so that 2 x 128 accumulator columns
+// + the 256 columns of the resident bf16 queries fill the 512 TMEM columns exactly.
+constexpr int BN_TS = 128;
+constexpr int B_QUARTER = (BN_TS / 2) * 128;  // bytes: each CTA stages 64 rows x 64 bf16
+constexpr uint32_t IDESC_TS = ptx::idesc_bf16_f32(2 * BM, BN_TS);
 
 struct TcParams {
     int B;
@@ -62,6 +67,7 @@ struct TcParams {
     float* cand_score;
     int n_chunks;
     int cap_local;
+    const __nv_bfloat16* q_bf;    // [BmaxPad][Dp] queries (TS mode loads them into TMEM)
     int ivf;                      // IVF mode: only rows of the query's probed lists count
     const int16_t* row_list;      // [rows] list of every stored row
     const uint64_t* pmask;        // [B][4] probed-list bitmask per query
@@ -119,16 +125,25 @@ __device__ __forceinline__ void emit_chunk(const uint32_t (&r)[32], uint32_t mas
 // (128 rows), so the per-SM L2 -> SM operand feed halves; the leader CTA issues the MMA for
 // both and its commits multicast to both CTAs' barriers. The epilogue is unchanged: TMEM lane
 // == query in each CTA. TEMPTY lives in the leader and counts both CTAs' epilogue warps.
-template <int RP, int KL, bool PAIR>
+//
+// TS (requires PAIR): the queries live in TMEM instead of shared memory (tcgen05.mma with an
+// [a-tmem] operand): the epilogue warps load their own query rows into TMEM columns
+// [256, 512) with tcgen05.st before the first tile, so every MMA reads only B from shared
+// memory — the smem crossbar (128 B/clk), which A + both B halves + the TMA writes saturated,
+// gets 25% headroom. Tiles shrink to 128 columns to make room in TMEM.
+template <int RP, int KL, bool PAIR, bool TS>
 __global__ void __launch_bounds__(THREADS, 1)
     k_score_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmE,
                const TcParams p) {
+    static_assert(!TS || PAIR, "TMEM-resident A is implemented for CTA pairs");
+    constexpr int TBN = TS ? BN_TS : BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    constexpr int BSTG = PAIR ? B_HALF : B_STAGE;
+    constexpr int KPS = TS ? 2 : 1;  // 64-wide K chunks per ring stage (TS: 2 x 8 KB boxes)
+    constexpr int BSTG = TS ? KPS * B_QUARTER : (PAIR ? B_HALF : B_STAGE);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + p.kch * A_CHUNK;
+    uint8_t* sB = smem + (TS ? 0 : p.kch * A_CHUNK);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * BSTG);
     const int S = p.n_stages;
     // full[S] | empty[S] | a_full | tfull[2] | tempty[2]
@@ -151,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(bar(FULL + i), 1);
             ptx::mbar_init(bar(EMPTY + i), 1);
         }
-        ptx::mbar_init(bar(AFULL), 1);
+        ptx::mbar_init(bar(AFULL), TS ? 8 : 1);  // TS: every epilogue warp of both CTAs
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar(TFULL + i), 1);
             ptx::mbar_init(bar(TEMPTY + i), PAIR ? 8 : 4);  // one group of 4 warps per acc
@@ -182,7 +197,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer
-            if (PAIR) {
+            if (TS) {
+                // queries go to TMEM through the epilogue warps
+            } else if (PAIR) {
                 // both CTAs load their own queries / their half of each tile; the bytes
                 // complete on the leader's barriers, whose expectation covers both halves
                 if (leader) ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(2 * p.kch * A_CHUNK));
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ph = 0;
             for (int lt = 0; lt < ntiles; ++lt) {
                 const int64_t tile = t0 + lt;
-                for (int kc = 0; kc < p.kch; ++kc, s = (s + 1 == S) ? 0 : s + 1,
+                for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
                          ph ^= (s == 0) ? 1u : 0u) {
                     ptx::mbar_wait_sleep(bar(EMPTY + s), ph ^ 1u);
                     if (p.experiment == 2) {
@@ -207,9 +224,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                         continue;
                     }
                     if (PAIR) {
-                        if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
-                        ptx::tma_load_2d_pair(ptx::smem_u32(sB + s * BSTG), &tmE, bar(FULL + s),
-                                              kc * 64, (int32_t)(tile * BN + rank * (BN / 2)));
+                        if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)(2 * BSTG));
+#pragma unroll
+                        for (int u = 0; u < KPS; ++u)
+                            ptx::tma_load_2d_pair(
+                                ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
+                                (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
                     } else {
                         ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
                         ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
@@ -224,7 +244,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---------------- MMA issuer: the converged warp waits, one elected lane issues
             // for the whole CTA / pair. Descriptors advance by constants (K16 step = 32 B =
             // 2 in the >>4 address field), keeping the per-chunk issue path short.
-            ptx::mbar_wait(bar(AFULL), 0);
+            if (TS)
+                ptx::mbar_wait_cluster(bar(AFULL), 0);
+            else
+                ptx::mbar_wait(bar(AFULL), 0);
             ptx::tc_fence_after();
             const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sA));
             const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sB));
@@ -235,8 +258,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t aph = (lt >> 1) & 1u;
                 ptx::mbar_wait_sleep(bar(TEMPTY + acc), aph ^ 1u);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kc = 0; kc < p.kch; ++kc, s = (s + 1 == S) ? 0 : s + 1,
+                const uint32_t d_tmem = tmem_base + acc * TBN;
+                for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
                          ph ^= (s == 0) ? 1u : 0u) {
                     ptx::mbar_wait_sleep(bar(FULL + s), ph);
                     ptx::tc_fence_after();
@@ -244,13 +267,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const uint64_t bd = bdesc0 + (uint64_t)(s * (BSTG >> 4));
                     if (ptx::elect_one()) {
 #pragma unroll
+                        for (int u = 0; u < KPS; ++u)
+#pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            if (PAIR)
-                                ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, IDESC_PAIR,
-                                                   (kc | k) != 0 ? 1u : 0u);
+                            const uint32_t acc_in = ((kc + u) | k) != 0 ? 1u : 0u;
+                            const uint64_t bk = bd + (uint64_t)(u * ((BSTG / KPS) >> 4)) + 2 * k;
+                            if (TS)
+                                ptx::mma_bf16_pair_ts(
+                                    d_tmem, tmem_base + 2 * TBN + (kc + u) * 32 + k * 8, bk,
+                                    IDESC_TS, acc_in);
+                            else if (PAIR)
+                                ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bk, IDESC_PAIR, acc_in);
                             else
-                                ptx::mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, IDESC,
-                                              (kc | k) != 0 ? 1u : 0u);
+                                ptx::mma_bf16(d_tmem, ad + 2 * k, bk, IDESC, acc_in);
                         }
                         // frees the smem stage (both CTAs' halves) when the MMAs finish
                         if (PAIR)
@@ -274,7 +303,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         // ---------------- epilogue: TMEM lane == query
         constexpr int E = 32 / RP;          // entries per 32-column chunk
-        constexpr int SPT = BN / RP;        // slots per tile
+        constexpr int SPT = TBN / RP;       // slots per tile
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
         const int vchunk = blockIdx.y * EPI_GROUPS + grp;
@@ -300,6 +329,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t g_next = qvalid ? __ldcg(&p.thr[q]) : 0u;  // shared k-th best, one tile ahead
         float pub_top1 = -INFINITY;
         int done = 0;  // tiles drained by this group
+        if (TS) {
+            // this warp's 32 query rows -> TMEM lanes [32 quarter, +32), columns [2 TBN, 2 TBN +
+            // Dp / 2): lane = query, column = bf16 pair (k, k+1) of the row, K-major
+            const uint4* qrow = reinterpret_cast<const uint4*>(
+                p.q_bf + (int64_t)(qblock * BM + quarter * 32 + lane) * (p.kch * 64));
+            for (int cb = 0; cb < p.kch * 32; cb += 32) {
+                uint32_t v[32];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint4 w = __ldg(qrow + cb / 4 + u);
+                    v[4 * u] = w.x;
+                    v[4 * u + 1] = w.y;
+                    v[4 * u + 2] = w.z;
+                    v[4 * u + 3] = w.w;
+                }
+                ptx::tmem_st32(lane_base + 2 * TBN + cb, v);
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(bar(AFULL), 0));
+        }
 
         for (int lt = grp; lt < ntiles; lt += EPI_GROUPS) {
             const int acc = lt & 1;
@@ -312,30 +363,45 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t slot0 = tile * SPT;
             ptx::mbar_wait_sleep(bar(TFULL + acc), aph);  // no spinning on the MMA's SMSPs
             ptx::tc_fence_after();
-            if (done == 0 && p.k <= BN / 32 && p.experiment == 0 && !p.ivf) {
+            constexpr int NSUB = (TS && E >= 2) ? 2 : 1;  // TS tiles have only 4 chunks
+            if (done == 0 && p.k <= NSUB * TBN / 32 && p.experiment == 0 && !p.ivf) {
                 // First tile of this slice: the threshold is still -inf, so a one-pass scan
                 // would emit the whole record sequence of the tile (~k + k ln(256/k)). A
-                // pre-pass takes each fully valid chunk's best entry; the k-th largest of
-                // those k+ distinct entries' scores (their minimum over >= k chunks, taken as
-                // the min over all 8) lower-bounds T_a, and the emitting pass starts from it.
+                // pre-pass takes each fully valid (sub-)chunk's best entry; the k-th largest of
+                // those k+ distinct entries' scores (their minimum over >= k (sub-)chunks) lower-
+                // bounds T_a, and the emitting pass starts from it.
                 float lo_best = INFINITY;
                 int n_full = 0;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = 0; c < TBN / 32; ++c) {
                     uint32_t r[32];
                     __syncwarp();
-                    ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
+                    ptx::tmem_ld32(lane_base + acc * TBN + c * 32, r);
                     const int64_t sc = slot0 + c * E;
                     uint32_t vb = __ldg(p.valid_bits + (sc >> 5)) >> (int)(sc & 31);
                     if (E < 32) vb &= (1u << (E & 31)) - 1u;
                     ptx::tmem_ld_wait();
-                    const float cmax = ptx::max32(r);
-                    if (vb == (E < 32 ? (1u << (E & 31)) - 1u : 0xFFFFFFFFu)) {
-                        lo_best = fminf(lo_best, fminf(1.0f, fmaxf(-1.0f, cmax)));
-                        ++n_full;
+#pragma unroll
+                    for (int h = 0; h < NSUB; ++h) {
+                        constexpr int EH = E / NSUB;
+                        float cmax;
+                        if (NSUB == 1) {
+                            cmax = ptx::max32(r);
+                        } else {
+                            cmax = __uint_as_float(r[16 * h]);
+#pragma unroll
+                            for (int j = 1; j < 16; ++j)
+                                cmax = fmaxf(cmax, __uint_as_float(r[16 * h + j]));
+                        }
+                        const uint32_t hb = (vb >> (EH * h)) & (EH < 32 ? (1u << (EH & 31)) - 1u
+                                                                         : 0xFFFFFFFFu);
+                        if (hb == (EH < 32 ? (1u << (EH & 31)) - 1u : 0xFFFFFFFFu)) {
+                            lo_best = fminf(lo_best, fminf(1.0f, fmaxf(-1.0f, cmax)));
+                            ++n_full;
+                        }
                     }
                 }
-                if (qvalid && n_full == BN / 32) {
+                if (qvalid && n_full == NSUB * TBN / 32) {
                     theta = fmaxf(theta, lo_best - eps2);
                     if (lo_best > published) {
                         atomicMax(&p.thr[q], f2ord(lo_best));
@@ -348,14 +414,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             // one tcgen05.ld, a 16-op FMNMX3 max tree over the raw scores, one compare; max and clamp
             // commute, so the per-entry clamped maxima are only formed on the rare path.
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < TBN / 32; ++c) {
                 if (p.experiment == 1 || p.experiment == 2) break;  // profiling: no epilogue
                 uint32_t r[32];
                 // tcgen05.ld is .sync.aligned: reconverge lanes that diverged on the previous
                 // chunk's emission path before it (a partially valid warp, B % 32 != 0, hangs
                 // otherwise)
                 __syncwarp();
-                ptx::tmem_ld32(lane_base + acc * BN + c * 32, r);
+                ptx::tmem_ld32(lane_base + acc * TBN + c * 32, r);
                 ptx::tmem_ld_wait();
                 if (qvalid && fminf(1.0f, fmaxf(-1.0f, ptx::max32(r))) >= theta) {
                     if (p.ivf) {
@@ -363,7 +429,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         // (index.cpp:306-307); the hot max above may include other rows, which
                         // only makes this rare path run more often, never changes a result
                         const uint4* rl4 = reinterpret_cast<const uint4*>(
-                            p.row_list + tile * BN + c * 32);
+                            p.row_list + tile * TBN + c * 32);
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             const uint4 w = __ldg(rl4 + v);
@@ -411,7 +477,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // their running bests is the k-th best of k distinct entries, <= T_a. It tracks
                 // the whole scanned prefix of the cache (a slice's own k-th best tracks only
                 // its 1/n_chunks share), so the emission threshold converges tiles earlier.
-                const float best = list[KL - p.k];
+                float best = -INFINITY;  // the best real slot (slots above the k-th hold +inf;
+#pragma unroll                                 // no dynamic index: list stays in registers)
+                for (int i = 0; i < KL; ++i) best = list[i] < INFINITY ? fmaxf(best, list[i]) : best;
                 if (best > pub_top1) {
                     __stcg(&p.top1[(int64_t)q * kMaxSlices + vchunk], f2ord(best));
                     pub_top1 = best;
@@ -495,10 +563,10 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32
     return r == CUDA_SUCCESS;
 }
 
-template <int RP, int KL, bool PAIR>
+template <int RP, int KL, bool PAIR, bool TS>
 void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     static bool attr_set = false;
-    auto kern = k_score_tc<RP, KL, PAIR>;
+    auto kern = k_score_tc<RP, KL, PAIR, TS>;
     if (!attr_set) {
         SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      c.smem_optin));
@@ -517,29 +585,29 @@ void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        SW_CUDA(cudaLaunchKernelEx(&cfg, kern, c.tm_q, c.tm_rows_half, p));
+        SW_CUDA(cudaLaunchKernelEx(&cfg, kern, c.tm_q, TS ? c.tm_rows_q64 : c.tm_rows_half, p));
     } else {
         kern<<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
     }
 }
 
-template <int RP, bool PAIR>
+template <int RP, bool PAIR, bool TS>
 void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     if (p.k <= 8)
-        launch_tc_kl<RP, 8, PAIR>(c, p, grid, smem, st);
+        launch_tc_kl<RP, 8, PAIR, TS>(c, p, grid, smem, st);
     else
-        launch_tc_kl<RP, 32, PAIR>(c, p, grid, smem, st);
+        launch_tc_kl<RP, 32, PAIR, TS>(c, p, grid, smem, st);
 }
 
-template <bool PAIR>
+template <bool PAIR, bool TS>
 void launch_tc(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     switch (c.Rp) {
-        case 1: launch_tc_rp<1, PAIR>(c, p, grid, smem, st); break;
-        case 2: launch_tc_rp<2, PAIR>(c, p, grid, smem, st); break;
-        case 4: launch_tc_rp<4, PAIR>(c, p, grid, smem, st); break;
-        case 8: launch_tc_rp<8, PAIR>(c, p, grid, smem, st); break;
-        case 16: launch_tc_rp<16, PAIR>(c, p, grid, smem, st); break;
-        case 32: launch_tc_rp<32, PAIR>(c, p, grid, smem, st); break;
+        case 1: launch_tc_rp<1, PAIR, TS>(c, p, grid, smem, st); break;
+        case 2: launch_tc_rp<2, PAIR, TS>(c, p, grid, smem, st); break;
+        case 4: launch_tc_rp<4, PAIR, TS>(c, p, grid, smem, st); break;
+        case 8: launch_tc_rp<8, PAIR, TS>(c, p, grid, smem, st); break;
+        case 16: launch_tc_rp<16, PAIR, TS>(c, p, grid, smem, st); break;
+        case 32: launch_tc_rp<32, PAIR, TS>(c, p, grid, smem, st); break;
         default: throw Error(SW_EINVAL, "rows per entry pad must be a power of two <= 32");
     }
 }
@@ -550,31 +618,48 @@ bool encode_tensor_maps(Ctx& c) {
     if (c.Dp > 512) return false;
     bool ok = encode_2d(&c.tm_rows, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN);
     ok = ok && encode_2d(&c.tm_rows_half, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN / 2);
+    ok = ok && encode_2d(&c.tm_rows_q64, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN_TS / 2);
     ok = ok && encode_2d(&c.tm_q, c.q_bf, (uint64_t)c.Dp, (uint64_t)c.BmaxPad, BM);
     return ok;
 }
 
 // Returns the number of kernels launched (1).
 int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
-    // grid: x = 128-query block, y = contiguous range of 256-row tiles (<= 148 CTAs per block row)
+    // grid: x = 128-query block, y = contiguous range of tiles (<= 148 CTAs per block row)
     TcParams p{};
     p.B = B;
     p.kch = c.Dp / 64;
-    const int budget = c.smem_optin - 1024 - 256;
-    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_STAGE);
-    SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
+    const int budget = c.smem_optin - 1024 - 512;
     p.k = k;
     const int qb = (B + BM - 1) / BM;
-    // CTA pairs need an even number of 128-query blocks; SW_SCORE_PAIR=0 forces single CTAs
+    // CTA pairs need an even number of 128-query blocks; SW_SCORE_PAIR=0 forces single CTAs.
+    // SW_SCORE_TS=1 keeps a pair's queries in TMEM (TS MMA). Measured slower and therefore off:
+    // the tensor core's A reads and the epilogue's accumulator reads then share the TMEM read
+    // port (MMA + feed 0.657 -> 0.715 ms, full kernel 0.749 -> 0.936 ms at 1M x 1024).
     static const bool pair_ok = [] {
         const char* e = getenv("SW_SCORE_PAIR");
         return !(e && e[0] == '0');
     }();
+    static const bool ts_ok = [] {
+        const char* e = getenv("SW_SCORE_TS");
+        return e && e[0] == '1';
+    }();
     const bool pair = pair_ok && qb >= 2 && qb % 2 == 0;
-    if (pair) p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_HALF);
+    const bool ts = pair && ts_ok && p.kch * 32 <= 256 && p.kch % 2 == 0;
+    int stage_bytes = B_STAGE, a_bytes = p.kch * A_CHUNK, max_stages = 8;
+    if (ts) {
+        stage_bytes = 2 * B_QUARTER;  // two 64-wide K chunks per stage
+        a_bytes = 0;
+        max_stages = 12;
+    } else if (pair) {
+        stage_bytes = B_HALF;
+    }
+    p.n_stages = std::min(max_stages, (budget - a_bytes) / stage_bytes);
+    SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
+    const int tbn = ts ? BN_TS : BN;
     const int64_t rows_hw = c.high_water * c.Rp;
-    p.n_tiles = (rows_hw + BN - 1) / BN;
-    const int qblocks = (B + BM - 1) / BM;
+    p.n_tiles = (rows_hw + tbn - 1) / tbn;
+    const int qblocks = qb;
     int64_t chunks = std::max<int64_t>(1, 148 / qblocks);
     chunks = std::min<int64_t>(chunks, p.n_tiles);
     p.tiles_per_cta = (p.n_tiles + chunks - 1) / chunks;
@@ -584,6 +669,7 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     p.q_eps = c.q_eps;
     p.thr = c.thr;
     p.top1 = c.top1;
+    p.q_bf = c.q_bf;
     p.ivf = ivf ? 1 : 0;
     p.row_list = c.row_list;
     p.pmask = c.pmask;
@@ -594,19 +680,21 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     p.n_chunks = (int)chunks * EPI_GROUPS;  // emission slices: (CTA, epilogue group)
     p.cap_local = (kCandCap / p.n_chunks) & ~3;  // multiple of 4: 16-byte aligned slices
     c.last_chunks = p.n_chunks;
-    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK +
-                        (size_t)p.n_stages * (pair ? B_HALF : B_STAGE) + 256;
+    const size_t smem = 1024 + (size_t)a_bytes + (size_t)p.n_stages * stage_bytes + 512;
     c.last_score_pair = pair;
+    c.last_score_ts = ts;
     static const int experiment = [] {
         const char* e = getenv("SW_SCORE_EXPERIMENT");
         return e ? atoi(e) : 0;
     }();
     p.experiment = experiment;
     dim3 grid((unsigned)qblocks, (unsigned)chunks);
-    if (pair)
-        launch_tc<true>(c, p, grid, smem, st);
+    if (ts)
+        launch_tc<true, true>(c, p, grid, smem, st);
+    else if (pair)
+        launch_tc<true, false>(c, p, grid, smem, st);
     else
-        launch_tc<false>(c, p, grid, smem, st);
+        launch_tc<false, false>(c, p, grid, smem, st);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

@@ -137,6 +137,7 @@ struct Ctx {
     int last_chunks = 1;
     bool last_ivf = false;         // last search probed IVF lists (nprobe < C)
     bool last_score_pair = false;  // last scoring launch ran as tcgen05 CTA pairs
+    bool last_score_ts = false;    // ... with the queries resident in TMEM (TS MMA)
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
     double* cand_exact = nullptr;   // [Bmax][kCandCap]
@@ -153,6 +154,7 @@ struct Ctx {
     // TMA descriptors (encoded once at creation; cover the full capacity)
     CUtensorMap tm_rows{};
     CUtensorMap tm_rows_half{};  // 128-row boxes for the CTA-pair scoring kernel
+    CUtensorMap tm_rows_q64{};   // 64-row boxes for the CTA-pair TMEM-A (TS) kernel
     CUtensorMap tm_q{};
     bool tc_ok = false;
     int smem_optin = 0;

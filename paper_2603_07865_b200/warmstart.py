@@ -238,7 +238,8 @@ class WarmStartCache:
     def launch_info(self):
         k, t, m = C.c_int32(), C.c_int32(), C.c_int32()
         _lib.lib().sw_last_launch_info(self._h, C.byref(k), C.byref(t), C.byref(m))
-        return {"kernels": k.value, "tensor_cores": bool(t.value), "cta_pair": t.value == 2}
+        return {"kernels": k.value, "tensor_cores": bool(t.value), "cta_pair": t.value >= 2,
+                "a_in_tmem": t.value == 3}
 
     # ------------------------------------------------------------------ hot path
     def _dev(self, a, dtype):
