@@ -255,7 +255,13 @@ class Ref:
         L.ref_cache_new.restype = C.c_void_p
         L.ref_cache_new.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64]
+        L.ref_cache_new_ivf.restype = C.c_void_p
+        L.ref_cache_new_ivf.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                        C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_uint64,
+                                        C.c_uint64]
         L.ref_cache_free.argtypes = [C.c_void_p]
+        L.ref_cache_index_save.restype = C.c_int
+        L.ref_cache_index_save.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_cache_admit.restype = C.c_int64
         L.ref_cache_admit.argtypes = [C.c_void_p, f32p, C.c_int, C.c_double, C.c_double, C.c_double]
         L.ref_cache_record_reuse.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_double,

@@ -471,7 +471,31 @@ void* ref_cache_new(uint64_t capacity, double decay, double grace, double floor_
     r->cm->index().set_rebuild_interval(UINT64_MAX);
     return r;
 }
+// CacheManager in IVF mode exactly as Pipeline builds it (pipeline.cpp:79-81)
+void* ref_cache_new_ivf(uint64_t capacity, double decay, double grace, double floor_q,
+                        double delta, uint64_t emb_seed, int centroids, int nprobe,
+                        uint64_t index_seed, uint64_t interval) {
+    CacheConfig c;
+    c.capacity = capacity;
+    c.decay_per_hour = decay;
+    c.grace_hours = grace;
+    c.quality_floor = floor_q;
+    c.pyramid_delta = delta;
+    c.embedding_seed = emb_seed;
+    auto* r = new RefCache;
+    r->cm = std::make_unique<CacheManager>(c, (uint32_t)centroids, (uint32_t)nprobe, index_seed);
+    r->cm->index().set_rebuild_interval(interval);
+    return r;
+}
 void ref_cache_free(void* p) { delete static_cast<RefCache*>(p); }
+int ref_cache_index_save(void* p, const char* path) {
+    try {
+        static_cast<RefCache*>(p)->cm->index().save(path);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return (int)static_cast<RefCache*>(p)->cm->index().centroid_count();
+}
 // admit a clip with the given embedding/duration (latent is irrelevant to every policy decision)
 int64_t ref_cache_admit(void* p, const float* emb, int dim, double duration, double quality,
                         double now_h) {

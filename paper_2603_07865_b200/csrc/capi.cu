@@ -140,6 +140,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.prank, (size_t)c.Bmax * kMaxCentroids);
     dalloc(&c.pmask, (size_t)c.Bmax * 4);
     c.ivf_rows.assign((size_t)c.S, 0);
+    SW_CUDA(cudaMemset(c.row_list, 0xFF, sizeof(int16_t) * (size_t)nrow));  // no list
     SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
     SW_CUDA(cudaMemsetAsync(c.valid, 0, (size_t)c.S, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.valid_bits, 0, sizeof(uint32_t) * (size_t)(c.S / 32 + 16), c.mstream));
@@ -531,7 +532,12 @@ int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t 
         c.high_water += n;
         // IVF mode: a bulk load like IvfIndex::build(vecs) — no mutation counting; rows join the
         // current centroids' lists (sw_ivf_rebuild re-clusters)
-        if (c.ivf && c.ivf_C > 0) ivf_set_centroids(c, c.h_cent.data(), c.ivf_C);
+        if (c.ivf) {
+            std::vector<int64_t> sl((size_t)n);
+            for (int64_t i = 0; i < n; ++i) sl[(size_t)i] = slot0 + i;
+            ivf_mark_tails(c, sl, std::vector<int32_t>((size_t)n, c.R));
+            if (c.ivf_C > 0) ivf_set_centroids(c, c.h_cent.data(), c.ivf_C);
+        }
         return SW_OK;
     });
 }

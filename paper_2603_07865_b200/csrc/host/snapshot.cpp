@@ -137,7 +137,16 @@ void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uin
             std::memcpy(pad.data() + (size_t)j * c.Df, cent.data() + (size_t)j * dim, 4 * dim);
         SW_CUDA(cudaMemcpy(c.cent, pad.data(), 4 * pad.size(), cudaMemcpyHostToDevice));
     }
-    // stored list of every row (the snapshot's lists, not recomputed)
+    // stored list of every row (the snapshot's lists, not recomputed); pad rows in no list
+    {
+        std::vector<int64_t> sl;
+        std::vector<int32_t> nrr;
+        for (uint64_t id : ids) {
+            sl.push_back(c.slot_of.at(id));
+            nrr.push_back(c.h_nrows[(size_t)sl.back()]);
+        }
+        ivf_mark_tails(c, sl, nrr);
+    }
     size_t k = 0;
     for (uint64_t id : ids) {
         const int64_t slot = c.slot_of.at(id);

@@ -222,6 +222,17 @@ __global__ void k_probe_rank(const float* __restrict__ q, int D, const float* __
     }
 }
 
+// rows [nrows[slot], Rp) of each slot belong to no list (pad rows repeat row 0 in the bf16
+// shadow; they must never make an entry eligible through a stale list id)
+__global__ void k_list_tails(const int64_t* __restrict__ slots, const int32_t* __restrict__ nr,
+                             int64_t n, int Rp, int16_t* __restrict__ row_list) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * Rp) return;
+    const int64_t e = i / Rp;
+    const int r = (int)(i - e * Rp);
+    if (r >= nr[e]) row_list[slots[e] * Rp + r] = -1;
+}
+
 // --------------------------------------------------------------------------- host helpers
 struct MtRng {  // Rng (core.hpp:75-93) over the standard-specified mt19937_64
     std::mt19937_64 g;
@@ -409,6 +420,20 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
 
 }  // namespace
 
+void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector<int32_t>& nr) {
+    if (slots.empty()) return;
+    DBuf<int64_t> d_s(slots.size());
+    DBuf<int32_t> d_n(nr.size());
+    SW_CUDA(cudaMemcpy(d_s.p, slots.data(), sizeof(int64_t) * slots.size(), cudaMemcpyHostToDevice));
+    SW_CUDA(cudaMemcpy(d_n.p, nr.data(), sizeof(int32_t) * nr.size(), cudaMemcpyHostToDevice));
+    const int64_t tot = (int64_t)slots.size() * c.Rp;
+    k_list_tails<<<(unsigned)((tot + 255) / 256), 256, 0, c.mstream>>>(d_s.p, d_n.p,
+                                                                    (int64_t)slots.size(), c.Rp,
+                                                                    c.row_list);
+    SW_CUDA(cudaGetLastError());
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+}
+
 // Rows the index knows about, in the reference's rebuild order: entries by id, each entry's rows
 // by (level, start) (index.cpp:267-272).
 static std::vector<int64_t> rebuild_order(Ctx& c) {
@@ -459,6 +484,11 @@ void ivf_rebuild(Ctx& c) {
 void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<int32_t>& base,
                    const std::vector<int32_t>& nr) {
     const size_t n = slot.size();
+    {
+        std::vector<int32_t> tot(n);
+        for (size_t e = 0; e < n; ++e) tot[e] = base[e] + nr[e];
+        ivf_mark_tails(c, slot, tot);
+    }
     size_t e0 = 0;
     while (e0 < n) {
         if (nr[e0] > 0 && c.ivf_C == 0) {  // first insertion seeds a single centroid

@@ -279,6 +279,7 @@ void ivf_rebuild(Ctx& c);
 void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<int32_t>& base,
                    const std::vector<int32_t>& nr);
 void ivf_on_remove(Ctx& c, int64_t slot);
+void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector<int32_t>& nr);
 void ivf_set_centroids(Ctx& c, const float* h, int C);
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
 // phase-vocoder time stretch (vocoder.cu)

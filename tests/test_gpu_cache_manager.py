@@ -25,15 +25,21 @@ def _ref_cands(ref, h):
     return buf[:n].tolist()
 
 
-@pytest.mark.parametrize("seed", [1, 2])
-def test_cache_manager_matches_reference(ref, seed):
+@pytest.mark.parametrize("seed,ivf", [(1, None), (2, None), (3, (8, 2, 120, 17))])
+def test_cache_manager_matches_reference(ref, seed, ivf):
+    """ivf = (centroids, nprobe, rebuild interval, index seed): the reference's default IVF
+    index under the same churn (rebuilds triggered by admits, evictions and refines)."""
     from paper_2603_07865_b200.warmstart import CacheManager, WarmStartCache
     dim, cap, delta = 64, 48, 0.25
     emb_seed = ref.derive_seed(seed, 0x5345474D)
     wc = WarmStartCache(dim, rows_per_entry=7, max_entries=cap + 8, max_batch=32,
                         latent_shape=None, tc_always=True)
+    if ivf:
+        wc.ivf_configure(ivf[0], ivf[1], ivf[2], ivf[3])
     cm = CacheManager(wc, capacity=cap, pyramid_delta=delta, embedding_seed=emb_seed)
-    rh = ref.lib.ref_cache_new(cap, 0.9, 1.0, 0.3, delta, emb_seed)
+    rh = (ref.lib.ref_cache_new(cap, 0.9, 1.0, 0.3, delta, emb_seed) if not ivf else
+          ref.lib.ref_cache_new_ivf(cap, 0.9, 1.0, 0.3, delta, emb_seed, ivf[0], ivf[1],
+                                        ivf[3], ivf[2]))
     rng = np.random.default_rng(seed)
     centres = ref.random_unit_vectors(seed + 100, 6, dim)
     now = 0.0
@@ -112,3 +118,5 @@ def test_cache_manager_matches_reference(ref, seed):
     finally:
         ref.lib.ref_cache_free(rh)
     assert n_admit > 100 and n_reuse > 100 and n_refine > 10 and n_refined > 0
+    if ivf:
+        assert wc.ivf_info()["rebuilds"] > 5  # re-clustered many times during the churn
