@@ -409,20 +409,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
             }
-            // Hot loop kept compact (not unrolled: the rare emission path is instantiated once,
-            // so the epilogue stays resident in the instruction cache). Per 32-column chunk:
-            // one tcgen05.ld, a 16-op FMNMX3 max tree over the raw scores, one compare; max and clamp
-            // commute, so the per-entry clamped maxima are only formed on the rare path.
-#pragma unroll 1
-            for (int c = 0; c < TBN / 32; ++c) {
-                if (p.experiment == 1 || p.experiment == 2) break;  // profiling: no epilogue
-                uint32_t r[32];
-                // tcgen05.ld is .sync.aligned: reconverge lanes that diverged on the previous
-                // chunk's emission path before it (a partially valid warp, B % 32 != 0, hangs
-                // otherwise)
-                __syncwarp();
-                ptx::tmem_ld32(lane_base + acc * TBN + c * 32, r);
-                ptx::tmem_ld_wait();
+            // Hot loop kept compact (rolled: the rare emission path is instantiated twice, so
+            // the epilogue stays resident in the instruction cache). Per 32-column chunk: a
+            // 16-op FMNMX3 max tree over the raw scores and one compare; max and clamp commute,
+            // so the per-entry clamped maxima are only formed on the rare path. The TMEM loads
+            // are software-pipelined over two register buffers: chunk c + 1 is in flight while
+            // chunk c is examined, halving the epilogue's drain latency per tile (the MMA can
+            // reuse an accumulator only once the epilogue released it).
+            auto examine = [&](uint32_t(&r)[32], int c) {
                 if (qvalid && fminf(1.0f, fmaxf(-1.0f, ptx::max32(r))) >= theta) {
                     if (p.ivf) {
                         // IVF: a row counts only if its list is among the query's probed lists
@@ -461,6 +455,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mask &= vbits;
                     if (mask)
                         emit_chunk<RP, KL>(r, mask, sc, theta, list, kth, eps2, cnt, slice, p);
+                }
+                // tcgen05.ld is .sync.aligned: reconverge lanes that diverged on the emission
+                // path before the next one (a partially valid warp, B % 32 != 0, hangs otherwise)
+                __syncwarp();
+            };
+            if (p.experiment != 1 && p.experiment != 2) {
+                constexpr int NCH = TBN / 32;  // even
+                const uint32_t tb = lane_base + acc * TBN;
+                uint32_t ra[32], rb[32];
+                __syncwarp();
+                ptx::tmem_ld32(tb, ra);
+                ptx::tmem_ld_wait();
+#pragma unroll 1
+                for (int c = 0; c < NCH; c += 2) {
+                    ptx::tmem_ld32(tb + (c + 1) * 32, rb);  // in flight while chunk c is examined
+                    examine(ra, c);
+                    ptx::tmem_ld_wait();
+                    if (c + 2 < NCH) ptx::tmem_ld32(tb + (c + 2) * 32, ra);
+                    examine(rb, c + 1);
+                    ptx::tmem_ld_wait();
                 }
             }
             ptx::tc_fence_before();
