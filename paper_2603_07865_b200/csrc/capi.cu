@@ -64,7 +64,9 @@ static void free_ctx(Ctx& c) {
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
-                    c.cent, c.row_list, c.prank, c.pmask};
+                    c.cent, c.row_list, c.prank, c.pmask, c.d_sorted_slot, c.d_rows_sorted,
+                    c.d_sorted_vbits, c.d_list_tile0, c.d_list_ntiles, c.d_qcnt, c.d_qlist,
+                    c.d_qbase, c.d_qg, c.d_qmap, c.d_items};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);

@@ -530,9 +530,16 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
         ivf = launch_probe_rank(c, d_q, B, st);  // IvfIndex probe lists (nprobe < C)
     }
     kernels += ivf ? 1 : 0;
+    int64_t grp_items = 0;
+    if (ivf && tc) {  // reference-default IVF, one row per entry: list-grouped tcgen05 GEMM
+        StageScope sc(c, SW_STAGE_PREP, st);
+        grp_items = ivf_group_prepare(c, B, st);
+        kernels += grp_items > 0 ? 4 : 0;
+    }
     if (tc) {
         StageScope sc(c, SW_STAGE_SCORE_TC, st);
-        kernels += launch_score_tc(c, B, k, ivf, st);
+        kernels += grp_items > 0 ? launch_score_tc_grouped(c, B, k, grp_items, st)
+                                 : launch_score_tc(c, B, k, ivf, st);
     }
     FinishParams p{};
     p.B = B;

@@ -124,6 +124,7 @@ void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uin
     if (!ids.empty())
         insert(c, (int64_t)ids.size(), ids.data(), off.data(), rows.data(), segs.data());
     c.ivf = true;
+    c.grp_dirty = true;
     c.ivf_target = std::max<int>(1, (int)C);
     c.ivf_nprobe = (int)nprobe;
     c.ivf_seed = 0;

@@ -187,6 +187,58 @@ __global__ void k_farthest(const float* __restrict__ rows, int Df, int D,
     }
 }
 
+// Probe ranking, centroids staged once per block (transposed [D][CP] in smem, conflict-free) and
+// reused for the block's queries: group g of CP threads ranks query b; thread j computes
+// dot(q_b, c_j) sequentially in dimension order, then its rank as below.
+template <int CP>
+__global__ void __launch_bounds__(256) k_probe_rank_smem(const float* __restrict__ q, int B, int D,
+                                                          const float* __restrict__ cent, int Df,
+                                                          int C, int np,
+                                                          uint8_t* __restrict__ prank,
+                                                          uint64_t* __restrict__ pmask) {
+    extern __shared__ float sm[];
+    float* cT = sm;                       // [D][CP]
+    constexpr int G = 256 / CP;           // queries per pass
+    double* sc = reinterpret_cast<double*>(cT + (size_t)D * CP);  // [G][CP]
+    for (int i = threadIdx.x; i < D * CP; i += blockDim.x) {
+        const int d = i / CP, j = i % CP;
+        cT[i] = j < C ? cent[(int64_t)j * Df + d] : 0.0f;
+    }
+    __syncthreads();
+    const int g = threadIdx.x / CP, j = threadIdx.x % CP;
+    for (int b0 = blockIdx.x * G; b0 < B; b0 += gridDim.x * G) {
+        const int b = b0 + g;
+        double a = 0.0;
+        if (b < B && j < C) {
+            const float* qb = q + (int64_t)b * D;
+            for (int d = 0; d < D; ++d) a = fma((double)__ldg(qb + d), (double)cT[d * CP + j], a);
+        }
+        sc[g * CP + j] = a;
+        __syncthreads();
+        if (b < B) {
+            uint8_t r = kNotProbed;
+            if (j < C) {
+                int rank = 0;
+                for (int i = 0; i < C; ++i) {
+                    const double si = sc[g * CP + i], sj = sc[g * CP + j];
+                    rank += (si > sj || (si == sj && i < j)) ? 1 : 0;
+                }
+                if (rank < np) r = (uint8_t)rank;
+            }
+            for (int jj = j; jj < kMaxCentroids; jj += CP)
+                prank[(int64_t)b * kMaxCentroids + jj] = jj == j ? r : kNotProbed;
+            const unsigned ballot = __ballot_sync(0xffffffffu, r != kNotProbed);
+            if ((j & 31) == 0) {
+                uint32_t* pm32 = reinterpret_cast<uint32_t*>(pmask + (int64_t)b * 4);
+                pm32[j >> 5] = ballot;
+                if (j == 0)
+                    for (int w = CP / 32; w < 8; ++w) pm32[w] = 0u;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Probe ranking per query (index.cpp:295-304): thread j computes dot(q, c_j) sequentially, its
 // rank = #{i : s_i > s_j or (s_i == s_j and i < j)} is its position in the partial sort. Writes
 // the rank (255 when not among the first nprobe) and the probed-list bitmask.
@@ -231,6 +283,101 @@ __global__ void k_list_tails(const int64_t* __restrict__ slots, const int32_t* _
     const int64_t e = i / Rp;
     const int r = (int)(i - e * Rp);
     if (r >= nr[e]) row_list[slots[e] * Rp + r] = -1;
+}
+
+// ---- grouped IVF search (one row per entry) --------------------------------------------
+// queries of each probed list: qlist[l][*] (order irrelevant: a query's results do not depend
+// on which block it shares)
+__global__ void k_group_count(const uint8_t* __restrict__ prank, int C, int np,
+                              int32_t* __restrict__ qcnt, int32_t* __restrict__ qlist, int Bmax) {
+    const int q = blockIdx.x, j = threadIdx.x;
+    if (j >= C) return;
+    if (prank[(int64_t)q * kMaxCentroids + j] < np) {
+        const int pos = atomicAdd(&qcnt[j], 1);
+        qlist[(int64_t)j * Bmax + pos] = q;
+    }
+}
+
+// work items: list j, query block b of its queries, tile chunk jj of its tiles
+__global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
+                             const int32_t* __restrict__ tile0, const int32_t* __restrict__ ntl,
+                             int tpc, int32_t* __restrict__ qbase, int4* __restrict__ items) {
+    __shared__ int s_nb[kMaxCentroids], s_ni[kMaxCentroids];
+    const int j = threadIdx.x;
+    int nb = 0, ch = 0;
+    if (j < C && qcnt[j] > 0 && ntl[j] > 0) {
+        nb = (qcnt[j] + 127) / 128;
+        ch = (ntl[j] + tpc - 1) / tpc;
+    }
+    s_nb[j] = nb;
+    s_ni[j] = nb * ch;
+    __syncthreads();
+    if (j == 0) {  // exclusive scans over <= 256 lists
+        int a = 0, b = 0;
+        for (int i = 0; i < kMaxCentroids; ++i) {
+            const int x = s_nb[i], y = s_ni[i];
+            s_nb[i] = a;
+            s_ni[i] = b;
+            a += x;
+            b += y;
+        }
+        qbase[kMaxCentroids] = a;
+    }
+    __syncthreads();
+    if (j < kMaxCentroids) qbase[j] = s_nb[j];
+    for (int b = 0; b < nb; ++b)
+        for (int jj = 0; jj < ch; ++jj)
+            items[s_ni[j] + b * ch + jj] =
+                make_int4((s_nb[j] + b) * 128, tile0[j] + jj * tpc, min(tpc, ntl[j] - jj * tpc),
+                          j | (jj << 8));
+}
+
+// gathered query rows (one warp per row): qg[g] = q_bf[qmap[g]] (zeros for padding)
+__global__ void k_group_gather(const int32_t* __restrict__ qcnt,
+                               const int32_t* __restrict__ qlist, const int32_t* __restrict__ qbase,
+                               int C, int Bmax, const __nv_bfloat16* __restrict__ q_bf, int Dp,
+                               __nv_bfloat16* __restrict__ qg, int32_t* __restrict__ qmap,
+                               int64_t rows) {
+    const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= rows) return;
+    const int blk = (int)(g / 128), r = (int)(g % 128);
+    int q = -1;
+    if (blk < qbase[kMaxCentroids]) {
+        int lo = 0, hi = C - 1;  // last list with qbase <= blk
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (qbase[mid] <= blk) lo = mid; else hi = mid - 1;
+        }
+        const int idx = (blk - qbase[lo]) * 128 + r;
+        if (idx < qcnt[lo]) q = qlist[(int64_t)lo * Bmax + idx];
+    }
+    if (lane == 0) qmap[g] = q;
+    const uint4* src = reinterpret_cast<const uint4*>(q_bf + (int64_t)(q < 0 ? 0 : q) * Dp);
+    uint4* dst = reinterpret_cast<uint4*>(qg + g * Dp);
+    for (int i = lane; i < Dp / 8; i += 32) dst[i] = q < 0 ? make_uint4(0, 0, 0, 0) : src[i];
+}
+
+// list-sorted arena copy: row r <- arena row sorted_slot[r] (zeros for tile padding)
+__global__ void k_sort_rows(const int32_t* __restrict__ sorted_slot, int64_t rows,
+                            const __nv_bfloat16* __restrict__ src, int Dp,
+                            __nv_bfloat16* __restrict__ dst) {
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const int32_t s = sorted_slot[r];
+    const uint4* a = reinterpret_cast<const uint4*>(src + (int64_t)(s < 0 ? 0 : s) * Dp);
+    uint4* b = reinterpret_cast<uint4*>(dst + r * Dp);
+    for (int i = lane; i < Dp / 8; i += 32) b[i] = s < 0 ? make_uint4(0, 0, 0, 0) : a[i];
+}
+
+// unvisited (query, slice) pairs read as empty by the finish kernel
+__global__ void k_fill_slices(int B, int n_chunks, int k, int32_t* __restrict__ slice_cnt,
+                              float* __restrict__ cta_topk) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)B * n_chunks) return;
+    slice_cnt[i] = 0;
+    for (int t = 0; t < k; ++t) cta_topk[i * kMaxTopK + t] = -INFINITY;
 }
 
 // --------------------------------------------------------------------------- host helpers
@@ -462,6 +609,7 @@ static std::vector<int64_t> rebuild_order(Ctx& c) {
 
 // IvfIndex::rebuild (index.cpp:257-283)
 void ivf_rebuild(Ctx& c) {
+    c.grp_dirty = true;
     c.ivf_mutations = 0;
     c.ivf_rebuilds++;
     std::vector<int64_t> perm = rebuild_order(c);
@@ -484,6 +632,7 @@ void ivf_rebuild(Ctx& c) {
 void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<int32_t>& base,
                    const std::vector<int32_t>& nr) {
     const size_t n = slot.size();
+    c.grp_dirty = true;
     {
         std::vector<int32_t> tot(n);
         for (size_t e = 0; e < n; ++e) tot[e] = base[e] + nr[e];
@@ -522,12 +671,14 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
 
 // IvfIndex::remove (index.cpp:236-255), after the slot was cleared.
 void ivf_on_remove(Ctx& c, int64_t slot) {
+    c.grp_dirty = true;
     c.ivf_mutations += (uint64_t)c.ivf_rows[(size_t)slot];
     c.ivf_rows[(size_t)slot] = 0;
     if (c.ivf_mutations >= c.ivf_interval) ivf_rebuild(c);
 }
 
 void ivf_set_centroids(Ctx& c, const float* h, int C) {
+    c.grp_dirty = true;
     c.h_cent.assign(h, h + (size_t)C * c.D);
     c.ivf_C = C;
     upload_centroids(c, c.h_cent, C);
@@ -543,6 +694,128 @@ void ivf_set_centroids(Ctx& c, const float* h, int C) {
     }
 }
 
+// ---------------------------------------------------------------- grouped IVF search
+// The list-sorted arena copy: rows of list l contiguous from tile grp_tile0[l] (tile-aligned,
+// so every 256-row tile belongs to ONE list), ascending slot order inside a list.
+static void build_sorted(Ctx& c) {
+    const int64_t S = c.high_water;
+    const int C = c.ivf_C;
+    std::vector<uint8_t> valid((size_t)S);
+    std::vector<int16_t> rl((size_t)S);
+    if (S > 0) {
+        SW_CUDA(cudaMemcpy(valid.data(), c.valid, S, cudaMemcpyDeviceToHost));
+        SW_CUDA(cudaMemcpy(rl.data(), c.row_list, 2 * S, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int64_t> cnt((size_t)C, 0);
+    for (int64_t i = 0; i < S; ++i)
+        if (valid[(size_t)i] && rl[(size_t)i] >= 0 && rl[(size_t)i] < C) ++cnt[(size_t)rl[(size_t)i]];
+    c.grp_tile0.assign((size_t)C, 0);
+    c.grp_ntiles.assign((size_t)C, 0);
+    int64_t t = 0;
+    int maxt = 0;
+    for (int j = 0; j < C; ++j) {
+        c.grp_tile0[(size_t)j] = (int32_t)t;
+        c.grp_ntiles[(size_t)j] = (int32_t)((cnt[(size_t)j] + 255) / 256);
+        t += c.grp_ntiles[(size_t)j];
+        maxt = std::max(maxt, (int)c.grp_ntiles[(size_t)j]);
+    }
+    c.grp_rows = t * 256;
+    std::vector<int32_t> sorted((size_t)std::max<int64_t>(c.grp_rows, 1), -1);
+    std::vector<int64_t> pos((size_t)C);
+    for (int j = 0; j < C; ++j) pos[(size_t)j] = (int64_t)c.grp_tile0[(size_t)j] * 256;
+    for (int64_t i = 0; i < S; ++i)
+        if (valid[(size_t)i] && rl[(size_t)i] >= 0 && rl[(size_t)i] < C)
+            sorted[(size_t)pos[(size_t)rl[(size_t)i]]++] = (int32_t)i;
+    // chunking: tpc tiles per work item, <= kMaxSlices / nprobe chunks per list
+    const int np = std::max(1, std::min(c.ivf_nprobe, C));
+    // 16+ tiles per item amortise the per-item pipeline ramp (A load, TMA / MMA fill, drain)
+    c.grp_tpc = std::max(16, (maxt * np + kMaxSlices - 1) / kMaxSlices);
+    c.grp_ch = std::max(1, (maxt + c.grp_tpc - 1) / c.grp_tpc);
+    if (c.grp_rows > c.grp_cap_rows) {
+        cudaFree(c.d_sorted_slot);
+        cudaFree(c.d_rows_sorted);
+        cudaFree(c.d_sorted_vbits);
+        c.grp_cap_rows = c.grp_rows + 64 * 256;
+        SW_CUDA(cudaMalloc(&c.d_sorted_slot, sizeof(int32_t) * c.grp_cap_rows));
+        SW_CUDA(cudaMalloc(&c.d_rows_sorted, sizeof(__nv_bfloat16) * c.grp_cap_rows * c.Dp));
+        SW_CUDA(cudaMalloc(&c.d_sorted_vbits, sizeof(uint32_t) * (c.grp_cap_rows / 32 + 16)));
+        SW_REQUIRE(encode_2d_map(&c.tm_sorted, c.d_rows_sorted, (uint64_t)c.Dp,
+                                 (uint64_t)c.grp_cap_rows, 256),
+                   "grouped IVF: tensor map encode failed");
+    }
+    if (!c.d_list_tile0) {
+        SW_CUDA(cudaMalloc(&c.d_list_tile0, sizeof(int32_t) * kMaxCentroids));
+        SW_CUDA(cudaMalloc(&c.d_list_ntiles, sizeof(int32_t) * kMaxCentroids));
+        SW_CUDA(cudaMalloc(&c.d_qcnt, sizeof(int32_t) * kMaxCentroids));
+        SW_CUDA(cudaMalloc(&c.d_qbase, sizeof(int32_t) * (kMaxCentroids + 1)));
+        SW_CUDA(cudaMalloc(&c.d_qlist, sizeof(int32_t) * (size_t)kMaxCentroids * c.Bmax));
+    }
+    std::vector<uint32_t> vb((size_t)(c.grp_cap_rows / 32 + 16), 0u);
+    for (int64_t r = 0; r < c.grp_rows; ++r)
+        if (sorted[(size_t)r] >= 0) vb[(size_t)(r >> 5)] |= 1u << (r & 31);
+    if (c.grp_rows > 0)
+        SW_CUDA(cudaMemcpy(c.d_sorted_slot, sorted.data(), sizeof(int32_t) * c.grp_rows,
+                           cudaMemcpyHostToDevice));
+    SW_CUDA(cudaMemcpy(c.d_sorted_vbits, vb.data(), sizeof(uint32_t) * vb.size(),
+                       cudaMemcpyHostToDevice));
+    std::vector<int32_t> t0v(kMaxCentroids, 0), ntv(kMaxCentroids, 0);
+    std::copy(c.grp_tile0.begin(), c.grp_tile0.end(), t0v.begin());
+    std::copy(c.grp_ntiles.begin(), c.grp_ntiles.end(), ntv.begin());
+    SW_CUDA(cudaMemcpy(c.d_list_tile0, t0v.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice));
+    SW_CUDA(cudaMemcpy(c.d_list_ntiles, ntv.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice));
+    if (c.grp_rows > 0) {
+        k_sort_rows<<<(unsigned)((c.grp_rows + 7) / 8), 256, 0, c.mstream>>>(
+            c.d_sorted_slot, c.grp_rows, c.rows_bf, c.Dp, c.d_rows_sorted);
+        SW_CUDA(cudaGetLastError());
+    }
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+    c.grp_C = C;
+    c.grp_max_chunks = c.grp_ch;
+    c.grp_dirty = false;
+}
+
+int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st) {
+    static const bool enabled = [] {
+        const char* e = getenv("SW_IVF_GROUPED");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled || !c.ivf || c.ivf_C == 0 || c.Rp != 1 || !c.tc_ok) return 0;
+    const int np = std::min(c.ivf_nprobe, c.ivf_C);
+    if (np >= c.ivf_C) return 0;
+    if (c.grp_dirty || c.grp_C != c.ivf_C) build_sorted(c);
+    if (c.grp_rows == 0) return 0;
+    const int64_t blocks = ((int64_t)B * np + 127) / 128 + c.ivf_C;
+    const int64_t max_items = blocks * c.grp_ch;
+    if (np * c.grp_ch > kMaxSlices) return 0;
+    if (blocks * 128 > c.qg_cap) {
+        cudaFree(c.d_qg);
+        cudaFree(c.d_qmap);
+        c.qg_cap = blocks * 128;
+        SW_CUDA(cudaMalloc(&c.d_qg, sizeof(__nv_bfloat16) * c.qg_cap * c.Dp));
+        SW_CUDA(cudaMalloc(&c.d_qmap, sizeof(int32_t) * c.qg_cap));
+        SW_REQUIRE(encode_2d_map(&c.tm_qg, c.d_qg, (uint64_t)c.Dp, (uint64_t)c.qg_cap, 128),
+                   "grouped IVF: tensor map encode failed");
+    }
+    if (max_items > c.items_cap) {
+        cudaFree(c.d_items);
+        c.items_cap = max_items;
+        SW_CUDA(cudaMalloc(&c.d_items, sizeof(int4) * c.items_cap));
+    }
+    SW_CUDA(cudaMemsetAsync(c.d_qcnt, 0, sizeof(int32_t) * kMaxCentroids, st));
+    SW_CUDA(cudaMemsetAsync(c.d_items, 0, sizeof(int4) * max_items, st));
+    k_group_count<<<B, kMaxCentroids, 0, st>>>(c.prank, c.ivf_C, np, c.d_qcnt, c.d_qlist, c.Bmax);
+    k_group_plan<<<1, kMaxCentroids, 0, st>>>(c.d_qcnt, c.ivf_C, c.d_list_tile0, c.d_list_ntiles,
+                                              c.grp_tpc, c.d_qbase, c.d_items);
+    k_group_gather<<<(unsigned)((blocks * 128 + 7) / 8), 256, 0, st>>>(
+        c.d_qcnt, c.d_qlist, c.d_qbase, c.ivf_C, c.Bmax, c.q_bf, c.Dp, c.d_qg, c.d_qmap,
+        blocks * 128);
+    const int n_chunks = np * c.grp_ch;
+    k_fill_slices<<<(unsigned)(((int64_t)B * n_chunks + 255) / 256), 256, 0, st>>>(
+        B, n_chunks, kMaxTopK, c.slice_cnt, c.cta_topk);
+    SW_CUDA(cudaGetLastError());
+    return max_items;
+}
+
 // Search-time probe ranking; returns true when lists restrict the search (nprobe < C).
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st) {
     if (!c.ivf) return false;
@@ -553,8 +826,28 @@ bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st) {
     }
     const int np = std::min(c.ivf_nprobe, c.ivf_C);
     if (np >= c.ivf_C) return false;  // every list probed == exhaustive
-    k_probe_rank<<<B, kMaxCentroids, 0, st>>>(d_q, c.D, c.cent, c.Df, c.ivf_C, np, c.prank,
-                                              c.pmask);
+    const int cp = c.ivf_C <= 32 ? 32 : c.ivf_C <= 64 ? 64 : c.ivf_C <= 128 ? 128 : 256;
+    const size_t smem = sizeof(float) * (size_t)c.D * cp + sizeof(double) * 256;
+    if (smem <= 200 * 1024) {
+        auto launch = [&](auto kern) {
+            static bool attr = false;
+            if (!attr) {
+                SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024));
+                attr = true;
+            }
+            const int grid = (int)std::min<int64_t>(148, (B + 256 / cp - 1) / (256 / cp));
+            kern<<<grid, 256, smem, st>>>(d_q, B, c.D, c.cent, c.Df, c.ivf_C, np, c.prank,
+                                          c.pmask);
+        };
+        if (cp == 32) launch(k_probe_rank_smem<32>);
+        else if (cp == 64) launch(k_probe_rank_smem<64>);
+        else if (cp == 128) launch(k_probe_rank_smem<128>);
+        else launch(k_probe_rank_smem<256>);
+    } else {
+        k_probe_rank<<<B, kMaxCentroids, 0, st>>>(d_q, c.D, c.cent, c.Df, c.ivf_C, np, c.prank,
+                                                  c.pmask);
+    }
     SW_CUDA(cudaGetLastError());
     return true;
 }

@@ -19,6 +19,8 @@
 // entry score. Every CTA's running k-th best is a lower bound of T_a, and CTAs share it through
 // an atomicMax per query, so the emission threshold tightens as the scan proceeds. The exact
 // fp64 rescoring (exact.cu) then decides ties and order bit-exactly.
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "sw_internal.cuh"
 
@@ -68,6 +70,14 @@ struct TcParams {
     int n_chunks;
     int cap_local;
     const __nv_bfloat16* q_bf;    // [BmaxPad][Dp] queries (TS mode loads them into TMEM)
+    // grouped IVF mode (single CTAs): one work item per CTA — a block of 128 queries that all
+    // probe list l, gathered into contiguous rows, against a chunk of list l's tiles in the
+    // list-sorted arena copy. items[b] = {gathered row base, tile0, n_tiles (0: idle), l | j<<8}.
+    const int4* items;
+    const int32_t* qmap;          // gathered row -> query id (-1: padding)
+    const int32_t* sorted_slot;   // list-sorted row -> arena slot (-1: padding)
+    const uint8_t* prank;         // [B][kMaxCentroids] probe rank of each list
+    int grp_ch;                   // slice of (query, list l, chunk j) = rank(l) * grp_ch + j
     int ivf;                      // IVF mode: only rows of the query's probed lists count
     const int16_t* row_list;      // [rows] list of every stored row
     const uint64_t* pmask;        // [B][4] probed-list bitmask per query
@@ -104,7 +114,8 @@ __device__ __forceinline__ void emit_chunk(const uint32_t (&r)[32], uint32_t mas
         const float m = fminf(1.0f, fmaxf(-1.0f, t[0]));
         if (m < theta) continue;  // theta may have risen within this chunk
         if (cnt < p.cap_local) {
-            p.cand_slot[slice + cnt] = (int32_t)(slot_c + e);
+            p.cand_slot[slice + cnt] =
+                p.sorted_slot ? p.sorted_slot[slot_c + e] : (int32_t)(slot_c + e);
             p.cand_score[slice + cnt] = m;
         }
         ++cnt;
@@ -154,8 +165,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int qblock = blockIdx.x;
-    const int64_t t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
-    const int64_t t1 = min(p.n_tiles, t0 + p.tiles_per_cta);
+    int qrow = qblock * BM;  // first query row of this CTA in the (gathered) query matrix
+    int64_t t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
+    int64_t t1 = min(p.n_tiles, t0 + p.tiles_per_cta);
+    int g_list = 0, g_chunk = 0;
+    if (p.items) {
+        const int4 it = p.items[blockIdx.x];
+        qrow = it.x;
+        t0 = it.y;
+        t1 = t0 + it.z;
+        g_list = it.w & 255;
+        g_chunk = it.w >> 8;
+    }
     if (t0 >= t1) return;  // uniform for the whole CTA (and for both CTAs of a pair)
     const int ntiles = (int)(t1 - t0);
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
@@ -205,12 +226,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (leader) ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(2 * p.kch * A_CHUNK));
                 for (int kc = 0; kc < p.kch; ++kc)
                     ptx::tma_load_2d_pair(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL),
-                                          kc * 64, qblock * BM);
+                                          kc * 64, qrow);
             } else {
                 ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
                 for (int kc = 0; kc < p.kch; ++kc)
                     ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
-                                     qblock * BM);
+                                     qrow);
             }
             int s = 0;  // ring stage and its phase, advanced incrementally (no division)
             uint32_t ph = 0;
@@ -306,9 +327,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int SPT = TBN / RP;       // slots per tile
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
-        const int vchunk = blockIdx.y * EPI_GROUPS + grp;
-        const int q = qblock * BM + quarter * 32 + lane;
-        const bool qvalid = q < p.B;
+        const int q = p.qmap ? p.qmap[qrow + quarter * 32 + lane] : qrow + quarter * 32 + lane;
+        const bool qvalid = q >= 0 && q < p.B;
+        int vchunk = blockIdx.y * EPI_GROUPS + grp;
+        if (p.items)  // grouped IVF: slice = (probe rank of this list for q, chunk of the list)
+            vchunk = qvalid ? (int)p.prank[(int64_t)q * kMaxCentroids + g_list] * p.grp_ch + g_chunk
+                            : 0;
         float eps2 = 0.0f;
         if (qvalid) eps2 = 2.0f * p.q_eps[q];
         uint64_t pm0 = 0, pm1 = 0, pm2 = 0, pm3 = 0;  // probed lists (IVF mode)
@@ -333,7 +357,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // this warp's 32 query rows -> TMEM lanes [32 quarter, +32), columns [2 TBN, 2 TBN +
             // Dp / 2): lane = query, column = bf16 pair (k, k+1) of the row, K-major
             const uint4* qrow = reinterpret_cast<const uint4*>(
-                p.q_bf + (int64_t)(qblock * BM + quarter * 32 + lane) * (p.kch * 64));
+                p.q_bf + (int64_t)(qrow + quarter * 32 + lane) * (p.kch * 64));
             for (int cb = 0; cb < p.kch * 32; cb += 32) {
                 uint32_t v[32];
 #pragma unroll
@@ -627,6 +651,66 @@ void launch_tc(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t s
 }
 
 }  // namespace
+
+bool encode_2d_map(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+    return encode_2d(m, base, inner, rows, box_rows);
+}
+
+// Grouped IVF search (ivf_group_prepare built c.d_items / d_qg / the sorted arena): one single
+// CTA per work item, max_items CTAs (idle items exit at once).
+int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_t st) {
+    TcParams p{};
+    p.B = B;
+    p.kch = c.Dp / 64;
+    const int budget = c.smem_optin - 1024 - 512;
+    p.k = k;
+    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_STAGE);
+    SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
+    p.n_tiles = c.grp_rows / BN;
+    p.tiles_per_cta = 1;
+    p.n_slots = c.grp_rows;
+    p.valid_bits = c.d_sorted_vbits;
+    p.q_eps = c.q_eps;
+    p.thr = c.thr;
+    p.top1 = c.top1;
+    p.q_bf = c.d_qg;
+    p.ivf = 0;  // every row of a work item belongs to the list its queries probe
+    p.row_list = c.row_list;
+    p.pmask = c.pmask;
+    p.slice_cnt = c.slice_cnt;
+    p.cta_topk = c.cta_topk;
+    p.cand_slot = c.cand_slot;
+    p.cand_score = c.cand_score;
+    p.items = c.d_items;
+    p.qmap = c.d_qmap;
+    p.sorted_slot = c.d_sorted_slot;
+    p.prank = c.prank;
+    p.grp_ch = c.grp_ch;
+    p.n_chunks = std::min(c.ivf_nprobe, c.ivf_C) * c.grp_ch;
+    SW_REQUIRE(p.n_chunks <= kMaxSlices, "grouped IVF: too many slices per query");
+    p.cap_local = (kCandCap / p.n_chunks) & ~3;
+    c.last_chunks = p.n_chunks;
+    c.last_score_pair = false;
+    c.last_score_ts = false;
+    p.experiment = 0;
+    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 512;
+    static bool attr_set = false;
+    auto kern = [&](auto rp_tag, auto kl_tag) {
+        constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
+        auto kf = k_score_tc<RPv, KLv, false, false>;
+        SW_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     c.smem_optin));
+        kf<<<dim3((unsigned)max_items, 1), THREADS, smem, st>>>(c.tm_qg, c.tm_sorted, p);
+    };
+    (void)attr_set;
+    SW_REQUIRE(c.Rp == 1, "grouped IVF search needs one row per entry");
+    if (k <= 8)
+        kern(std::integral_constant<int, 1>{}, std::integral_constant<int, 8>{});
+    else
+        kern(std::integral_constant<int, 1>{}, std::integral_constant<int, 32>{});
+    SW_CUDA(cudaGetLastError());
+    return 1;
+}
 
 bool encode_tensor_maps(Ctx& c) {
     if (c.Dp > 512) return false;

@@ -174,6 +174,27 @@ struct Ctx {
     uint8_t* prank = nullptr;         // [Bmax][kMaxCentroids] probe rank per list, 255 = not probed
     uint64_t* pmask = nullptr;        // [Bmax][4] probed-list bitmask (read by the tcgen05 epilogue)
     std::vector<int32_t> ivf_rows;    // [S] rows of each slot the index has seen (insert order)
+    // grouped IVF search (one row per entry): a list-sorted, tile-aligned bf16 copy of the arena
+    // (rebuilt lazily after index changes) and per-batch query groups per probed list
+    bool grp_dirty = true;
+    int64_t grp_rows = 0, grp_cap_rows = 0;
+    int grp_C = 0, grp_tpc = 8, grp_ch = 1, grp_max_chunks = 0;
+    std::vector<int32_t> grp_tile0, grp_ntiles;
+    int32_t* d_sorted_slot = nullptr;        // [grp_cap_rows] arena slot of each sorted row
+    __nv_bfloat16* d_rows_sorted = nullptr;  // [grp_cap_rows][Dp]
+    uint32_t* d_sorted_vbits = nullptr;      // [grp_cap_rows / 32 + 16]
+    int32_t* d_list_tile0 = nullptr;         // [kMaxCentroids]
+    int32_t* d_list_ntiles = nullptr;        // [kMaxCentroids]
+    int32_t* d_qcnt = nullptr;               // [kMaxCentroids] queries probing each list
+    int32_t* d_qlist = nullptr;              // [kMaxCentroids][Bmax]
+    int32_t* d_qbase = nullptr;              // [kMaxCentroids + 1] first gathered block per list
+    __nv_bfloat16* d_qg = nullptr;           // [qg_cap][Dp] gathered query rows
+    int32_t* d_qmap = nullptr;               // [qg_cap] query id of each gathered row
+    int64_t qg_cap = 0;
+    int4* d_items = nullptr;                 // [items_cap]
+    int64_t items_cap = 0;
+    CUtensorMap tm_sorted{};
+    CUtensorMap tm_qg{};
 
     // host bookkeeping (mirrors the reference's entry_vector_counts_, index.hpp:92)
     std::unordered_map<uint64_t, int64_t> slot_of;
@@ -282,6 +303,10 @@ void ivf_on_remove(Ctx& c, int64_t slot);
 void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector<int32_t>& nr);
 void ivf_set_centroids(Ctx& c, const float* h, int C);
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
+// grouped IVF search: returns the upper bound of work items (0 = grouped path not applicable)
+int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st);
+bool encode_2d_map(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32_t box_rows);
+int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_t st);
 // phase-vocoder time stretch (vocoder.cu)
 int time_stretch_batch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int B,
                        int rate, const double* target_s, int n, int hop_a, float* d_out,
