@@ -322,6 +322,7 @@ __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
             b += y;
         }
         qbase[kMaxCentroids] = a;
+        qbase[kMaxCentroids + 1] = b;  // work items (persistent scoring CTAs walk them)
     }
     __syncthreads();
     if (j < kMaxCentroids) qbase[j] = s_nb[j];
@@ -747,7 +748,7 @@ static void build_sorted(Ctx& c) {
         SW_CUDA(cudaMalloc(&c.d_list_tile0, sizeof(int32_t) * kMaxCentroids));
         SW_CUDA(cudaMalloc(&c.d_list_ntiles, sizeof(int32_t) * kMaxCentroids));
         SW_CUDA(cudaMalloc(&c.d_qcnt, sizeof(int32_t) * kMaxCentroids));
-        SW_CUDA(cudaMalloc(&c.d_qbase, sizeof(int32_t) * (kMaxCentroids + 1)));
+        SW_CUDA(cudaMalloc(&c.d_qbase, sizeof(int32_t) * (kMaxCentroids + 2)));
         SW_CUDA(cudaMalloc(&c.d_qlist, sizeof(int32_t) * (size_t)kMaxCentroids * c.Bmax));
     }
     std::vector<uint32_t> vb((size_t)(c.grp_cap_rows / 32 + 16), 0u);

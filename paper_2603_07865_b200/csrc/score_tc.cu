@@ -78,6 +78,7 @@ struct TcParams {
     const int32_t* sorted_slot;   // list-sorted row -> arena slot (-1: padding)
     const uint8_t* prank;         // [B][kMaxCentroids] probe rank of each list
     int grp_ch;                   // slice of (query, list l, chunk j) = rank(l) * grp_ch + j
+    const int32_t* n_items;       // grouped: device count of real items (persistent CTAs loop)
     int ivf;                      // IVF mode: only rows of the query's probed lists count
     const int16_t* row_list;      // [rows] list of every stored row
     const uint64_t* pmask;        // [B][4] probed-list bitmask per query
@@ -157,28 +158,44 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* sB = smem + (TS ? 0 : p.kch * A_CHUNK);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * BSTG);
     const int S = p.n_stages;
-    // full[S] | empty[S] | a_full | tfull[2] | tempty[2]
+    // full[S] | empty[S] | a_full | tfull[2] | tempty[2] | a_empty
     auto bar = [&](int i) { return ptx::smem_u32(&bars[i]); };
-    const int FULL = 0, EMPTY = S, AFULL = 2 * S, TFULL = 2 * S + 1, TEMPTY = 2 * S + 3;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 5]);
+    const int FULL = 0, EMPTY = S, AFULL = 2 * S, TFULL = 2 * S + 1, TEMPTY = 2 * S + 3,
+              AEMPTY = 2 * S + 5;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 6]);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int qblock = blockIdx.x;
-    int qrow = qblock * BM;  // first query row of this CTA in the (gathered) query matrix
-    int64_t t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
-    int64_t t1 = min(p.n_tiles, t0 + p.tiles_per_cta);
-    int g_list = 0, g_chunk = 0;
-    if (p.items) {
-        const int4 it = p.items[blockIdx.x];
-        qrow = it.x;
-        t0 = it.y;
-        t1 = t0 + it.z;
-        g_list = it.w & 255;
-        g_chunk = it.w >> 8;
-    }
-    if (t0 >= t1) return;  // uniform for the whole CTA (and for both CTAs of a pair)
-    const int ntiles = (int)(t1 - t0);
+    // Work items. Normal mode: ONE item per CTA — query block blockIdx.x x tile range
+    // blockIdx.y. Grouped IVF mode: persistent CTAs walk items blockIdx.x, + gridDim.x, ...
+    // (list, 128-query block, tile chunk); TMEM, barriers and the smem ring persist across
+    // items, and the queries of item i+1 load as soon as the MMAs of item i are done with A.
+    struct Item {
+        int qrow, ntiles, list, chunk;
+        int64_t t0;
+    };
+    auto item_at = [&](int i) {
+        Item r;
+        if (p.items) {
+            const int4 it = p.items[i];
+            r.qrow = it.x;
+            r.t0 = it.y;
+            r.ntiles = it.z;
+            r.list = it.w & 255;
+            r.chunk = it.w >> 8;
+        } else {
+            r.qrow = qblock * BM;
+            r.t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
+            r.ntiles = (int)max((int64_t)0, min(p.n_tiles, r.t0 + p.tiles_per_cta) - r.t0);
+            r.list = r.chunk = 0;
+        }
+        return r;
+    };
+    const int n_items = p.items ? *p.n_items : 1;
+    const int item0 = p.items ? (int)blockIdx.x : 0;
+    const int istep = p.items ? (int)gridDim.x : 1;
+    if (item0 >= n_items || item_at(item0).ntiles == 0) return;  // uniform for the CTA / pair
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
 
@@ -188,6 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(bar(EMPTY + i), 1);
         }
         ptx::mbar_init(bar(AFULL), TS ? 8 : 1);  // TS: every epilogue warp of both CTAs
+        ptx::mbar_init(bar(AEMPTY), 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar(TFULL + i), 1);
             ptx::mbar_init(bar(TEMPTY + i), PAIR ? 8 : 4);  // one group of 4 warps per acc
@@ -218,43 +236,51 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer
-            if (TS) {
-                // queries go to TMEM through the epilogue warps
-            } else if (PAIR) {
-                // both CTAs load their own queries / their half of each tile; the bytes
-                // complete on the leader's barriers, whose expectation covers both halves
-                if (leader) ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(2 * p.kch * A_CHUNK));
-                for (int kc = 0; kc < p.kch; ++kc)
-                    ptx::tma_load_2d_pair(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL),
-                                          kc * 64, qrow);
-            } else {
-                ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
-                for (int kc = 0; kc < p.kch; ++kc)
-                    ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
-                                     qrow);
-            }
             int s = 0;  // ring stage and its phase, advanced incrementally (no division)
             uint32_t ph = 0;
-            for (int lt = 0; lt < ntiles; ++lt) {
-                const int64_t tile = t0 + lt;
-                for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
-                         ph ^= (s == 0) ? 1u : 0u) {
-                    ptx::mbar_wait_sleep(bar(EMPTY + s), ph ^ 1u);
-                    if (p.experiment == 2) {
-                        if (leader) ptx::mbar_arrive(bar(FULL + s));
-                        continue;
-                    }
-                    if (PAIR) {
-                        if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)(2 * BSTG));
-#pragma unroll
-                        for (int u = 0; u < KPS; ++u)
-                            ptx::tma_load_2d_pair(
-                                ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
-                                (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
-                    } else {
-                        ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
-                        ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
-                                         kc * 64, (int32_t)(tile * BN));
+            int itn = 0;
+            for (int ii = item0; ii < n_items; ii += istep, ++itn) {
+                const Item itm = item_at(ii);
+                const int qrow = itm.qrow;
+                const int64_t t0 = itm.t0;
+                const int ntiles = itm.ntiles;
+                if (itn > 0) ptx::mbar_wait_sleep(bar(AEMPTY), (uint32_t)((itn - 1) & 1));
+                if (TS) {
+                    // queries go to TMEM through the epilogue warps
+                } else if (PAIR) {
+                    // both CTAs load their own queries / their half of each tile; the bytes
+                    // complete on the leader's barriers, whose expectation covers both halves
+                    if (leader) ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(2 * p.kch * A_CHUNK));
+                    for (int kc = 0; kc < p.kch; ++kc)
+                        ptx::tma_load_2d_pair(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL),
+                                              kc * 64, qrow);
+                } else {
+                    ptx::mbar_arrive_expect_tx(bar(AFULL), (uint32_t)(p.kch * A_CHUNK));
+                    for (int kc = 0; kc < p.kch; ++kc)
+                        ptx::tma_load_2d(ptx::smem_u32(sA + kc * A_CHUNK), &tmQ, bar(AFULL), kc * 64,
+                                         qrow);
+                }
+                for (int lt = 0; lt < ntiles; ++lt) {
+                    const int64_t tile = t0 + lt;
+                    for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
+                             ph ^= (s == 0) ? 1u : 0u) {
+                        ptx::mbar_wait_sleep(bar(EMPTY + s), ph ^ 1u);
+                        if (p.experiment == 2) {
+                            if (leader) ptx::mbar_arrive(bar(FULL + s));
+                            continue;
+                        }
+                        if (PAIR) {
+                            if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)(2 * BSTG));
+    #pragma unroll
+                            for (int u = 0; u < KPS; ++u)
+                                ptx::tma_load_2d_pair(
+                                    ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
+                                    (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
+                        } else {
+                            ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
+                            ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
+                                             kc * 64, (int32_t)(tile * BN));
+                        }
                     }
                 }
             }
@@ -265,58 +291,67 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---------------- MMA issuer: the converged warp waits, one elected lane issues
             // for the whole CTA / pair. Descriptors advance by constants (K16 step = 32 B =
             // 2 in the >>4 address field), keeping the per-chunk issue path short.
-            if (TS)
-                ptx::mbar_wait_cluster(bar(AFULL), 0);
-            else
-                ptx::mbar_wait(bar(AFULL), 0);
-            ptx::tc_fence_after();
             const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sA));
             const uint64_t bdesc0 = ptx::umma_desc_sw128(ptx::smem_u32(sB));
             int s = 0;
             uint32_t ph = 0;
-            for (int lt = 0; lt < ntiles; ++lt) {
-                const int acc = lt & 1;
-                const uint32_t aph = (lt >> 1) & 1u;
-                ptx::mbar_wait_sleep(bar(TEMPTY + acc), aph ^ 1u);
+            int gt = 0;  // tiles across items: accumulator index and phase
+            int itn = 0;
+            for (int ii = item0; ii < n_items; ii += istep, ++itn) {
+                const int ntiles = item_at(ii).ntiles;
+                if (TS)
+                    ptx::mbar_wait_cluster(bar(AFULL), (uint32_t)(itn & 1));
+                else
+                    ptx::mbar_wait(bar(AFULL), (uint32_t)(itn & 1));
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * TBN;
-                for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
-                         ph ^= (s == 0) ? 1u : 0u) {
-                    ptx::mbar_wait_sleep(bar(FULL + s), ph);
+                for (int lt = 0; lt < ntiles; ++lt, ++gt) {
+                    const int acc = gt & 1;
+                    const uint32_t aph = (gt >> 1) & 1u;
+                    ptx::mbar_wait_sleep(bar(TEMPTY + acc), aph ^ 1u);
                     ptx::tc_fence_after();
-                    const uint64_t ad = adesc0 + (uint64_t)(kc * (A_CHUNK >> 4));
-                    const uint64_t bd = bdesc0 + (uint64_t)(s * (BSTG >> 4));
-                    if (ptx::elect_one()) {
-#pragma unroll
-                        for (int u = 0; u < KPS; ++u)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t acc_in = ((kc + u) | k) != 0 ? 1u : 0u;
-                            const uint64_t bk = bd + (uint64_t)(u * ((BSTG / KPS) >> 4)) + 2 * k;
-                            if (TS)
-                                ptx::mma_bf16_pair_ts(
-                                    d_tmem, tmem_base + 2 * TBN + (kc + u) * 32 + k * 8, bk,
-                                    IDESC_TS, acc_in);
-                            else if (PAIR)
-                                ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bk, IDESC_PAIR, acc_in);
+                    const uint32_t d_tmem = tmem_base + acc * TBN;
+                    for (int kc = 0; kc < p.kch; kc += KPS, s = (s + 1 == S) ? 0 : s + 1,
+                             ph ^= (s == 0) ? 1u : 0u) {
+                        ptx::mbar_wait_sleep(bar(FULL + s), ph);
+                        ptx::tc_fence_after();
+                        const uint64_t ad = adesc0 + (uint64_t)(kc * (A_CHUNK >> 4));
+                        const uint64_t bd = bdesc0 + (uint64_t)(s * (BSTG >> 4));
+                        if (ptx::elect_one()) {
+    #pragma unroll
+                            for (int u = 0; u < KPS; ++u)
+    #pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint32_t acc_in = ((kc + u) | k) != 0 ? 1u : 0u;
+                                const uint64_t bk = bd + (uint64_t)(u * ((BSTG / KPS) >> 4)) + 2 * k;
+                                if (TS)
+                                    ptx::mma_bf16_pair_ts(
+                                        d_tmem, tmem_base + 2 * TBN + (kc + u) * 32 + k * 8, bk,
+                                        IDESC_TS, acc_in);
+                                else if (PAIR)
+                                    ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bk, IDESC_PAIR, acc_in);
+                                else
+                                    ptx::mma_bf16(d_tmem, ad + 2 * k, bk, IDESC, acc_in);
+                            }
+                            // frees the smem stage (both CTAs' halves) when the MMAs finish
+                            if (PAIR)
+                                ptx::mma_commit_pair(bar(EMPTY + s));
                             else
-                                ptx::mma_bf16(d_tmem, ad + 2 * k, bk, IDESC, acc_in);
+                                ptx::mma_commit(bar(EMPTY + s));
                         }
-                        // frees the smem stage (both CTAs' halves) when the MMAs finish
+                        __syncwarp();
+                    }
+                    // accumulator ready for the epilogue (of both CTAs)
+                    if (ptx::elect_one()) {
                         if (PAIR)
-                            ptx::mma_commit_pair(bar(EMPTY + s));
+                            ptx::mma_commit_pair(bar(TFULL + acc));
                         else
-                            ptx::mma_commit(bar(EMPTY + s));
+                            ptx::mma_commit(bar(TFULL + acc));
                     }
                     __syncwarp();
                 }
-                // accumulator ready for the epilogue (of both CTAs)
-                if (ptx::elect_one()) {
-                    if (PAIR)
-                        ptx::mma_commit_pair(bar(TFULL + acc));
-                    else
-                        ptx::mma_commit(bar(TFULL + acc));
-                }
+                // the item's MMAs are issued: A may be overwritten once they complete
+                // (multi-item CTAs are single-CTA grouped IVF only)
+                if (p.items && ptx::elect_one()) ptx::mma_commit(bar(AEMPTY));
                 __syncwarp();
             }
         }
@@ -327,6 +362,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int SPT = TBN / RP;       // slots per tile
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
+        int gt = 0;  // tiles across items (accumulator index / phase, as the MMA counts them)
+        for (int ii = item0; ii < n_items; ii += istep) {
+        const Item itm = item_at(ii);
+        const int qrow = itm.qrow;
+        const int64_t t0 = itm.t0;
+        const int ntiles = itm.ntiles;
+        const int g_list = itm.list, g_chunk = itm.chunk;
         const int q = p.qmap ? p.qmap[qrow + quarter * 32 + lane] : qrow + quarter * 32 + lane;
         const bool qvalid = q >= 0 && q < p.B;
         int vchunk = blockIdx.y * EPI_GROUPS + grp;
@@ -377,8 +419,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
 
         for (int lt = grp; lt < ntiles; lt += EPI_GROUPS) {
-            const int acc = lt & 1;
-            const uint32_t aph = (lt >> 1) & 1u;
+            const int acc = (gt + lt) & 1;
+            const uint32_t aph = ((gt + lt) >> 1) & 1u;
             const int64_t tile = t0 + lt;
             if (qvalid) {
                 theta = fmaxf(theta, ord2f(g_next) - eps2);
@@ -523,7 +565,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     pub_top1 = best;
                 }
                 float bound = kth;
-                if ((done & (done - 1)) == 0 && p.n_chunks >= p.k) {  // tiles 1, 2, 4, 8, ...
+                // refresh at tiles 1, 2, 4, 8, ... (grouped IVF items of <= 16 tiles: 2 and 8)
+                const bool refresh = p.items ? (done == 2 || done == 8) : (done & (done - 1)) == 0;
+                if (refresh && p.n_chunks >= p.k) {
                     float sel[KL];
 #pragma unroll
                     for (int i = 0; i < KL; ++i) sel[i] = (i < KL - p.k) ? INFINITY : -INFINITY;
@@ -553,6 +597,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int i = 0; i < KL; ++i)
                 if (i >= KL - p.k) tk[i - (KL - p.k)] = list[i];
+        }
+            gt += ntiles;
         }
     }
     ptx::tc_fence_before();
@@ -686,6 +732,7 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.sorted_slot = c.d_sorted_slot;
     p.prank = c.prank;
     p.grp_ch = c.grp_ch;
+    p.n_items = c.d_qbase + kMaxCentroids + 1;  // device count written by k_group_plan
     p.n_chunks = std::min(c.ivf_nprobe, c.ivf_C) * c.grp_ch;
     SW_REQUIRE(p.n_chunks <= kMaxSlices, "grouped IVF: too many slices per query");
     p.cap_local = (kCandCap / p.n_chunks) & ~3;
@@ -700,7 +747,9 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
         auto kf = k_score_tc<RPv, KLv, false, false>;
         SW_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      c.smem_optin));
-        kf<<<dim3((unsigned)max_items, 1), THREADS, smem, st>>>(c.tm_qg, c.tm_sorted, p);
+        // persistent: one CTA per SM walks the items (max_items only bounds the grid)
+        kf<<<dim3((unsigned)std::min<int64_t>(max_items, 148), 1), THREADS, smem, st>>>(
+            c.tm_qg, c.tm_sorted, p);
     };
     (void)attr_set;
     SW_REQUIRE(c.Rp == 1, "grouped IVF search needs one row per entry");
