@@ -205,6 +205,14 @@ int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t entry_id, int16_t* lists, int32_t c
  * (host): 0, or SW_EINVAL where the reference throws (empty clip, target <= 0, stretch ratio
  * outside [0.4, 2.5]). A bad window / hop fails the call with SW_EINVAL (StftConfig::validate).
  * Stream-ordered; host arrays may be reused once the call returns. */
+/* Alignment used by sw_align_noise / sw_warmstart: SW_ALIGN_CROP_TILE (default; crop or tile
+ * cyclically, the north-star definition) or SW_ALIGN_VOCODER — the reference's own alignment
+ * (slice_clip + time_stretch{window, hop}, pipeline.cpp:158-169) applied to every latent channel
+ * (c, f) at the latent frame rate, then the same forward noising. A request whose stretch ratio
+ * leaves [0.4, 2.5] (where the reference throws and serves cold) keeps an untouched output. */
+#define SW_ALIGN_CROP_TILE 0
+#define SW_ALIGN_VOCODER 1
+int sw_set_align_mode(sw_ctx* ctx, int32_t mode, int32_t window, int32_t hop);
 int sw_time_stretch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int32_t B,
                     int32_t sample_rate, const double* target_s, int32_t window, int32_t hop,
                     float* d_out, int64_t out_cap, int64_t* out_off, int32_t* out_len,

@@ -154,6 +154,7 @@ def lib() -> C.CDLL:
         "sw_ivf_entry_lists": ([vp, u64, vp, i32], C.c_int),
         "sw_swix_load": ([vp, C.c_char_p], C.c_int),
         "sw_ctx_info": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "sw_set_align_mode": ([vp, i32, i32, i32], C.c_int),
         "swb_create": ([vp, i32, i32, u64, C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy), u64,
                         i32, i32, C.POINTER(vp)], C.c_int),
         "swb_destroy": ([vp], C.c_int),
@@ -186,7 +187,7 @@ EXPORTED = [
     "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",
     "sw_ivf_rebuild", "sw_ivf_info", "sw_ivf_centroids", "sw_ivf_set_centroids",
     "sw_ivf_entry_lists", "sw_swix_load", "sw_swix_save", "sw_swem_read", "sw_time_stretch",
-    "sw_ctx_info", "swb_create", "swb_destroy", "swb_submit", "swb_stats",
+    "sw_ctx_info", "sw_set_align_mode", "swb_create", "swb_destroy", "swb_submit", "swb_stats",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

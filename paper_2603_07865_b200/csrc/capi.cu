@@ -66,7 +66,7 @@ static void free_ctx(Ctx& c) {
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
                     c.cent, c.row_list, c.prank, c.pmask, c.d_sorted_slot, c.d_rows_sorted,
                     c.d_sorted_vbits, c.d_list_tile0, c.d_list_ntiles, c.d_qcnt, c.d_qlist,
-                    c.d_qbase, c.d_qg, c.d_qmap, c.d_items};
+                    c.d_qbase, c.d_qg, c.d_qmap, c.d_items, c.d_voc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
@@ -640,6 +640,22 @@ int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t id, int16_t* lists, int32_t cap) {
 }
 
 // ---------------------------------------------------------------- phase vocoder
+int sw_set_align_mode(sw_ctx* ctx, int32_t mode, int32_t window, int32_t hop) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        SW_REQUIRE(mode == SW_ALIGN_CROP_TILE || mode == SW_ALIGN_VOCODER, "unknown align mode");
+        SW_REQUIRE(window >= 2 && (window & (window - 1)) == 0 && window <= 1024,
+                   "stft window size must be a power of two >= 2 (at most 1024 here)");
+        SW_REQUIRE(hop >= 1 && hop <= window, "stft hop must be in (0, window_size]");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        c.align_mode = mode;
+        c.voc_win = window;
+        c.voc_hop = hop;
+        return SW_OK;
+    });
+}
+
 int sw_time_stretch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int32_t B,
                     int32_t sample_rate, const double* target_s, int32_t window, int32_t hop,
                     float* d_out, int64_t out_cap, int64_t* out_off, int32_t* out_len,

@@ -174,6 +174,11 @@ struct Ctx {
     uint8_t* prank = nullptr;         // [Bmax][kMaxCentroids] probe rank per list, 255 = not probed
     uint64_t* pmask = nullptr;        // [Bmax][4] probed-list bitmask (read by the tcgen05 epilogue)
     std::vector<int32_t> ivf_rows;    // [S] rows of each slot the index has seen (insert order)
+    // alignment of the chosen latent: 0 crop / tile (default), 1 the reference's phase vocoder
+    int align_mode = 0;
+    int voc_win = 128, voc_hop = 32;  // StftConfig (pipeline.hpp:36)
+    void* d_voc = nullptr;            // per-request vocoder plans + aligned flags
+    int voc_cap = 0;
     // grouped IVF search (one row per entry): a list-sorted, tile-aligned bf16 copy of the arena
     // (rebuilt lazily after index changes) and per-batch query groups per probed list
     bool grp_dirty = true;
@@ -308,6 +313,9 @@ int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st);
 bool encode_2d_map(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32_t box_rows);
 int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_t st);
 // phase-vocoder time stretch (vocoder.cu)
+const int32_t* launch_align_vocoder(Ctx& c, const sw_choice* d_ch, const sw_request* d_req,
+                                    int B, int rank, float* d_out, int t_out_max,
+                                    cudaStream_t st);
 int time_stretch_batch(const float* d_in, const int64_t* in_off, const int32_t* in_len, int B,
                        int rate, const double* target_s, int n, int hop_a, float* d_out,
                        int64_t out_cap, int64_t* out_off, int32_t* out_len, int32_t* status,

@@ -63,22 +63,15 @@ __device__ void fft_stages(double2* a, int n, const double2* __restrict__ tw) {
 
 __device__ __forceinline__ int bitrev(int i, int logn) { return (int)(__brev((unsigned)i) >> (32 - logn)); }
 
-__global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ in, int in_stride,
-                                                     float* __restrict__ out, int out_stride,
-                                                     const ClipDesc* __restrict__ desc, int n,
-                                                     int logn, int hop_a,
-                                                     const double* __restrict__ window,
-                                                     const double2* __restrict__ tw_fwd,
-                                                     const double2* __restrict__ tw_inv,
-                                                     double* __restrict__ work) {
-    extern __shared__ double2 buf[];  // [n]
-    const ClipDesc d = desc[blockIdx.x];
-    if (d.status != 0) return;
+// One clip's time_stretch by one CTA: x[i * xs] for i < in_len -> y[i * ys] for i < ylim
+// (<= target). buf: n complex doubles; acc / wsum: natural doubles each (smem or global).
+__device__ void stretch_clip(const float* __restrict__ x, int xs, int in_len, float* __restrict__ y,
+                             int ys, int ylim, int target, int hop_s, int frames, int natural,
+                             int n, int logn, int hop_a, const double* __restrict__ window,
+                             const double2* __restrict__ tw_fwd, const double2* __restrict__ tw_inv,
+                             double2* buf, double* acc, double* wsum) {
     const int half = n / 2;
-    const float* x = in + d.in_off;
-    double* acc = work + d.work_off;
-    double* wsum = acc + d.natural;
-    for (int i = threadIdx.x; i < d.natural; i += blockDim.x) {
+    for (int i = threadIdx.x; i < natural; i += blockDim.x) {
         acc[i] = 0.0;
         wsum[i] = 0.0;
     }
@@ -87,12 +80,12 @@ __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ i
     double2 ob[NB];
 #pragma unroll
     for (int u = 0; u < NB; ++u) prev_phase[u] = synth_phase[u] = 0.0;
-    for (int m = 0; m < d.frames; ++m) {
+    for (int m = 0; m < frames; ++m) {
         __syncthreads();
         // stft frame m (vocoder.cpp:80-88): window[i] * padded[m hop_a + i], zero past the clip
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const int s = m * hop_a + i;
-            const float v = s < d.in_len ? x[(int64_t)s * in_stride] : 0.0f;
+            const float v = s < in_len ? x[(int64_t)s * xs] : 0.0f;
             buf[bitrev(i, logn)] = make_double2(__dmul_rn(__ldg(&window[i]), (double)v), 0.0);
         }
         __syncthreads();
@@ -117,7 +110,7 @@ __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ i
                 const double dev = wrap_phase(__dsub_rn(__dsub_rn(cur, prev_phase[u]), expected));
                 const double inst = __dadd_rn(omega, __ddiv_rn(dev, (double)hop_a));
                 synth_phase[u] =
-                    wrap_phase(__dadd_rn(synth_phase[u], __dmul_rn(inst, (double)d.hop_s)));
+                    wrap_phase(__dadd_rn(synth_phase[u], __dmul_rn(inst, (double)hop_s)));
                 prev_phase[u] = cur;
                 phase = synth_phase[u];
             }
@@ -135,7 +128,7 @@ __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ i
         __syncthreads();
         fft_stages(buf, n, tw_inv);
         // istft overlap-add (vocoder.cpp:104-111): real part of x / n, frames in order
-        const int64_t off = (int64_t)m * d.hop_s;
+        const int64_t off = (int64_t)m * hop_s;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const double w = __ldg(&window[i]);
             const double re = __ddiv_rn(buf[i].x, (double)n);
@@ -144,12 +137,96 @@ __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ i
         }
     }
     __syncthreads();
-    float* y = out + d.out_off;
-    for (int i = threadIdx.x; i < d.target; i += blockDim.x) {
+    for (int i = threadIdx.x; i < ylim; i += blockDim.x) {
         float v = 0.0f;
-        if (i < d.natural && wsum[i] > 1e-9) v = (float)__ddiv_rn(acc[i], wsum[i]);
-        y[(int64_t)i * out_stride] = v;
+        if (i < natural && wsum[i] > 1e-9) v = (float)__ddiv_rn(acc[i], wsum[i]);
+        y[(int64_t)i * ys] = v;
     }
+}
+
+__global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ in, float* __restrict__ out,
+                                                     const ClipDesc* __restrict__ desc, int n,
+                                                     int logn, int hop_a,
+                                                     const double* __restrict__ window,
+                                                     const double2* __restrict__ tw_fwd,
+                                                     const double2* __restrict__ tw_inv,
+                                                     double* __restrict__ work) {
+    extern __shared__ double2 buf[];  // [n]
+    const ClipDesc d = desc[blockIdx.x];
+    if (d.status != 0) return;
+    double* acc = work + d.work_off;
+    stretch_clip(in + d.in_off, 1, d.in_len, out + d.out_off, 1, d.target, d.target, d.hop_s,
+                 d.frames, d.natural, n, logn, hop_a, window, tw_fwd, tw_inv, buf, acc,
+                 acc + d.natural);
+}
+
+// ---- the reference's alignment inside the warm-start path (sw_set_align_mode VOCODER)
+struct VocReq {
+    int64_t src;      // float offset of (slot, channel 0, frame lo, feature 0) in the latent arena
+    int32_t t_seg, target, ylim, hop_s, frames, natural, status;
+};
+
+// per request: slice_clip frames (simgen.cpp:116-119) and time_stretch's plan
+// (vocoder.cpp:139-157) of the segment clip at the latent frame rate
+__global__ void k_voc_plan(const sw_choice* __restrict__ ch, const sw_request* __restrict__ rq,
+                           int B, int rank, const int32_t* __restrict__ tsrc, int64_t Lslots,
+                           int C, int Tmax, int F, int fps, int t_out_max, int n, int hop_a,
+                           VocReq* __restrict__ vr, int32_t* __restrict__ ok) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    VocReq v{};
+    v.status = 1;
+    const sw_choice c = ch[b];
+    if (c.hit && (rank < 0 || c.owner == rank)) {
+        const int ts = tsrc[c.slot];
+        long long lo = llround(c.segment.start_s * fps);
+        long long hi = llround((c.segment.start_s + c.segment.length_s) * fps);
+        lo = min(lo, (long long)ts);
+        hi = max(min(hi, (long long)ts), lo);
+        v.t_seg = (int)(hi - lo);
+        const double L = rq[b].duration_s;
+        if (v.t_seg > 0 && L > 0.0) {
+            const double r = L / ((double)v.t_seg / fps);
+            if (r >= 0.4 && r <= 2.5) {  // else the reference throws (pipeline falls back cold)
+                v.hop_s = max(1, (int)llround(hop_a * r));
+                const long long target = llround(L * fps);
+                long long frames_l = 1;
+                if (target > n) frames_l = 1 + llround((double)(target - n) / v.hop_s);
+                const int frames = (int)max(2LL, frames_l);
+                v.target = (int)target;
+                v.ylim = min(v.target, t_out_max);
+                // frames are causal: output frames [0, ylim) only see frames m with
+                // m hop_s < ylim, so the rest (which would write past t_out_max) are skipped
+                v.frames = v.ylim > 0 ? min(frames, (v.ylim - 1) / v.hop_s + 1) : 0;
+                v.natural = v.frames > 0 ? (v.frames - 1) * v.hop_s + n : 0;
+                v.src = ((c.slot % Lslots) * C * (int64_t)Tmax + lo) * F;
+                v.status = v.frames > 0 ? 0 : 1;
+            }
+        }
+    }
+    vr[b] = v;
+    ok[b] = v.status == 0 ? 1 : 0;
+}
+
+// one CTA per (request, latent channel (c, f)): the 1-D series latent[c][lo + t][f] stretched to
+// llround(L fps) frames -> x0[b][c][t][f]; acc / wsum in dynamic smem after the FFT buffer
+__global__ void __launch_bounds__(VT) k_voc_align(const float* __restrict__ latent,
+                                                  const VocReq* __restrict__ vr, int C, int Tmax,
+                                                  int F, int t_out_max, float* __restrict__ out,
+                                                  int n, int logn, int hop_a,
+                                                  const double* __restrict__ window,
+                                                  const double2* __restrict__ tw_fwd,
+                                                  const double2* __restrict__ tw_inv) {
+    extern __shared__ double2 buf[];
+    const int b = blockIdx.y, ch = blockIdx.x;
+    const VocReq v = vr[b];
+    if (v.status != 0) return;
+    const int c = ch / F, f = ch % F;
+    double* acc = reinterpret_cast<double*>(buf + n);
+    const float* x = latent + v.src + (int64_t)c * Tmax * F + f;
+    float* y = out + ((int64_t)b * C + c) * t_out_max * F + f;
+    stretch_clip(x, F, v.t_seg, y, F, v.ylim, v.target, v.hop_s, v.frames, v.natural, n, logn,
+                 hop_a, window, tw_fwd, tw_inv, buf, acc, acc + v.natural);
 }
 
 struct Tables {
@@ -257,12 +334,52 @@ int time_stretch_batch(const float* d_in, const int64_t* in_off, const int32_t* 
     SW_CUDA(cudaMemcpyAsync(d_desc, desc.data(), sizeof(ClipDesc) * B, cudaMemcpyHostToDevice, st));
     int logn = 0;
     while ((1 << logn) < n) ++logn;
-    k_time_stretch<<<B, VT, sizeof(double2) * n, st>>>(d_in, 1, d_out, 1, d_desc, n, logn, hop_a,
+    k_time_stretch<<<B, VT, sizeof(double2) * n, st>>>(d_in, d_out, d_desc, n, logn, hop_a,
                                                       tb.window, tb.tw_fwd, tb.tw_inv, d_work);
     SW_CUDA(cudaGetLastError());
     SW_CUDA(cudaFreeAsync(d_desc, st));
     SW_CUDA(cudaFreeAsync(d_work, st));
     return 1;
+}
+
+// The reference's alignment (slice_clip + time_stretch, pipeline.cpp:158-169) of the chosen
+// latent to the requested duration, per latent channel, written as x0 into d_out; the caller
+// then applies the forward noising in place (align.cu, k_noise_inplace). Requests whose stretch
+// ratio falls outside [0.4, 2.5] (the reference throws; its pipeline serves them cold) are
+// left untouched. Returns the per-request "aligned" flags (stream-ordered device scratch).
+const int32_t* launch_align_vocoder(Ctx& c, const sw_choice* d_ch, const sw_request* d_req,
+                                    int B, int rank, float* d_out, int t_out_max,
+                                    cudaStream_t st) {
+    const int n = c.voc_win, hop_a = c.voc_hop;
+    const int fps = (int)llround(c.cfg.latent_fps);
+    SW_REQUIRE(std::fabs(c.cfg.latent_fps - fps) < 1e-12,
+               "the vocoder alignment needs an integral latent frame rate (AudioClip::sample_rate)");
+    const Tables tb = tables_for(n);
+    if (!c.d_voc || c.voc_cap < B) {
+        cudaFree(c.d_voc);
+        c.voc_cap = c.Bmax;
+        SW_CUDA(cudaMalloc(&c.d_voc, (sizeof(VocReq) + sizeof(int32_t)) * c.voc_cap));
+    }
+    VocReq* vr = reinterpret_cast<VocReq*>(c.d_voc);
+    int32_t* ok = reinterpret_cast<int32_t*>(vr + c.voc_cap);
+    k_voc_plan<<<(B + 127) / 128, 128, 0, st>>>(d_ch, d_req, B, rank, c.tsrc, c.Lslots, c.C, c.Tmax,
+                                                c.F, fps, t_out_max, n, hop_a, vr, ok);
+    int logn = 0;
+    while ((1 << logn) < n) ++logn;
+    const size_t nat_bound = (size_t)t_out_max + n + 1;  // natural <= ylim - 1 + n
+    const size_t smem = sizeof(double2) * n + 2 * sizeof(double) * nat_bound;
+    SW_REQUIRE(smem <= 200 * 1024, "vocoder alignment: stretched latent too long for smem");
+    static size_t attr = 0;
+    if (smem > attr) {
+        SW_CUDA(cudaFuncSetAttribute(k_voc_align, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        attr = smem;
+    }
+    k_voc_align<<<dim3(c.C * c.F, B), VT, smem, st>>>(c.latent, vr, c.C, c.Tmax, c.F, t_out_max,
+                                                       d_out, n, logn, hop_a, tb.window,
+                                                       tb.tw_fwd, tb.tw_inv);
+    SW_CUDA(cudaGetLastError());
+    return ok;
 }
 
 }  // namespace sw

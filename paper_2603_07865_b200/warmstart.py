@@ -206,6 +206,12 @@ class WarmStartCache:
         n = check(_lib.lib().sw_ivf_entry_lists(self._h, entry_id, ptr(out), 32), "entry_lists")
         return out[:n]
 
+    def set_align_mode(self, mode: str = "crop_tile", window: int = 128, hop: int = 32):
+        """'crop_tile' (default) or 'vocoder' — the reference's slice_clip + time_stretch
+        (pipeline.cpp:158-169) per latent channel, StftConfig{window, hop}."""
+        m = {"crop_tile": 0, "vocoder": 1}[mode]
+        check(_lib.lib().sw_set_align_mode(self._h, m, window, hop), "sw_set_align_mode")
+
     # ------------------------------------------------------------------ snapshots
     def load_swix(self, path: str):
         """IvfIndex::load (index.cpp:371-406) into this (empty) cache's device arena."""

@@ -59,3 +59,59 @@ def test_time_stretch_errors(ref):
     assert got[-1] is not None and got[-1].shape == (600,)
     with pytest.raises(ValueError):
         time_stretch([x], 200, [2.0], window=100, hop=25)  # StftConfig::validate
+
+
+def test_align_vocoder_mode_matches_reference(ref, orc):
+    """sw_align_noise in SW_ALIGN_VOCODER mode: every latent channel (c, f) of the chosen segment
+    (slice_clip frames) stretched by the reference's time_stretch at the latent frame rate, then
+    the same forward noising (eps input) as the crop/tile mode."""
+    from paper_2603_07865_b200.synth import SynthCache, perturbed_queries, request_durations
+    from paper_2603_07865_b200.warmstart import (Policy, SelectorConfig, WarmStartCache,
+                                                 requests)
+    c = SynthCache(48, 64, 0.25, seed=7)
+    wc = WarmStartCache(64, rows_per_entry=7, max_entries=48, latent_shape=(4, 256, 8),
+                        max_batch=64)
+    rng = np.random.default_rng(2)
+    lats = []
+    for e in range(48):
+        ts = int(np.floor(c.durations[e] * 25 + 0.5))
+        lat = rng.standard_normal((4, ts, 8)).astype(np.float32)
+        lats.append(lat)
+        wc.insert(int(c.ids[e]), c.entry_rows(e), c.levels[c.off[e]:c.off[e + 1]],
+                  c.starts[c.off[e]:c.off[e + 1]], c.lengths[c.off[e]:c.off[e + 1]], latent=lat)
+    wc.set_align_mode("vocoder", 128, 32)
+    B = 40
+    q = perturbed_queries(c, B, seed=9)
+    L = request_durations(B, 2.5, 10.0, seed=10)
+    ids = np.arange(500, 500 + B, dtype=np.uint64)
+    reqs = requests(ids, L, np.full(B, 200, np.int32))
+    buf = wc.plan(q, reqs, sel=SelectorConfig(8), policy=Policy("fixed", fixed_arm=6))
+    ch = wc.choices(buf)
+    assert ch["hit"].sum() > B // 2
+    eps = rng.standard_normal((B, 4, 256, 8)).astype(np.float32)
+    out = wc.align_noise(buf, reqs, 256, eps=eps).cpu().numpy()
+    abar = orc.abar_table()
+    slot_of = {int(i): e for e, i in enumerate(c.ids)}
+    n_checked = 0
+    for b in range(B):
+        if not ch["hit"][b]:
+            continue
+        lat = lats[slot_of[int(ch["entry_id"][b])]][:, :256]  # the arena keeps T_max frames
+        lo = min(int(np.floor(ch["start_s"][b] * 25 + 0.5)), lat.shape[1])
+        hi = max(min(int(np.floor((ch["start_s"][b] + ch["length_s"][b]) * 25 + 0.5)),
+                     lat.shape[1]), lo)
+        t_out = min(int(np.floor(L[b] * 25 + 0.5)), 256)
+        ab = abar[orc.abar_index(200, int(ch["steps_skipped"][b]))]
+        s0, s1 = np.float32(np.sqrt(ab)), np.float32(np.sqrt(1 - ab))
+        for cc in range(4):
+            for f in range(8):
+                y = ref.time_stretch(lat[cc, lo:hi, f], 25, float(L[b]))
+                assert y is not None  # the duration gate keeps the ratio inside [2/3, 2]
+                x0 = y[:t_out].astype(np.float64)
+                exp = (np.float64(s1) * eps[b, cc, :t_out, f] + (np.float32(s0) * y[:t_out]).astype(np.float64))
+                got = out[b, cc, :t_out, f]
+                assert np.all(np.abs(got - exp) <= 1e-5 * np.maximum(1.0, np.abs(exp))), (b, cc, f)
+                del x0
+        assert not out[b, :, t_out:].any()
+        n_checked += 1
+    assert n_checked > B // 2
