@@ -471,6 +471,20 @@ def main():
             torch.cuda.synchronize(dev)
             align_alone[mode] = a0.elapsed_time(a1) / reps
         del eps_t
+        # the reference's alignment (phase vocoder per latent channel) on the same choices
+        wc.set_align_mode("vocoder", 128, 32)
+        _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+                                     .data_ptr(), B, None, 1234, out.data_ptr(), T_, sp),
+                   "sw_align_noise")
+        a0.record(stream)
+        for _ in range(3):
+            _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+                                         .data_ptr(), B, None, 1234, out.data_ptr(), T_, sp),
+                       "sw_align_noise")
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        align_alone["vocoder_philox"] = a0.elapsed_time(a1) / 3
+        wc.set_align_mode("crop_tile")
 
     # ---- phase-vocoder time_stretch (the reference's alignment, vocoder.cpp:128-207) side
     # measurement: 1024 clips of the simulated 200 Hz 1-D latent, segment 4-12 s stretched to a

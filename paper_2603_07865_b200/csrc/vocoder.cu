@@ -24,7 +24,7 @@ namespace sw {
 
 namespace {
 
-constexpr int VT = 128;          // threads per clip
+constexpr int VT = 64;           // threads per clip (one radix-2 butterfly each at N = 128)
 constexpr int kMaxWin = 1024;
 
 struct ClipDesc {
@@ -65,6 +65,7 @@ __device__ __forceinline__ int bitrev(int i, int logn) { return (int)(__brev((un
 
 // One clip's time_stretch by one CTA: x[i * xs] for i < in_len -> y[i * ys] for i < ylim
 // (<= target). buf: n complex doubles; acc / wsum: natural doubles each (smem or global).
+template <int NB>  // bins per thread: k = threadIdx.x + VT u, u < NB (NB * VT > n / 2)
 __device__ void stretch_clip(const float* __restrict__ x, int xs, int in_len, float* __restrict__ y,
                              int ys, int ylim, int target, int hop_s, int frames, int natural,
                              int n, int logn, int hop_a, const double* __restrict__ window,
@@ -75,7 +76,6 @@ __device__ void stretch_clip(const float* __restrict__ x, int xs, int in_len, fl
         acc[i] = 0.0;
         wsum[i] = 0.0;
     }
-    constexpr int NB = kMaxWin / 2 / VT + 1;  // bins per thread: k = threadIdx.x + VT u
     double prev_phase[NB], synth_phase[NB];
     double2 ob[NB];
 #pragma unroll
@@ -114,7 +114,9 @@ __device__ void stretch_clip(const float* __restrict__ x, int xs, int in_len, fl
                 prev_phase[u] = cur;
                 phase = synth_phase[u];
             }
-            ob[u] = make_double2(__dmul_rn(mag, cos(phase)), __dmul_rn(mag, sin(phase)));  // polar
+            double sn, cs;
+            sincos(phase, &sn, &cs);  // one range reduction for both (polar)
+            ob[u] = make_double2(__dmul_rn(mag, cs), __dmul_rn(mag, sn));
         }
         __syncthreads();
         // synthesis frame, conjugate-symmetric, into bit-reversed order for the inverse FFT
@@ -144,6 +146,7 @@ __device__ void stretch_clip(const float* __restrict__ x, int xs, int in_len, fl
     }
 }
 
+template <int NB>
 __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ in, float* __restrict__ out,
                                                      const ClipDesc* __restrict__ desc, int n,
                                                      int logn, int hop_a,
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(VT) k_time_stretch(const float* __restrict__ i
     const ClipDesc d = desc[blockIdx.x];
     if (d.status != 0) return;
     double* acc = work + d.work_off;
-    stretch_clip(in + d.in_off, 1, d.in_len, out + d.out_off, 1, d.target, d.target, d.hop_s,
+    stretch_clip<NB>(in + d.in_off, 1, d.in_len, out + d.out_off, 1, d.target, d.target, d.hop_s,
                  d.frames, d.natural, n, logn, hop_a, window, tw_fwd, tw_inv, buf, acc,
                  acc + d.natural);
 }
@@ -210,6 +213,7 @@ __global__ void k_voc_plan(const sw_choice* __restrict__ ch, const sw_request* _
 
 // one CTA per (request, latent channel (c, f)): the 1-D series latent[c][lo + t][f] stretched to
 // llround(L fps) frames -> x0[b][c][t][f]; acc / wsum in dynamic smem after the FFT buffer
+template <int NB>
 __global__ void __launch_bounds__(VT) k_voc_align(const float* __restrict__ latent,
                                                   const VocReq* __restrict__ vr, int C, int Tmax,
                                                   int F, int t_out_max, float* __restrict__ out,
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(VT) k_voc_align(const float* __restrict__ late
     double* acc = reinterpret_cast<double*>(buf + n);
     const float* x = latent + v.src + (int64_t)c * Tmax * F + f;
     float* y = out + ((int64_t)b * C + c) * t_out_max * F + f;
-    stretch_clip(x, F, v.t_seg, y, F, v.ylim, v.target, v.hop_s, v.frames, v.natural, n, logn,
+    stretch_clip<NB>(x, F, v.t_seg, y, F, v.ylim, v.target, v.hop_s, v.frames, v.natural, n, logn,
                  hop_a, window, tw_fwd, tw_inv, buf, acc, acc + v.natural);
 }
 
@@ -334,8 +338,15 @@ int time_stretch_batch(const float* d_in, const int64_t* in_off, const int32_t* 
     SW_CUDA(cudaMemcpyAsync(d_desc, desc.data(), sizeof(ClipDesc) * B, cudaMemcpyHostToDevice, st));
     int logn = 0;
     while ((1 << logn) < n) ++logn;
-    k_time_stretch<<<B, VT, sizeof(double2) * n, st>>>(d_in, d_out, d_desc, n, logn, hop_a,
-                                                      tb.window, tb.tw_fwd, tb.tw_inv, d_work);
+    auto go = [&](auto kern) {
+        kern<<<B, VT, sizeof(double2) * n, st>>>(d_in, d_out, d_desc, n, logn, hop_a, tb.window,
+                                                 tb.tw_fwd, tb.tw_inv, d_work);
+    };
+    // smallest NB with NB * VT > n / 2 (bins 0..n/2): registers 64 (n <= 254) .. 158 (n = 1024)
+    if (n / 2 < 2 * VT) go(k_time_stretch<2>);
+    else if (n / 2 < 3 * VT) go(k_time_stretch<3>);
+    else if (n / 2 < 5 * VT) go(k_time_stretch<5>);
+    else go(k_time_stretch<9>);
     SW_CUDA(cudaGetLastError());
     SW_CUDA(cudaFreeAsync(d_desc, st));
     SW_CUDA(cudaFreeAsync(d_work, st));
@@ -369,15 +380,18 @@ const int32_t* launch_align_vocoder(Ctx& c, const sw_choice* d_ch, const sw_requ
     const size_t nat_bound = (size_t)t_out_max + n + 1;  // natural <= ylim - 1 + n
     const size_t smem = sizeof(double2) * n + 2 * sizeof(double) * nat_bound;
     SW_REQUIRE(smem <= 200 * 1024, "vocoder alignment: stretched latent too long for smem");
-    static size_t attr = 0;
-    if (smem > attr) {
-        SW_CUDA(cudaFuncSetAttribute(k_voc_align, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
-        attr = smem;
-    }
-    k_voc_align<<<dim3(c.C * c.F, B), VT, smem, st>>>(c.latent, vr, c.C, c.Tmax, c.F, t_out_max,
-                                                       d_out, n, logn, hop_a, tb.window,
-                                                       tb.tw_fwd, tb.tw_inv);
+    auto go = [&](auto kern) {
+        SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        kern<<<dim3(c.C * c.F, B), VT, smem, st>>>(c.latent, vr, c.C, c.Tmax, c.F, t_out_max,
+                                                    d_out, n, logn, hop_a, tb.window, tb.tw_fwd,
+                                                    tb.tw_inv);
+    };
+    // smallest NB with NB * VT > n / 2 (bins 0..n/2): registers 64 (n <= 254) .. 158 (n = 1024)
+    if (n / 2 < 2 * VT) go(k_voc_align<2>);
+    else if (n / 2 < 3 * VT) go(k_voc_align<3>);
+    else if (n / 2 < 5 * VT) go(k_voc_align<5>);
+    else go(k_voc_align<9>);
     SW_CUDA(cudaGetLastError());
     return ok;
 }
