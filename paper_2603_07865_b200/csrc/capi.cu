@@ -169,6 +169,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     SW_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     SW_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
     SW_CUDA(cudaDeviceGetAttribute(&c.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    SW_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
     c.tc_ok = major == 10 && minor == 0 && encode_tensor_maps(c);
     SW_CUDA(cudaEventCreateWithFlags(&c.scratch_ev, cudaEventDisableTiming));
 }

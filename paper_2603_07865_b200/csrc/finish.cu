@@ -12,6 +12,7 @@
 //     block sums (gater.cpp:18-26) -> 128-byte HitRec (the multi-GPU all-gather record)
 //  E  (optional) score_candidates + select + context_features + choose_arm + t* (select_dev.cuh)
 #include <cfloat>
+#include <cstdlib>
 
 #include "select_dev.cuh"
 
@@ -26,6 +27,7 @@ constexpr int SC = 32;      // dims per staged chunk of the rescoring ring
 constexpr int SP = SC + 4;  // 144-byte smem rows: 16 B aligned for cp.async; the 8 lanes of each
                             // LDS.128 phase read rows l..l+7 -> banks 4l..4l+3, conflict-free
 constexpr int NST = 4;      // ring stages per warp
+constexpr int SPHI = 64;    // candidates whose block sums phase B keeps in shared memory
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -81,6 +83,8 @@ struct FinSmem {
     int32_t sel_row[kMaxTopK];
     double sel_sim[kMaxTopK];
     HitRec rec[kMaxTopK];  // mirror of the hit records for the select stage
+    double phi[SPHI][8];   // gater block sums of the best row of candidates i < SPHI (phase B)
+    int32_t sel_idx[kMaxTopK];
     float cut;
     int n, ovf, nh, emitted;
 };
@@ -118,6 +122,38 @@ __device__ __forceinline__ double chain_dot(const float4* __restrict__ rp,
     return s;
 }
 
+// chain_dot that also produces the gater's 8 block sums (gater.cpp:18-26: block j is the
+// sequential fp64 sum over [j D/8, (j+1) D/8) starting from 0) as a second, independent chain;
+// valid when D == Df and D % 32 == 0 (blocks are whole float4 runs).
+template <int N4, int PF>
+__device__ __forceinline__ double chain_dot_phi(const float4* __restrict__ rp,
+                                                const double* __restrict__ qd, double (&phi)[8]) {
+    constexpr int BS4 = N4 / 8;
+    float4 ring[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) ring[i] = __ldg(rp + i);
+    double s = 0.0, bsum = 0.0;
+#pragma unroll
+    for (int i = 0; i < N4; ++i) {
+        const float4 x = ring[i % PF];
+        if (i + PF < N4) ring[i % PF] = __ldg(rp + i + PF);
+        const double x0 = x.x, x1 = x.y, x2 = x.z, x3 = x.w;
+        s = fma(qd[4 * i + 0], x0, s);
+        bsum = fma(qd[4 * i + 0], x0, bsum);
+        s = fma(qd[4 * i + 1], x1, s);
+        bsum = fma(qd[4 * i + 1], x1, bsum);
+        s = fma(qd[4 * i + 2], x2, s);
+        bsum = fma(qd[4 * i + 2], x2, bsum);
+        s = fma(qd[4 * i + 3], x3, s);
+        bsum = fma(qd[4 * i + 3], x3, bsum);
+        if ((i + 1) % BS4 == 0) {
+            phi[(i + 1) / BS4 - 1] = bsum;
+            bsum = 0.0;
+        }
+    }
+    return s;
+}
+
 __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
                                                 const double* __restrict__ qd, int n4) {
     switch (n4) {
@@ -139,7 +175,8 @@ __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
     return s;
 }
 
-__global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
+template <bool RING>
+__global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
     extern __shared__ double qd[];  // query as doubles, Df
     __shared__ FinSmem S;
     const int b = blockIdx.x;
@@ -294,7 +331,11 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
     // cp.async ring (coalesced 128-byte row segments), and lane l runs ITS row's sequential fp64
     // chain from shared memory.
     const int64_t items = n << p.logRp;
-    float* ring = reinterpret_cast<float*>(qd + p.Df) + (size_t)warp * NST * 32 * SP;
+    // block sums ride along phase B for D in {64, 128, 256, 512} (unpadded, whole-float4 blocks)
+    const bool fast_phi = !RING && p.D == p.Df && (p.D == 64 || p.D == 128 || p.D == 256 ||
+                                                   p.D == 512);
+    float* ring = RING ? reinterpret_cast<float*>(qd + p.Df) + (size_t)warp * NST * 32 * SP
+                       : nullptr;
     const int nch = (p.Df + SC - 1) / SC;
     for (int64_t g0 = (int64_t)warp * 32; g0 < items; g0 += FT) {
         const int64_t w = g0 + lane;
@@ -317,49 +358,71 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                     key = (pr << 6) | r;
             }
         }
-        // lane l stages float4 (l & 7) of rows (l >> 3) + 4u, u = 0..7
-        const float* src[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int64_t rj = __shfl_sync(full, row, (lane >> 3) + 4 * u);
-            src[u] = rj >= 0 ? p.rows + rj * p.Df + 4 * (lane & 7) : nullptr;
-        }
-        auto issue = [&](int ch) {
-            if (ch < nch) {
-                const int d0 = ch * SC;
-                float* dst = ring + (size_t)(ch % NST) * 32 * SP + 4 * (lane & 7);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (src[u] && d0 + 4 * (lane & 7) < p.Df)
-                        cp_async16(dst + ((lane >> 3) + 4 * u) * SP, src[u] + d0);
-            }
-            cp_async_commit();  // empty groups keep the wait count uniform
-        };
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < NST - 1; ++c) issue(c);
         double s = 0.0;
-        for (int ch = 0; ch < nch; ++ch) {
-            issue(ch + NST - 1);
-            cp_async_wait<NST - 1>();
-            __syncwarp();
+        double phi[8];
+        if constexpr (!RING) {
+            // lane l streams ITS row straight from L2 (phase A bulk-prefetched it) with a
+            // 16-deep float4 register ring; no shared-memory staging, so 1024 query CTAs fit
+            // in one wave. With whole-float4 gater blocks the same pass also yields the block
+            // sums (phase D then does not re-read the row)
             if (row >= 0) {
-                const float4* sr4 =
-                    reinterpret_cast<const float4*>(ring + ((size_t)(ch % NST) * 32 + lane) * SP);
-                const double* qq = qd + ch * SC;
-                const int dn4 = min(SC, p.Df - ch * SC) >> 2;
-#pragma unroll
-                for (int d4 = 0; d4 < SC / 4; ++d4) {  // sequential order i = 0..D-1
-                    if (d4 < dn4) {
-                        const float4 x = sr4[d4];
-                        s = fma(qq[4 * d4 + 0], (double)x.x, s);
-                        s = fma(qq[4 * d4 + 1], (double)x.y, s);
-                        s = fma(qq[4 * d4 + 2], (double)x.z, s);
-                        s = fma(qq[4 * d4 + 3], (double)x.w, s);
+                const float4* rp4 = reinterpret_cast<const float4*>(p.rows + row * p.Df);
+                if (fast_phi) {
+                    switch (p.D) {
+                        case 512: s = chain_dot_phi<128, 16>(rp4, qd, phi); break;
+                        case 256: s = chain_dot_phi<64, 16>(rp4, qd, phi); break;
+                        case 128: s = chain_dot_phi<32, 16>(rp4, qd, phi); break;
+                        default: s = chain_dot_phi<16, 16>(rp4, qd, phi); break;
                     }
+                } else {
+                    s = chain_dot_any(rp4, qd, p.Df >> 2);
                 }
             }
-            __syncwarp();  // this ring slot is refilled NST - 1 chunks later
+        } else {
+            // lane l stages float4 (l & 7) of rows (l >> 3) + 4u, u = 0..7
+            const float* src[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t rj = __shfl_sync(full, row, (lane >> 3) + 4 * u);
+                src[u] = rj >= 0 ? p.rows + rj * p.Df + 4 * (lane & 7) : nullptr;
+            }
+            auto issue = [&](int ch) {
+                if (ch < nch) {
+                    const int d0 = ch * SC;
+                    float* dst = ring + (size_t)(ch % NST) * 32 * SP + 4 * (lane & 7);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (src[u] && d0 + 4 * (lane & 7) < p.Df)
+                            cp_async16(dst + ((lane >> 3) + 4 * u) * SP, src[u] + d0);
+                }
+                cp_async_commit();  // empty groups keep the wait count uniform
+            };
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < NST - 1; ++c) issue(c);
+            s = 0.0;
+            for (int ch = 0; ch < nch; ++ch) {
+                issue(ch + NST - 1);
+                cp_async_wait<NST - 1>();
+                __syncwarp();
+                if (row >= 0) {
+                    const float4* sr4 =
+                        reinterpret_cast<const float4*>(ring + ((size_t)(ch % NST) * 32 + lane) * SP);
+                    const double* qq = qd + ch * SC;
+                    const int dn4 = min(SC, p.Df - ch * SC) >> 2;
+#pragma unroll
+                    for (int d4 = 0; d4 < SC / 4; ++d4) {  // sequential order i = 0..D-1
+                        if (d4 < dn4) {
+                            const float4 x = sr4[d4];
+                            s = fma(qq[4 * d4 + 0], (double)x.x, s);
+                            s = fma(qq[4 * d4 + 1], (double)x.y, s);
+                            s = fma(qq[4 * d4 + 2], (double)x.z, s);
+                            s = fma(qq[4 * d4 + 3], (double)x.w, s);
+                        }
+                    }
+                }
+                __syncwarp();  // this ring slot is refilled NST - 1 chunks later
+            }
         }
         double sim = row >= 0 ? fmin(1.0, fmax(-1.0, s)) : -DBL_MAX;  // core.cpp:35-36
         int rw = row >= 0 ? key : 0x7fffffff;
@@ -372,6 +435,12 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
             }
         }
         if (rw != 0x7fffffff) rw &= 63;  // key -> row index
+        if constexpr (!RING) {
+            if (fast_phi && w < items && i < SPHI && row >= 0 && r == rw) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) S.phi[i][j] = phi[j];
+            }
+        }
         if (w < items && r == 0) {
             if (i < SMAXC) {
                 S.ex[i] = sim;
@@ -397,7 +466,7 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
             double bs = -DBL_MAX;
             uint64_t bid = ~0ull;
             int64_t bslot = -1;
-            int brw = 0;
+            int brw = 0, bidx = 0;
             for (int64_t i = lane; i < n; i += 32) {
                 const bool sm = i < SMAXC;
                 const double sv = sm ? S.ex[i] : p.exact[base + i];
@@ -411,6 +480,7 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                     bid = id;
                     bslot = slot;
                     brw = sm ? S.brow[i] : p.best_row[base + i];
+                    bidx = (int)i;
                 }
             }
             for (int o = 16; o; o >>= 1) {
@@ -418,11 +488,13 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                 const uint64_t oid = __shfl_xor_sync(full, bid, o);
                 const int64_t oslot = __shfl_xor_sync(full, bslot, o);
                 const int orw = __shfl_xor_sync(full, brw, o);
+                const int oidx = __shfl_xor_sync(full, bidx, o);
                 if (oslot >= 0 && (bslot < 0 || before(os, oid, bs, bid))) {
                     bs = os;
                     bid = oid;
                     bslot = oslot;
                     brw = orw;
+                    bidx = oidx;
                 }
             }
             if (bslot < 0) break;
@@ -430,6 +502,7 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
                 S.sel_slot[nh] = bslot;
                 S.sel_row[nh] = brw;
                 S.sel_sim[nh] = bs;
+                S.sel_idx[nh] = bidx;
             }
             ++nh;
             prev_sim = bs;
@@ -457,7 +530,9 @@ __global__ void __launch_bounds__(FT, 5) k_finish(const FinishParams p) {
             eid = p.ids[S.sel_slot[h]];
         }
         double s = 0.0;
-        if ((p.D & 31) == 0 && hi - lo == 64 && (lo & 3) == 0) {
+        if (fast_phi && S.sel_idx[h] < SPHI) {
+            s = S.phi[S.sel_idx[h]][j];  // computed by phase B from the same row
+        } else if ((p.D & 31) == 0 && hi - lo == 64 && (lo & 3) == 0) {
             s = chain_dot<16, 16>(reinterpret_cast<const float4*>(rp + lo), qd + lo);
         } else {
             for (size_t i = lo; i < hi; ++i) s = fma(qd[i], (double)rp[i], s);
@@ -582,14 +657,24 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     c.last_ivf = ivf;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
-        const size_t smem = sizeof(double) * c.Df + sizeof(float) * NWARP * NST * 32 * SP;
+        static const bool ring = [] {
+            const char* e = std::getenv("SW_FINISH_RING");
+            return e && e[0] == '1';
+        }();
+        const size_t smem =
+            sizeof(double) * c.Df + (ring ? sizeof(float) * NWARP * NST * 32 * SP : 0);
         static size_t attr = 0;
         if (smem > attr) {
-            SW_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+            SW_CUDA(cudaFuncSetAttribute(k_finish<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            SW_CUDA(cudaFuncSetAttribute(k_finish<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = smem;
         }
-        k_finish<<<B, FT, smem, st>>>(p);
+        if (ring)
+            k_finish<true><<<B, FT, smem, st>>>(p);
+        else
+            k_finish<false><<<B, FT, smem, st>>>(p);
     }
     SW_CUDA(cudaGetLastError());
     c.last_tc = tc ? (c.last_score_ts ? 3 : c.last_score_pair ? 2 : 1) : 0;  // 2: pairs, 3: +TS

@@ -19,6 +19,7 @@
 // entry score. Every CTA's running k-th best is a lower bound of T_a, and CTAs share it through
 // an atomicMax per query, so the emission threshold tightens as the scan proceeds. The exact
 // fp64 rescoring (exact.cu) then decides ties and order bit-exactly.
+#include <numeric>
 #include <type_traits>
 
 #include "ptx.cuh"
@@ -69,6 +70,12 @@ struct TcParams {
     float* cand_score;
     int n_chunks;
     int cap_local;
+    // balanced normal mode (bal_k > 0): 128-query groups (256 in pair mode) x bal_R tile ranges
+    // = units x bal_k items; unit u (a CTA, or a pair) walks items u, u + units, ..., so
+    // every SM works (the static (qblock, range) grid idles 148 mod #qblocks SMs)
+    int bal_R;
+    int bal_k;
+    int n_items_bal;  // groups x bal_R; unit u walks items u, u + units, ...
     const __nv_bfloat16* q_bf;    // [BmaxPad][Dp] queries (TS mode loads them into TMEM)
     // grouped IVF mode (single CTAs): one work item per CTA — a block of 128 queries that all
     // probe list l, gathered into contiguous rows, against a chunk of list l's tiles in the
@@ -167,6 +174,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int qblock = blockIdx.x;
+    const bool bal = !p.items && p.bal_k > 0;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     // Work items. Normal mode: ONE item per CTA — query block blockIdx.x x tile range
     // blockIdx.y. Grouped IVF mode: persistent CTAs walk items blockIdx.x, + gridDim.x, ...
     // (list, 128-query block, tile chunk); TMEM, barriers and the smem ring persist across
@@ -184,6 +193,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             r.ntiles = it.z;
             r.list = it.w & 255;
             r.chunk = it.w >> 8;
+        } else if (bal) {
+            // range-major: the groups sharing a tile range run it at the same time, so each
+            // range streams from HBM once and the other groups hit L2
+            const int ng = p.n_items_bal / p.bal_R;
+            const int rr = i / ng, g = i - rr * ng;
+            r.qrow = (PAIR ? 2 * g + (int)(blockIdx.x & 1) : g) * BM;
+            r.t0 = (int64_t)rr * p.tiles_per_cta;
+            r.ntiles = (int)max((int64_t)0, min(p.n_tiles, r.t0 + p.tiles_per_cta) - r.t0);
+            r.list = 0;
+            r.chunk = rr;
         } else {
             r.qrow = qblock * BM;
             r.t0 = (int64_t)blockIdx.y * p.tiles_per_cta;
@@ -192,9 +211,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         return r;
     };
-    const int n_items = p.items ? *p.n_items : 1;
-    const int item0 = p.items ? (int)blockIdx.x : 0;
-    const int istep = p.items ? (int)gridDim.x : 1;
+    const int istep = p.items ? (int)gridDim.x : bal ? (PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x) : 1;
+    // does item i load A? (balanced mode: only when its query block differs from the unit's
+    // previous item's)
+    auto loads_a = [&](int i, int first) {
+        return !bal || i == first || item_at(i).qrow != item_at(i - istep).qrow;
+    };
+    const int n_items = p.items ? *p.n_items : bal ? p.n_items_bal : 1;
+    const int item0 = p.items ? (int)blockIdx.x : bal ? unit : 0;
     if (item0 >= n_items || item_at(item0).ntiles == 0) return;  // uniform for the CTA / pair
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
@@ -238,14 +262,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---------------- TMA producer
             int s = 0;  // ring stage and its phase, advanced incrementally (no division)
             uint32_t ph = 0;
-            int itn = 0;
-            for (int ii = item0; ii < n_items; ii += istep, ++itn) {
+            int na = 0;  // A loads issued
+            for (int ii = item0; ii < n_items; ii += istep) {
                 const Item itm = item_at(ii);
                 const int qrow = itm.qrow;
                 const int64_t t0 = itm.t0;
                 const int ntiles = itm.ntiles;
-                if (itn > 0) ptx::mbar_wait_sleep(bar(AEMPTY), (uint32_t)((itn - 1) & 1));
-                if (TS) {
+                const bool lda = loads_a(ii, item0);
+                if (lda && na > 0) ptx::mbar_wait_sleep(bar(AEMPTY), (uint32_t)((na - 1) & 1));
+                if (lda) ++na;
+                if (!lda) {
+                    // same queries as the previous item: A stays resident
+                } else if (TS) {
                     // queries go to TMEM through the epilogue warps
                 } else if (PAIR) {
                     // both CTAs load their own queries / their half of each tile; the bytes
@@ -296,13 +324,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             int gt = 0;  // tiles across items: accumulator index and phase
-            int itn = 0;
-            for (int ii = item0; ii < n_items; ii += istep, ++itn) {
+            int na = 0;  // A loads consumed
+            for (int ii = item0; ii < n_items; ii += istep) {
                 const int ntiles = item_at(ii).ntiles;
-                if (TS)
-                    ptx::mbar_wait_cluster(bar(AFULL), (uint32_t)(itn & 1));
-                else
-                    ptx::mbar_wait(bar(AFULL), (uint32_t)(itn & 1));
+                if (loads_a(ii, item0)) {
+                    if (TS)
+                        ptx::mbar_wait_cluster(bar(AFULL), (uint32_t)(na & 1));
+                    else
+                        ptx::mbar_wait(bar(AFULL), (uint32_t)(na & 1));
+                    ++na;
+                }
                 ptx::tc_fence_after();
                 for (int lt = 0; lt < ntiles; ++lt, ++gt) {
                     const int acc = gt & 1;
@@ -349,9 +380,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     __syncwarp();
                 }
-                // the item's MMAs are issued: A may be overwritten once they complete
-                // (multi-item CTAs are single-CTA grouped IVF only)
-                if (p.items && ptx::elect_one()) ptx::mma_commit(bar(AEMPTY));
+                // the item's MMAs are issued: A may be overwritten once they complete (signalled
+                // only when the next item reloads A; both CTAs of a pair are told)
+                if (ii + istep < n_items && loads_a(ii + istep, item0) && ptx::elect_one()) {
+                    if (PAIR)
+                        ptx::mma_commit_pair(bar(AEMPTY));
+                    else
+                        ptx::mma_commit(bar(AEMPTY));
+                }
                 __syncwarp();
             }
         }
@@ -371,7 +407,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int g_list = itm.list, g_chunk = itm.chunk;
         const int q = p.qmap ? p.qmap[qrow + quarter * 32 + lane] : qrow + quarter * 32 + lane;
         const bool qvalid = q >= 0 && q < p.B;
-        int vchunk = blockIdx.y * EPI_GROUPS + grp;
+        int vchunk = (bal ? itm.chunk : (int)blockIdx.y) * EPI_GROUPS + grp;
         if (p.items)  // grouped IVF: slice = (probe rank of this list for q, chunk of the list)
             vchunk = qvalid ? (int)p.prank[(int64_t)q * kMaxCentroids + g_list] * p.grp_ch + g_chunk
                             : 0;
@@ -748,7 +784,7 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
         SW_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      c.smem_optin));
         // persistent: one CTA per SM walks the items (max_items only bounds the grid)
-        kf<<<dim3((unsigned)std::min<int64_t>(max_items, 148), 1), THREADS, smem, st>>>(
+        kf<<<dim3((unsigned)std::min<int64_t>(max_items, c.num_sms), 1), THREADS, smem, st>>>(
             c.tm_qg, c.tm_sorted, p);
     };
     (void)attr_set;
@@ -807,10 +843,37 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     const int64_t rows_hw = c.high_water * c.Rp;
     p.n_tiles = (rows_hw + tbn - 1) / tbn;
     const int qblocks = qb;
-    int64_t chunks = std::max<int64_t>(1, 148 / qblocks);
+    int64_t chunks = std::max<int64_t>(1, c.num_sms / qblocks);
     chunks = std::min<int64_t>(chunks, p.n_tiles);
     p.tiles_per_cta = (p.n_tiles + chunks - 1) / chunks;
     chunks = (p.n_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
+    // Balanced persistent schedule (opt-in, SW_SCORE_BAL=1): groups x R ranges = units x k
+    // items, so all SMs work (B = 1024: 4 pair groups over 74 pairs -> R = 37, 2 range-major
+    // items per pair, 148 SMs instead of 144). Measured SLOWER at config 3 and therefore off:
+    // 0.738 vs 0.707 ms full kernel, and even the pure-MMA ablation loses (0.546 vs 0.531 ms)
+    // although each pair issues 212 instead of 218 tiles — the item switch (A reload behind
+    // the last MMA of the previous item, B ring drained) costs more than the 4 extra SMs give.
+    static const bool bal_ok = [] {
+        const char* e = getenv("SW_SCORE_BAL");
+        return e && e[0] == '1';
+    }();
+    dim3 grid((unsigned)qblocks, (unsigned)chunks);
+    p.bal_R = p.bal_k = 0;
+    if (bal_ok && !ts) {
+        const int units = pair ? c.num_sms / 2 : c.num_sms;
+        const int groups = pair ? qblocks / 2 : qblocks;
+        const int R = units / std::gcd(groups, units);
+        const int64_t tpr = (p.n_tiles + R - 1) / R;
+        if (R * EPI_GROUPS <= kMaxSlices && (int64_t)(R - 1) * tpr < p.n_tiles &&
+            (int64_t)groups * R % units == 0) {
+            p.bal_R = R;
+            p.bal_k = (int)((int64_t)groups * R / units);
+            p.n_items_bal = groups * R;
+            p.tiles_per_cta = tpr;
+            chunks = R;
+            grid = dim3((unsigned)(pair ? 2 * units : units), 1);
+        }
+    }
     p.n_slots = c.high_water;
     p.valid_bits = c.valid_bits;
     p.q_eps = c.q_eps;
@@ -835,7 +898,6 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
         return e ? atoi(e) : 0;
     }();
     p.experiment = experiment;
-    dim3 grid((unsigned)qblocks, (unsigned)chunks);
     if (ts)
         launch_tc<true, true>(c, p, grid, smem, st);
     else if (pair)

@@ -158,6 +158,7 @@ struct Ctx {
     CUtensorMap tm_q{};
     bool tc_ok = false;
     int smem_optin = 0;
+    int num_sms = 148;
 
     // IVF coarse quantiser (IvfIndex, index.hpp:47-101). ivf == false: exhaustive (one list).
     bool ivf = false;
