@@ -72,6 +72,15 @@ static void free_ctx(Ctx& c) {
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
     for (cudaEvent_t e : c.prof_ev) cudaEventDestroy(e);
     if (c.scratch_ev) cudaEventDestroy(c.scratch_ev);
+    for (int i = 0; i < Ctx::kPipe; ++i) {
+        if (c.pipe_q[i]) cudaFree(c.pipe_q[i]);
+        if (c.pipe_req[i]) cudaFree(c.pipe_req[i]);
+        if (c.pipe_ch[i]) cudaFree(c.pipe_ch[i]);
+        for (cudaEvent_t e : {c.pipe_h2d[i], c.pipe_used[i], c.pipe_done[i]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (c.pipe_in) cudaStreamDestroy(c.pipe_in);
+    if (c.pipe_out) cudaStreamDestroy(c.pipe_out);
     if (c.mstream) cudaStreamDestroy(c.mstream);
 }
 
@@ -844,6 +853,77 @@ int sw_warmstart(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t
         int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, st);
         launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, st);
         c.last_kernels = kn + 1;
+        return SW_OK;
+    });
+}
+
+// Pipelined host path: the same work as sw_warmstart_host, returned before it completes.
+// Submission n uses staging slot n mod kPipe: its H2D runs on pipe_in once the slot's previous
+// batch has consumed it, the kernels on the caller's stream after that H2D (and after the
+// previous hot-path user, HotGuard), the D2H of the choices on pipe_out after the kernels. So
+// batch n+1's prompts cross PCIe while batch n is being scored.
+int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs, int32_t B,
+                             uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                             uint64_t philox_seed, sw_choice* choices, float* d_out,
+                             int32_t t_out_max, void* stream, int64_t* ticket) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && ticket && (B == 0 || (q && reqs && choices && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
+        std::lock_guard<std::mutex> pl(c.pipe_mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        if (!c.pipe_in) {
+            SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_in, cudaStreamNonBlocking));
+            SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_out, cudaStreamNonBlocking));
+            for (int i = 0; i < Ctx::kPipe; ++i) {
+                SW_CUDA(cudaMalloc(&c.pipe_q[i], sizeof(float) * (size_t)c.Bmax * c.D));
+                SW_CUDA(cudaMalloc(&c.pipe_req[i], sizeof(sw_request) * (size_t)c.Bmax));
+                SW_CUDA(cudaMalloc(&c.pipe_ch[i], sizeof(sw_choice) * (size_t)c.Bmax));
+                for (cudaEvent_t* e : {&c.pipe_h2d[i], &c.pipe_used[i], &c.pipe_done[i]})
+                    SW_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+                SW_CUDA(cudaEventRecord(c.pipe_used[i], c.pipe_in));
+            }
+        }
+        const int slot = (int)(c.pipe_seq % Ctx::kPipe);
+        cudaStream_t st = as_stream(stream);
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_in, c.pipe_used[slot], 0));
+        SW_CUDA(cudaMemcpyAsync(c.pipe_q[slot], q, sizeof(float) * (size_t)B * c.D,
+                                cudaMemcpyHostToDevice, c.pipe_in));
+        SW_CUDA(cudaMemcpyAsync(c.pipe_req[slot], reqs, sizeof(sw_request) * (size_t)B,
+                                cudaMemcpyHostToDevice, c.pipe_in));
+        SW_CUDA(cudaEventRecord(c.pipe_h2d[slot], c.pipe_in));
+        {
+            HotGuard lk(c, st);
+            SW_CUDA(cudaStreamWaitEvent(st, c.pipe_h2d[slot], 0));
+            int kn = plan_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed, sel, pol,
+                               c.pipe_ch[slot], st);
+            launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr, philox_seed,
+                               d_out, t_out_max, st);
+            SW_CUDA(cudaEventRecord(c.pipe_used[slot], st));
+            c.last_kernels = kn + 1;
+        }
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));
+        SW_CUDA(cudaMemcpyAsync(choices, c.pipe_ch[slot], sizeof(sw_choice) * (size_t)B,
+                                cudaMemcpyDeviceToHost, c.pipe_out));
+        SW_CUDA(cudaEventRecord(c.pipe_done[slot], c.pipe_out));
+        *ticket = c.pipe_seq++;
+        return SW_OK;
+    });
+}
+
+int sw_warmstart_host_wait(sw_ctx* ctx, int64_t ticket) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        cudaEvent_t e;
+        {
+            std::lock_guard<std::mutex> pl(c.pipe_mu);
+            SW_REQUIRE(ticket >= 0 && ticket < c.pipe_seq, "unknown ticket");
+            // a slot's event is re-recorded by later submissions; waiting on the newer record
+            // also covers the older batch (pipe_out runs the D2H copies in submission order)
+            e = c.pipe_done[ticket % Ctx::kPipe];
+        }
+        SW_CUDA(cudaEventSynchronize(e));
         return SW_OK;
     });
 }

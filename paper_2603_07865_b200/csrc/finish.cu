@@ -87,6 +87,7 @@ struct FinSmem {
     int32_t sel_idx[kMaxTopK];
     float cut;
     int n, ovf, nh, emitted;
+    long long t_ta, t_sync;
 };
 
 __device__ __forceinline__ bool before(double as, uint64_t aid, double bs, uint64_t bid) {
@@ -231,11 +232,13 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
                 kth = ord2f((uint32_t)(best >> 32));
             }
             if (lane == 0) S.cut = kth - 2.0f * p.q_eps[b];
+            if (lane == 0) S.t_ta = clock64();
         }
         // slice sizes of this warp's chunks c = warp + NWARP * j (lane j), loaded before the cut
         // is known so the round trip overlaps warp 0's T_a selection
         const int nloc = (p.n_chunks - warp + NWARP - 1) / NWARP;
         __syncthreads();
+        const long long t_sync = clock64();
         const float cut = S.cut;
         const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
         int emitted = 0;
@@ -319,6 +322,7 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
             }
         }
         if (lane == 0) atomicAdd(&S.emitted, emitted);  // every lane summed the same counts
+        if (t == 0) S.t_sync = t_sync;
     } else if (t == 0) {
         S.n = (int)p.n_slots;
     }
@@ -575,6 +579,10 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
         d[3] = (int32_t)(t_b - t_a);
         d[4] = (int32_t)(t_d - t_b);
         d[5] = (int32_t)(clock64() - t_d);
+        if (!p.implicit_all) {  // phase A split: T_a selection, barrier wait
+            d[6] = (int32_t)(S.t_ta - t_start);
+            d[7] = (int32_t)(S.t_sync - t_start);
+        }
     }
 }
 

@@ -215,6 +215,16 @@ struct Ctx {
     // scratch_ev, so concurrent readers on different streams never overlap on it.
     std::mutex scratch_mu;
     cudaEvent_t scratch_ev = nullptr;
+    // pipelined host path (sw_warmstart_host_submit / _wait): kPipe staging slots, H2D on
+    // pipe_in, D2H on pipe_out, so batch i+1's copies overlap batch i's kernels
+    static constexpr int kPipe = 2;
+    std::mutex pipe_mu;
+    int64_t pipe_seq = 0;
+    cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+    cudaEvent_t pipe_h2d[kPipe] = {}, pipe_used[kPipe] = {}, pipe_done[kPipe] = {};
+    float* pipe_q[kPipe] = {};
+    sw_request* pipe_req[kPipe] = {};
+    sw_choice* pipe_ch[kPipe] = {};
     // stage profiling (CUDA events on the launching stream; single-threaded use)
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;   // pool, pairs (start, stop)

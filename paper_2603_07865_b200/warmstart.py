@@ -319,6 +319,23 @@ class WarmStartCache:
               "sw_warmstart_host")
         return ch
 
+    def warmstart_host_submit(self, queries: np.ndarray, reqs: np.ndarray, choices: np.ndarray,
+                              d_out, t_out_max: int, seed: int = 1, sel: SelectorConfig = None,
+                              policy: Policy = None, philox_seed: int = 0, stream=None) -> int:
+        """Pipelined warmstart_host: returns a ticket at once; `queries`, `reqs` and `choices`
+        (a CHOICE_DTYPE array filled in place) must stay alive until warmstart_host_wait."""
+        sel = sel or SelectorConfig()
+        policy = policy or Policy()
+        t = C.c_int64()
+        check(_lib.lib().sw_warmstart_host_submit(
+            self._h, ptr(queries), ptr(reqs), queries.shape[0], seed, C.byref(sel.c()),
+            C.byref(policy.c()), philox_seed, ptr(choices), ptr(d_out), t_out_max, stream,
+            C.byref(t)), "sw_warmstart_host_submit")
+        return t.value
+
+    def warmstart_host_wait(self, ticket: int) -> None:
+        check(_lib.lib().sw_warmstart_host_wait(self._h, ticket), "sw_warmstart_host_wait")
+
     # ------------------------------------------------------------------ component entry points
     def score_select(self, sims, s_neg, durations, L, sel: SelectorConfig, rng_seed: int):
         """score_candidates + select on one candidate set (selector.cpp:24-85)."""
