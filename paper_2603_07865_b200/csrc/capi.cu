@@ -1058,6 +1058,8 @@ int sw_profile_enable(sw_ctx* ctx, int32_t on) {
     return guarded([&] {
         SW_REQUIRE(ctx, "null argument");
         ctx->c.prof = on != 0;
+        // on = SW_PROFILE_MASK | stage bits: time only those stages (fewer events in a loop)
+        ctx->c.prof_mask = (on & SW_PROFILE_MASK) ? (uint32_t)(on & 0xFF) : 0xFFu;
         return SW_OK;
     });
 }

@@ -227,6 +227,7 @@ struct Ctx {
     sw_choice* pipe_ch[kPipe] = {};
     // stage profiling (CUDA events on the launching stream; single-threaded use)
     bool prof = false;
+    uint32_t prof_mask = 0xFFu;         // stages recorded while prof is on
     std::vector<cudaEvent_t> prof_ev;   // pool, pairs (start, stop)
     std::vector<int> prof_stage;        // stage of each recorded pair
     size_t prof_used = 0;
@@ -259,7 +260,7 @@ struct StageScope {
     cudaStream_t st;
     size_t pair = (size_t)-1;
     StageScope(Ctx& cc, int stage, cudaStream_t s) : c(cc), st(s) {
-        if (!c.prof) return;
+        if (!c.prof || !((c.prof_mask >> stage) & 1u)) return;
         if (2 * (c.prof_used + 1) > c.prof_ev.size()) {
             for (int i = 0; i < 2; ++i) {
                 cudaEvent_t e;

@@ -221,8 +221,14 @@ class WarmStartCache:
         """IvfIndex::save (index.cpp:347-369) of this cache's index."""
         check(_lib.lib().sw_swix_save(self._h, path.encode()), "sw_swix_save")
 
-    def profile(self, on: bool = True):
-        check(_lib.lib().sw_profile_enable(self._h, int(on)), "profile")
+    def profile(self, on: bool = True, stages=None):
+        """Stage timing on/off; `stages` (names from _lib.STAGES) limits it to those stages."""
+        v = int(on)
+        if on and stages is not None:
+            v = 0x100
+            for name in stages:
+                v |= 1 << _lib.STAGES.index(name)
+        check(_lib.lib().sw_profile_enable(self._h, v), "profile")
 
     def profile_reset(self):
         check(_lib.lib().sw_profile_reset(self._h), "profile_reset")
