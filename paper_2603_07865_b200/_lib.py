@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsemwarm_b200.so")
+# SW_LIB_PATH: load another in-tree build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("SW_LIB_PATH") or os.path.join(PKG, "libsemwarm_b200.so")
 
 SW_OK = 0
 SW_EINVAL = -1

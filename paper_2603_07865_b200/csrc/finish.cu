@@ -195,128 +195,183 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
 
     // ---------------- A: certified candidate set
     if (!p.implicit_all) {
+        // slice sizes of this warp's chunks c = warp + NWARP * j (lane j) for the first pass,
+        // loaded before the cut is known so the round trip overlaps warp 0's T_a selection
+        const int nloc = (p.n_chunks - warp + NWARP - 1) / NWARP;
+        const int raw0 = lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + warp + NWARP * lane] : 0;
         if (warp == 0) {  // T_a over the union of the scoring CTAs' final lists
             const int m = p.n_chunks * p.k;
             const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
-            constexpr int NV = 16;  // m <= 512 held in registers (148 CTAs x 8 = 1184 max)
-            float vals[NV];
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int i = lane + 32 * u;
-                vals[u] = i < m ? tk[(i / p.k) * kMaxTopK + (i % p.k)] : -INFINITY;
-            }
-            unsigned long long prev = ~0ull;
+            constexpr int NV = 16;  // m <= 512 held in registers
             float kth = -INFINITY;
-            for (int r = 0; r < p.k; ++r) {
-                unsigned long long best = 0;
+            if (m <= 32 * NV) {
+                // k-th largest (duplicates counted) by descending distinct values: a warp max
+                // (REDUX) of the keys below the previous one, then a warp count of its copies
+                const bool pow2 = (p.k & (p.k - 1)) == 0;
+                const int lk = __ffs(p.k) - 1;
+                uint32_t key[NV];
 #pragma unroll
                 for (int u = 0; u < NV; ++u) {
-                    if (vals[u] == -INFINITY) continue;
-                    const unsigned long long key = ((unsigned long long)f2ord(vals[u]) << 32) |
-                                                   (0xFFFFFFFFu - (uint32_t)(lane + 32 * u));
-                    if (key < prev && key > best) best = key;
+                    const int i = lane + 32 * u;
+                    key[u] = 0u;  // below every real score's key
+                    if (i < m) {
+                        const int sl = pow2 ? i >> lk : i / p.k;
+                        const float v = tk[sl * kMaxTopK + (i - sl * p.k)];
+                        if (v != -INFINITY) key[u] = f2ord(v);
+                    }
                 }
-                for (int i = lane + 32 * NV; i < m; i += 32) {  // rare: very wide grids
-                    const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
-                    if (v == -INFINITY) continue;
-                    const unsigned long long key =
-                        ((unsigned long long)f2ord(v) << 32) | (0xFFFFFFFFu - (uint32_t)i);
-                    if (key < prev && key > best) best = key;
+                uint32_t prev = 0xFFFFFFFFu;
+                int total = 0;
+                for (;;) {
+                    uint32_t lm = 0u;
+#pragma unroll
+                    for (int u = 0; u < NV; ++u) lm = max(lm, key[u] < prev ? key[u] : 0u);
+                    const uint32_t cur = __reduce_max_sync(full, lm);
+                    if (cur == 0u) break;  // fewer than k valid entries: keep everything
+                    int c = 0;
+#pragma unroll
+                    for (int u = 0; u < NV; ++u) c += key[u] == cur ? 1 : 0;
+                    total += (int)__reduce_add_sync(full, (unsigned)c);
+                    prev = cur;
+                    if (total >= p.k) {
+                        kth = ord2f(cur);
+                        break;
+                    }
                 }
-                best = warp_max_u64(best);
-                if (best == 0) {  // fewer than k valid entries in the shard: keep everything
-                    kth = -INFINITY;
-                    break;
+            } else {  // very wide grids (small batches): 64-bit (value, index) keys from L2
+                unsigned long long prev = ~0ull;
+                for (int r = 0; r < p.k; ++r) {
+                    unsigned long long best = 0;
+                    for (int i = lane; i < m; i += 32) {
+                        const float v = tk[(i / p.k) * kMaxTopK + (i % p.k)];
+                        if (v == -INFINITY) continue;
+                        const unsigned long long key =
+                            ((unsigned long long)f2ord(v) << 32) | (0xFFFFFFFFu - (uint32_t)i);
+                        if (key < prev && key > best) best = key;
+                    }
+                    best = warp_max_u64(best);
+                    if (best == 0) {
+                        kth = -INFINITY;
+                        break;
+                    }
+                    prev = best;
+                    kth = ord2f((uint32_t)(best >> 32));
                 }
-                prev = best;
-                kth = ord2f((uint32_t)(best >> 32));
             }
             if (lane == 0) S.cut = kth - 2.0f * p.q_eps[b];
             if (lane == 0) S.t_ta = clock64();
         }
-        // slice sizes of this warp's chunks c = warp + NWARP * j (lane j), loaded before the cut
-        // is known so the round trip overlaps warp 0's T_a selection
-        const int nloc = (p.n_chunks - warp + NWARP - 1) / NWARP;
         __syncthreads();
         const long long t_sync = clock64();
         const float cut = S.cut;
         const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
         int emitted = 0;
+        // keeps one candidate: shared list (+ global spill list) and an L2 prefetch of its rows
+        auto keep = [&](int pos, int slot) {
+            if (pos < SMAXC) S.slot[pos] = slot;
+            p.list[base + pos] = slot;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             p.rows + (int64_t)slot * p.Rp * p.Df),
+                         "r"((uint32_t)row_bytes)
+                         : "memory");
+        };
         for (int j0 = 0; j0 < nloc; j0 += 32) {
             const int cj = warp + NWARP * (j0 + lane);
-            const int raw = j0 + lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + cj] : 0;
+            const int raw = j0 == 0 ? raw0
+                                    : (j0 + lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + cj] : 0);
             if (__any_sync(full, raw > p.cap_local) && lane == 0) S.ovf = 1;
             const int my_cnt = min(raw, p.cap_local);
             const int jn = min(32, nloc - j0);
-            // 4 chunks x 2 segments of 128 entries in flight per lane
-            for (int jg = 0; jg < jn; jg += 4) {
-                float4 sc[4][2];
-                int4 sl[4][2];
-                int cnt[4];
-                int64_t src[4];
+            // CH chunks per round, all their first-128-entry score segments in flight at once;
+            // a lane's pass bits (chunk u, element e -> bit 4u + e) are compacted with ONE warp
+            // scan + shared atomic per round, then only the passing slots are loaded
+            constexpr int CH = 8;
+            for (int jg = 0; jg < jn; jg += CH) {
+                float4 sc[CH];
+                int cnt[CH];
+                int64_t src[CH];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < CH; ++u) {
                     const int j = jg + u;
                     cnt[u] = __shfl_sync(full, my_cnt, j < jn ? j : 0);
                     if (j >= jn) cnt[u] = 0;
                     src[u] = base + (int64_t)(warp + NWARP * (j0 + j)) * p.cap_local;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = 128 * h + 4 * lane;
-                        sc[u][h] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                        sl[u][h] = make_int4(0, 0, 0, 0);
-                        if (i < cnt[u]) {
-                            sc[u][h] = *reinterpret_cast<const float4*>(p.cand_score + src[u] + i);
-                            sl[u][h] = *reinterpret_cast<const int4*>(p.cand_slot + src[u] + i);
-                        }
-                    }
+                    sc[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                    if (4 * lane < cnt[u])
+                        sc[u] = *reinterpret_cast<const float4*>(p.cand_score + src[u] + 4 * lane);
                 }
-                auto consume = [&](int cn, int i0, float4 sv, int4 lv) {
-                    const int i = i0 + 4 * lane;
-                    const float scv[4] = {sv.x, sv.y, sv.z, sv.w};
-                    const int slv[4] = {lv.x, lv.y, lv.z, lv.w};
-                    int mine = 0;
+                uint32_t bits = 0u;
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) mine += (i + e < cn && scv[e] >= cut) ? 1 : 0;
-                    int incl = mine;  // warp inclusive scan of per-lane pass counts
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int v = __shfl_up_sync(full, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    const int tot = __shfl_sync(full, incl, 31);
-                    int wbase = 0;
-                    if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
-                    wbase = __shfl_sync(full, wbase, 0);
-                    int pos = wbase + incl - mine;
+                for (int u = 0; u < CH; ++u) {
+                    emitted += cnt[u];
+                    const float v4[4] = {sc[u].x, sc[u].y, sc[u].z, sc[u].w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if (i + e < cn && scv[e] >= cut) {
-                            if (pos < SMAXC) S.slot[pos] = slv[e];
-                            p.list[base + pos] = slv[e];
-                            // pull the candidate's rows into L2 now; phase B stages them
-                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                             p.rows + (int64_t)slv[e] * p.Rp * p.Df),
-                                         "r"((uint32_t)row_bytes)
-                                         : "memory");
-                            ++pos;
+                    for (int e = 0; e < 4; ++e)
+                        if (4 * lane + e < cnt[u] && v4[e] >= cut) bits |= 1u << (4 * u + e);
+                }
+                const int mine = __popc(bits);
+                int incl = mine;  // warp inclusive scan of per-lane pass counts
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(full, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int tot = __shfl_sync(full, incl, 31);
+                int wbase = 0;
+                if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
+                int pos = __shfl_sync(full, wbase, 0) + incl - mine;
+                while (bits) {  // up to 4 slot loads in flight per lane
+                    int sl4[4];
+                    int nb = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        sl4[q] = -1;
+                        if (bits) {
+                            const int bit = __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            const int64_t sb =  // src[bit >> 2] without a local-memory array
+                                base + (int64_t)(warp + NWARP * (j0 + jg + (bit >> 2))) * p.cap_local;
+                            sl4[q] = p.cand_slot[sb + 4 * lane + (bit & 3)];
+                            ++nb;
                         }
                     }
-                };
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    emitted += cnt[u];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        if (128 * h < cnt[u]) consume(cnt[u], 128 * h, sc[u][h], sl[u][h]);
-                    for (int i0 = 256; i0 < cnt[u]; i0 += 128) {  // rare: slices > 256 entries
+                    for (int q = 0; q < 4; ++q)
+                        if (q < nb) keep(pos++, sl4[q]);
+                }
+                // rare: chunks with more than 128 emitted entries (count and base recomputed,
+                // so no register array is indexed dynamically)
+#pragma unroll 1
+                for (int u = 0; u < CH && jg + u < jn; ++u) {
+                    const int cu = __shfl_sync(full, my_cnt, jg + u);
+                    if (cu <= 128) continue;
+                    const int64_t su = base + (int64_t)(warp + NWARP * (j0 + jg + u)) * p.cap_local;
+                    for (int i0 = 128; i0 < cu; i0 += 128) {
                         const int i = i0 + 4 * lane;
                         float4 sv = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
                         int4 lv = make_int4(0, 0, 0, 0);
-                        if (i < cnt[u]) {
-                            sv = *reinterpret_cast<const float4*>(p.cand_score + src[u] + i);
-                            lv = *reinterpret_cast<const int4*>(p.cand_slot + src[u] + i);
+                        if (i < cu) {
+                            sv = *reinterpret_cast<const float4*>(p.cand_score + su + i);
+                            lv = *reinterpret_cast<const int4*>(p.cand_slot + su + i);
                         }
-                        consume(cnt[u], i0, sv, lv);
+                        const float scv[4] = {sv.x, sv.y, sv.z, sv.w};
+                        const int slv[4] = {lv.x, lv.y, lv.z, lv.w};
+                        int mn = 0;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) mn += (i + e < cu && scv[e] >= cut) ? 1 : 0;
+                        int in2 = mn;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int v = __shfl_up_sync(full, in2, o);
+                            if (lane >= o) in2 += v;
+                        }
+                        const int t2 = __shfl_sync(full, in2, 31);
+                        int wb2 = 0;
+                        if (lane == 0 && t2) wb2 = atomicAdd(&S.n, t2);
+                        int ps = __shfl_sync(full, wb2, 0) + in2 - mn;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (i + e < cu && scv[e] >= cut) keep(ps++, slv[e]);
                     }
                 }
             }
