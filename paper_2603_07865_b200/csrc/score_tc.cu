@@ -20,6 +20,13 @@
 // an atomicMax per query, so the emission threshold tightens as the scan proceeds. The exact
 // fp64 rescoring (exact.cu) then decides ties and order bit-exactly.
 #include <numeric>
+
+#ifndef SW_EPI_PAIRS
+// 1: epilogue TMEM stages of two 32-column chunks (64 columns in flight, 225 registers).
+// Measured slower than one chunk per stage (0.729 vs 0.713 ms at config 3): the drain is not
+// bound by the TMEM round trips.
+#define SW_EPI_PAIRS 0
+#endif
 #include <type_traits>
 
 #include "ptx.cuh"
@@ -563,8 +570,34 @@ __global__ void __launch_bounds__(THREADS, 1)
                 __syncwarp();
             };
             if (p.experiment != 1 && p.experiment != 2) {
-                constexpr int NCH = TBN / 32;  // even
+                constexpr int NCH = TBN / 32;
                 const uint32_t tb = lane_base + acc * TBN;
+#if SW_EPI_PAIRS
+                // two 32-column chunks per stage, two stages: 64 columns in flight while 64
+                // are examined, so a tile costs NCH / 2 TMEM round trips instead of NCH
+                static_assert(NCH % 4 == 0, "pairs of stages");
+                uint32_t ra[32], ra2[32], rb[32], rb2[32];
+                __syncwarp();
+                ptx::tmem_ld32(tb, ra);
+                ptx::tmem_ld32(tb + 32, ra2);
+                ptx::tmem_ld_wait();
+#pragma unroll 1
+                for (int c = 0; c < NCH; c += 4) {
+                    ptx::tmem_ld32(tb + (c + 2) * 32, rb);
+                    ptx::tmem_ld32(tb + (c + 3) * 32, rb2);
+                    examine(ra, c);
+                    examine(ra2, c + 1);
+                    ptx::tmem_ld_wait();
+                    if (c + 4 < NCH) {
+                        ptx::tmem_ld32(tb + (c + 4) * 32, ra);
+                        ptx::tmem_ld32(tb + (c + 5) * 32, ra2);
+                    }
+                    examine(rb, c + 2);
+                    examine(rb2, c + 3);
+                    ptx::tmem_ld_wait();
+                }
+#else
+                static_assert(NCH % 2 == 0, "even");
                 uint32_t ra[32], rb[32];
                 __syncwarp();
                 ptx::tmem_ld32(tb, ra);
@@ -578,6 +611,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     examine(rb, c + 1);
                     ptx::tmem_ld_wait();
                 }
+#endif
             }
             ptx::tc_fence_before();
             __syncwarp();
