@@ -85,6 +85,7 @@ struct FinSmem {
     HitRec rec[kMaxTopK];  // mirror of the hit records for the select stage
     double phi[SPHI][8];   // gater block sums of the best row of candidates i < SPHI (phase B)
     int32_t sel_idx[kMaxTopK];
+    int32_t pre[kMaxSlices + 1];  // exclusive prefix of the slices' emission counts (phase A)
     float cut;
     int n, ovf, nh, emitted;
     long long t_ta, t_sync;
@@ -176,6 +177,42 @@ __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
     return s;
 }
 
+// k-th largest (duplicates counted) of the m <= 32 NV values tk[(i / k) * kMaxTopK + i % k],
+// by descending distinct values: a warp max (REDUX) of the keys below the previous one, then a
+// warp count of its copies. -inf when fewer than k values are real. Warp-uniform result.
+template <int NV>
+__device__ __forceinline__ float kth_largest(const float* __restrict__ tk, int m, int k, int lane) {
+    const unsigned full = 0xffffffffu;
+    const bool pow2 = (k & (k - 1)) == 0;
+    const int lk = __ffs(k) - 1;
+    uint32_t key[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+        const int i = lane + 32 * u;
+        key[u] = 0u;  // below every real score's key
+        if (i < m) {
+            const int sl = pow2 ? i >> lk : i / k;
+            const float v = tk[sl * kMaxTopK + (i - sl * k)];
+            if (v != -INFINITY) key[u] = f2ord(v);
+        }
+    }
+    uint32_t prev = 0xFFFFFFFFu;
+    int total = 0;
+    for (;;) {
+        uint32_t lm = 0u;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) lm = max(lm, key[u] < prev ? key[u] : 0u);
+        const uint32_t cur = __reduce_max_sync(full, lm);
+        if (cur == 0u) return -INFINITY;  // fewer than k valid entries: keep everything
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) c += key[u] == cur ? 1 : 0;
+        total += (int)__reduce_add_sync(full, (unsigned)c);
+        prev = cur;
+        if (total >= k) return ord2f(cur);
+    }
+}
+
 template <bool RING>
 __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
     extern __shared__ double qd[];  // query as doubles, Df
@@ -195,49 +232,34 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
 
     // ---------------- A: certified candidate set
     if (!p.implicit_all) {
-        // slice sizes of this warp's chunks c = warp + NWARP * j (lane j) for the first pass,
-        // loaded before the cut is known so the round trip overlaps warp 0's T_a selection
-        const int nloc = (p.n_chunks - warp + NWARP - 1) / NWARP;
-        const int raw0 = lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + warp + NWARP * lane] : 0;
+        if (warp == 1) {
+            // meanwhile: exclusive prefix of the slices' emission counts (capped at the slice
+            // capacity; an overflowing slice flags the query) into shared memory
+            int carry = 0;
+            for (int j0 = 0; j0 < p.n_chunks; j0 += 32) {
+                const int j = j0 + lane;
+                const int raw = j < p.n_chunks ? p.slice_cnt[(int64_t)b * p.n_chunks + j] : 0;
+                if (__any_sync(full, raw > p.cap_local) && lane == 0) S.ovf = 1;
+                const int c = min(raw, p.cap_local);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(full, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                if (j < p.n_chunks) S.pre[j] = carry + incl - c;
+                carry += __shfl_sync(full, incl, 31);
+            }
+            if (lane == 0) S.pre[p.n_chunks] = carry;
+        }
         if (warp == 0) {  // T_a over the union of the scoring CTAs' final lists
             const int m = p.n_chunks * p.k;
             const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
-            constexpr int NV = 16;  // m <= 512 held in registers
             float kth = -INFINITY;
-            if (m <= 32 * NV) {
-                // k-th largest (duplicates counted) by descending distinct values: a warp max
-                // (REDUX) of the keys below the previous one, then a warp count of its copies
-                const bool pow2 = (p.k & (p.k - 1)) == 0;
-                const int lk = __ffs(p.k) - 1;
-                uint32_t key[NV];
-#pragma unroll
-                for (int u = 0; u < NV; ++u) {
-                    const int i = lane + 32 * u;
-                    key[u] = 0u;  // below every real score's key
-                    if (i < m) {
-                        const int sl = pow2 ? i >> lk : i / p.k;
-                        const float v = tk[sl * kMaxTopK + (i - sl * p.k)];
-                        if (v != -INFINITY) key[u] = f2ord(v);
-                    }
-                }
-                uint32_t prev = 0xFFFFFFFFu;
-                int total = 0;
-                for (;;) {
-                    uint32_t lm = 0u;
-#pragma unroll
-                    for (int u = 0; u < NV; ++u) lm = max(lm, key[u] < prev ? key[u] : 0u);
-                    const uint32_t cur = __reduce_max_sync(full, lm);
-                    if (cur == 0u) break;  // fewer than k valid entries: keep everything
-                    int c = 0;
-#pragma unroll
-                    for (int u = 0; u < NV; ++u) c += key[u] == cur ? 1 : 0;
-                    total += (int)__reduce_add_sync(full, (unsigned)c);
-                    prev = cur;
-                    if (total >= p.k) {
-                        kth = ord2f(cur);
-                        break;
-                    }
-                }
+            if (m <= 32 * 16) {
+                kth = kth_largest<16>(tk, m, p.k, lane);
+            } else if (m <= 32 * 40) {  // 148 slices x k = 8 (single-query batches)
+                kth = kth_largest<40>(tk, m, p.k, lane);
             } else {  // very wide grids (small batches): 64-bit (value, index) keys from L2
                 unsigned long long prev = ~0ull;
                 for (int r = 0; r < p.k; ++r) {
@@ -265,9 +287,9 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
         const long long t_sync = clock64();
         const float cut = S.cut;
         const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
-        int emitted = 0;
         // keeps one candidate: shared list (+ global spill list) and an L2 prefetch of its rows
-        auto keep = [&](int pos, int slot) {
+        auto keep = [&](int slot) {
+            const int pos = atomicAdd(&S.n, 1);  // list order is irrelevant (phase C sorts)
             if (pos < SMAXC) S.slot[pos] = slot;
             p.list[base + pos] = slot;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
@@ -275,109 +297,41 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
                          "r"((uint32_t)row_bytes)
                          : "memory");
         };
-        for (int j0 = 0; j0 < nloc; j0 += 32) {
-            const int cj = warp + NWARP * (j0 + lane);
-            const int raw = j0 == 0 ? raw0
-                                    : (j0 + lane < nloc ? p.slice_cnt[(int64_t)b * p.n_chunks + cj] : 0);
-            if (__any_sync(full, raw > p.cap_local) && lane == 0) S.ovf = 1;
-            const int my_cnt = min(raw, p.cap_local);
-            const int jn = min(32, nloc - j0);
-            // CH chunks per round, all their first-128-entry score segments in flight at once;
-            // a lane's pass bits (chunk u, element e -> bit 4u + e) are compacted with ONE warp
-            // scan + shared atomic per round, then only the passing slots are loaded
-            constexpr int CH = 8;
-            for (int jg = 0; jg < jn; jg += CH) {
-                float4 sc[CH];
-                int cnt[CH];
-                int64_t src[CH];
-#pragma unroll
-                for (int u = 0; u < CH; ++u) {
-                    const int j = jg + u;
-                    cnt[u] = __shfl_sync(full, my_cnt, j < jn ? j : 0);
-                    if (j >= jn) cnt[u] = 0;
-                    src[u] = base + (int64_t)(warp + NWARP * (j0 + j)) * p.cap_local;
-                    sc[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                    if (4 * lane < cnt[u])
-                        sc[u] = *reinterpret_cast<const float4*>(p.cand_score + src[u] + 4 * lane);
-                }
-                uint32_t bits = 0u;
-#pragma unroll
-                for (int u = 0; u < CH; ++u) {
-                    emitted += cnt[u];
-                    const float v4[4] = {sc[u].x, sc[u].y, sc[u].z, sc[u].w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (4 * lane + e < cnt[u] && v4[e] >= cut) bits |= 1u << (4 * u + e);
-                }
-                const int mine = __popc(bits);
-                int incl = mine;  // warp inclusive scan of per-lane pass counts
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(full, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const int tot = __shfl_sync(full, incl, 31);
-                int wbase = 0;
-                if (lane == 0 && tot) wbase = atomicAdd(&S.n, tot);
-                int pos = __shfl_sync(full, wbase, 0) + incl - mine;
-                while (bits) {  // up to 4 slot loads in flight per lane
-                    int sl4[4];
-                    int nb = 0;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        sl4[q] = -1;
-                        if (bits) {
-                            const int bit = __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const int64_t sb =  // src[bit >> 2] without a local-memory array
-                                base + (int64_t)(warp + NWARP * (j0 + jg + (bit >> 2))) * p.cap_local;
-                            sl4[q] = p.cand_slot[sb + 4 * lane + (bit & 3)];
-                            ++nb;
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (q < nb) keep(pos++, sl4[q]);
-                }
-                // rare: chunks with more than 128 emitted entries (count and base recomputed,
-                // so no register array is indexed dynamically)
-#pragma unroll 1
-                for (int u = 0; u < CH && jg + u < jn; ++u) {
-                    const int cu = __shfl_sync(full, my_cnt, jg + u);
-                    if (cu <= 128) continue;
-                    const int64_t su = base + (int64_t)(warp + NWARP * (j0 + jg + u)) * p.cap_local;
-                    for (int i0 = 128; i0 < cu; i0 += 128) {
-                        const int i = i0 + 4 * lane;
-                        float4 sv = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                        int4 lv = make_int4(0, 0, 0, 0);
-                        if (i < cu) {
-                            sv = *reinterpret_cast<const float4*>(p.cand_score + su + i);
-                            lv = *reinterpret_cast<const int4*>(p.cand_slot + su + i);
-                        }
-                        const float scv[4] = {sv.x, sv.y, sv.z, sv.w};
-                        const int slv[4] = {lv.x, lv.y, lv.z, lv.w};
-                        int mn = 0;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) mn += (i + e < cu && scv[e] >= cut) ? 1 : 0;
-                        int in2 = mn;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int v = __shfl_up_sync(full, in2, o);
-                            if (lane >= o) in2 += v;
-                        }
-                        const int t2 = __shfl_sync(full, in2, 31);
-                        int wb2 = 0;
-                        if (lane == 0 && t2) wb2 = atomicAdd(&S.n, t2);
-                        int ps = __shfl_sync(full, wb2, 0) + in2 - mn;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (i + e < cu && scv[e] >= cut) keep(ps++, slv[e]);
-                    }
-                }
+        // The emitted entries of all slices as one flat sequence (slice-major): thread t walks
+        // its contiguous share [t L, (t + 1) L), slice by slice, 8 score loads in flight, and
+        // loads the slot index only for entries that pass the cut.
+        const int total = S.pre[p.n_chunks];
+        const int L = (total + FT - 1) / FT;
+        int f = min(total, t * L);
+        const int fend = min(total, f + L);
+        int sl = 0;  // slice containing f: the last slice with pre[sl] <= f
+        {
+            int lo = 0, hi = p.n_chunks - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (S.pre[mid] <= f) lo = mid; else hi = mid - 1;
             }
+            sl = lo;
         }
-        if (lane == 0) atomicAdd(&S.emitted, emitted);  // every lane summed the same counts
-        if (t == 0) S.t_sync = t_sync;
+        while (f < fend) {
+            while (S.pre[sl + 1] <= f) ++sl;  // skip empty slices
+            const int seg_end = min(fend, S.pre[sl + 1]);
+            const int64_t src = base + (int64_t)sl * p.cap_local - S.pre[sl];  // + flat index
+            for (; f < seg_end; f += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = f + u < seg_end ? p.cand_score[src + f + u] : -INFINITY;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)  // (cut may be -inf: keep every real entry)
+                    if (f + u < seg_end && v[u] >= cut) keep(p.cand_slot[src + f + u]);
+            }
+            f = seg_end;
+        }
+        const int emitted = total;
+        if (t == 0) {
+            S.t_sync = t_sync;
+            S.emitted = emitted;
+        }
     } else if (t == 0) {
         S.n = (int)p.n_slots;
     }
