@@ -69,6 +69,7 @@ struct FinishParams {
     dev::SelParams sp;
     const sw_request* reqs;
     sw_choice* out;
+    int pf_lines;             // EXPERIMENT
     int ivf;                  // IVF mode: rows outside the query's probed lists do not count
     const int16_t* row_list;  // [rows] list of each stored row
     const uint8_t* prank;     // [B][kMaxCentroids] probe rank of each list (255: not probed)
@@ -127,52 +128,72 @@ __device__ __forceinline__ double chain_dot(const float4* __restrict__ rp,
 // chain_dot that also produces the gater's 8 block sums (gater.cpp:18-26: block j is the
 // sequential fp64 sum over [j D/8, (j+1) D/8) starting from 0) as a second, independent chain;
 // valid when D == Df and D % 32 == 0 (blocks are whole float4 runs).
+// The loops are ROLLED (one PF-float4 body, ~130 instructions): a fully unrolled 512-step
+// chain is ~32 KB of straight-line code per instantiation that each warp executes once, so
+// every instruction fetch missed the instruction cache (measured: phase B 41K cycles cold vs
+// 15K with the code cached).
 template <int N4, int PF>
 __device__ __forceinline__ double chain_dot_phi(const float4* __restrict__ rp,
                                                 const double* __restrict__ qd, double (&phi)[8]) {
     constexpr int BS4 = N4 / 8;
+    static_assert(BS4 % PF == 0, "ring period divides a block");
     float4 ring[PF];
 #pragma unroll
-    for (int i = 0; i < PF; ++i) ring[i] = __ldg(rp + i);
-    double s = 0.0, bsum = 0.0;
+    for (int u = 0; u < PF; ++u) ring[u] = __ldg(rp + u);
 #pragma unroll
-    for (int i = 0; i < N4; ++i) {
-        const float4 x = ring[i % PF];
-        if (i + PF < N4) ring[i % PF] = __ldg(rp + i + PF);
-        const double x0 = x.x, x1 = x.y, x2 = x.z, x3 = x.w;
-        s = fma(qd[4 * i + 0], x0, s);
-        bsum = fma(qd[4 * i + 0], x0, bsum);
-        s = fma(qd[4 * i + 1], x1, s);
-        bsum = fma(qd[4 * i + 1], x1, bsum);
-        s = fma(qd[4 * i + 2], x2, s);
-        bsum = fma(qd[4 * i + 2], x2, bsum);
-        s = fma(qd[4 * i + 3], x3, s);
-        bsum = fma(qd[4 * i + 3], x3, bsum);
-        if ((i + 1) % BS4 == 0) {
-            phi[(i + 1) / BS4 - 1] = bsum;
-            bsum = 0.0;
+    for (int j = 0; j < 8; ++j) phi[j] = 0.0;
+    double s = 0.0;
+#pragma unroll 1
+    for (int blk = 0; blk < 8; ++blk) {
+        double bsum = 0.0;
+#pragma unroll 1
+        for (int i0 = blk * BS4; i0 < (blk + 1) * BS4; i0 += PF) {
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const int i = i0 + u;
+                const float4 x = ring[u];
+                if (i + PF < N4) ring[u] = __ldg(rp + i + PF);
+                const double2 a = reinterpret_cast<const double2*>(qd)[2 * i];
+                const double2 b = reinterpret_cast<const double2*>(qd)[2 * i + 1];
+                const double x0 = x.x, x1 = x.y, x2 = x.z, x3 = x.w;
+                s = fma(a.x, x0, s);
+                bsum = fma(a.x, x0, bsum);
+                s = fma(a.y, x1, s);
+                bsum = fma(a.y, x1, bsum);
+                s = fma(b.x, x2, s);
+                bsum = fma(b.x, x2, bsum);
+                s = fma(b.y, x3, s);
+                bsum = fma(b.y, x3, bsum);
+            }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) phi[j] = j == blk ? bsum : phi[j];  // static register index
     }
     return s;
 }
 
 __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
                                                 const double* __restrict__ qd, int n4) {
-    switch (n4) {
-        case 128: return chain_dot<128, 16>(rp, qd);
-        case 64: return chain_dot<64, 16>(rp, qd);
-        case 32: return chain_dot<32, 16>(rp, qd);
-        case 16: return chain_dot<16, 16>(rp, qd);
-        default: break;
-    }
+    // rolled like chain_dot_phi (instruction-cache footprint), 8 float4 loads in flight
+    constexpr int PF = 8;
+    float4 ring[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) ring[u] = u < n4 ? __ldg(rp + u) : make_float4(0.f, 0.f, 0.f, 0.f);
     double s = 0.0;
-#pragma unroll 4
-    for (int i = 0; i < n4; ++i) {
-        const float4 x = __ldg(rp + i);
-        s = fma(qd[4 * i + 0], (double)x.x, s);
-        s = fma(qd[4 * i + 1], (double)x.y, s);
-        s = fma(qd[4 * i + 2], (double)x.z, s);
-        s = fma(qd[4 * i + 3], (double)x.w, s);
+#pragma unroll 1
+    for (int i0 = 0; i0 < n4; i0 += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = i0 + u;
+            if (i < n4) {
+                const float4 x = ring[u];
+                if (i + PF < n4) ring[u] = __ldg(rp + i + PF);
+                s = fma(qd[4 * i + 0], (double)x.x, s);
+                s = fma(qd[4 * i + 1], (double)x.y, s);
+                s = fma(qd[4 * i + 2], (double)x.z, s);
+                s = fma(qd[4 * i + 3], (double)x.w, s);
+            }
+        }
     }
     return s;
 }
@@ -287,15 +308,21 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
         const long long t_sync = clock64();
         const float cut = S.cut;
         const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
+        const int pf_lines = p.pf_lines;
         // keeps one candidate: shared list (+ global spill list) and an L2 prefetch of its rows
         auto keep = [&](int slot) {
             const int pos = atomicAdd(&S.n, 1);  // list order is irrelevant (phase C sorts)
             if (pos < SMAXC) S.slot[pos] = slot;
             p.list[base + pos] = slot;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                             p.rows + (int64_t)slot * p.Rp * p.Df),
-                         "r"((uint32_t)row_bytes)
-                         : "memory");
+            const char* rp = reinterpret_cast<const char*>(p.rows + (int64_t)slot * p.Rp * p.Df);
+            if (pf_lines) {  // EXPERIMENT: per-line prefetches through the SM's load path
+                for (int64_t o = 0; o < row_bytes; o += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + o));
+            } else {
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp),
+                             "r"((uint32_t)row_bytes)
+                             : "memory");
+            }
         };
         // The emitted entries of all slices as one flat sequence (slice-major): thread t walks
         // its contiguous share [t L, (t + 1) L), slice by slice, 8 score loads in flight, and
@@ -382,10 +409,10 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
                 const float4* rp4 = reinterpret_cast<const float4*>(p.rows + row * p.Df);
                 if (fast_phi) {
                     switch (p.D) {
-                        case 512: s = chain_dot_phi<128, 16>(rp4, qd, phi); break;
-                        case 256: s = chain_dot_phi<64, 16>(rp4, qd, phi); break;
-                        case 128: s = chain_dot_phi<32, 16>(rp4, qd, phi); break;
-                        default: s = chain_dot_phi<16, 16>(rp4, qd, phi); break;
+                        case 512: s = chain_dot_phi<128, 8>(rp4, qd, phi); break;
+                        case 256: s = chain_dot_phi<64, 8>(rp4, qd, phi); break;
+                        case 128: s = chain_dot_phi<32, 4>(rp4, qd, phi); break;
+                        default: s = chain_dot_phi<16, 2>(rp4, qd, phi); break;
                     }
                 } else {
                     s = chain_dot_any(rp4, qd, p.Df >> 2);
@@ -672,6 +699,8 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.row_list = c.row_list;
     p.prank = c.prank;
     c.last_ivf = ivf;
+    static const int pfl = getenv("SW_PF_LINES") ? 1 : 0;
+    p.pf_lines = pfl;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
         static const bool ring = [] {
@@ -687,6 +716,11 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
             SW_CUDA(cudaFuncSetAttribute(k_finish<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = smem;
+        }
+        static const bool twice = getenv("SW_FINISH_TWICE") != nullptr;  // EXPERIMENT
+        if (twice) {
+            FinishParams p2 = p;
+            k_finish<false><<<B, FT, smem, st>>>(p2);
         }
         if (ring)
             k_finish<true><<<B, FT, smem, st>>>(p);
