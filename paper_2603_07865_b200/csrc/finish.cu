@@ -69,7 +69,6 @@ struct FinishParams {
     dev::SelParams sp;
     const sw_request* reqs;
     sw_choice* out;
-    int pf_lines;             // EXPERIMENT
     int ivf;                  // IVF mode: rows outside the query's probed lists do not count
     const int16_t* row_list;  // [rows] list of each stored row
     const uint8_t* prank;     // [B][kMaxCentroids] probe rank of each list (255: not probed)
@@ -234,15 +233,18 @@ __device__ __forceinline__ float kth_largest(const float* __restrict__ tk, int m
     }
 }
 
-template <bool RING>
-__global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
+// FTT threads per query CTA: 64 (2 warps, 7 CTAs/SM: a 1024-query batch is one wave) or, for
+// small batches whose per-query latency is the metric, 256 (the flat candidate walk and the
+// enrichment spread over 8 warps).
+template <bool RING, int FTT = FT>
+__global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishParams p) {
     extern __shared__ double qd[];  // query as doubles, Df
     __shared__ FinSmem S;
     const int b = blockIdx.x;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const unsigned full = 0xffffffffu;
     const float* qb = p.q + (int64_t)b * p.D;
-    for (int d = t; d < p.Df; d += FT) qd[d] = d < p.D ? (double)qb[d] : 0.0;
+    for (int d = t; d < p.Df; d += FTT) qd[d] = d < p.D ? (double)qb[d] : 0.0;
     if (t == 0) {
         S.n = 0;
         S.ovf = 0;
@@ -308,27 +310,21 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
         const long long t_sync = clock64();
         const float cut = S.cut;
         const int64_t row_bytes = (int64_t)p.Rp * p.Df * 4;
-        const int pf_lines = p.pf_lines;
         // keeps one candidate: shared list (+ global spill list) and an L2 prefetch of its rows
         auto keep = [&](int slot) {
             const int pos = atomicAdd(&S.n, 1);  // list order is irrelevant (phase C sorts)
             if (pos < SMAXC) S.slot[pos] = slot;
             p.list[base + pos] = slot;
             const char* rp = reinterpret_cast<const char*>(p.rows + (int64_t)slot * p.Rp * p.Df);
-            if (pf_lines) {  // EXPERIMENT: per-line prefetches through the SM's load path
-                for (int64_t o = 0; o < row_bytes; o += 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + o));
-            } else {
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp),
-                             "r"((uint32_t)row_bytes)
-                             : "memory");
-            }
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp),
+                         "r"((uint32_t)row_bytes)
+                         : "memory");
         };
         // The emitted entries of all slices as one flat sequence (slice-major): thread t walks
         // its contiguous share [t L, (t + 1) L), slice by slice, 8 score loads in flight, and
         // loads the slot index only for entries that pass the cut.
         const int total = S.pre[p.n_chunks];
-        const int L = (total + FT - 1) / FT;
+        const int L = (total + FTT - 1) / FTT;
         int f = min(total, t * L);
         const int fend = min(total, f + L);
         int sl = 0;  // slice containing f: the last slice with pre[sl] <= f
@@ -377,7 +373,7 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
     float* ring = RING ? reinterpret_cast<float*>(qd + p.Df) + (size_t)warp * NST * 32 * SP
                        : nullptr;
     const int nch = (p.Df + SC - 1) / SC;
-    for (int64_t g0 = (int64_t)warp * 32; g0 < items; g0 += FT) {
+    for (int64_t g0 = (int64_t)warp * 32; g0 < items; g0 += FTT) {
         const int64_t w = g0 + lane;
         const int64_t i = w >> p.logRp;
         const int r = (int)(w & (p.Rp - 1));
@@ -556,7 +552,7 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
 
     // ---------------- D: enrichment (8 threads per hit): s_neg + gater block sums
     HitRec* hb = p.hits + (int64_t)b * kMaxTopK;
-    for (int tt = t; tt < nh * 8; tt += FT) {
+    for (int tt = t; tt < nh * 8; tt += FTT) {
         const int h = tt >> 3, j = tt & 7;
         const int64_t row = S.sel_slot[h] * p.Rp + S.sel_row[h];
         const float* rp = p.rows + row * p.Df;
@@ -598,7 +594,7 @@ __global__ void __launch_bounds__(FT, 7) k_finish(const FinishParams p) {
         const int nw = nh * (int)(sizeof(HitRec) / 16);
         const int4* srcw = reinterpret_cast<const int4*>(S.rec);
         int4* dstw = reinterpret_cast<int4*>(hb);
-        for (int i = t; i < nw; i += FT) dstw[i] = srcw[i];
+        for (int i = t; i < nw; i += FTT) dstw[i] = srcw[i];
     }
     const long long t_d = clock64();
 
@@ -699,8 +695,6 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.row_list = c.row_list;
     p.prank = c.prank;
     c.last_ivf = ivf;
-    static const int pfl = getenv("SW_PF_LINES") ? 1 : 0;
-    p.pf_lines = pfl;
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
         static const bool ring = [] {
@@ -715,15 +709,14 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             SW_CUDA(cudaFuncSetAttribute(k_finish<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            SW_CUDA(cudaFuncSetAttribute(k_finish<false, 256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = smem;
-        }
-        static const bool twice = getenv("SW_FINISH_TWICE") != nullptr;  // EXPERIMENT
-        if (twice) {
-            FinishParams p2 = p;
-            k_finish<false><<<B, FT, smem, st>>>(p2);
         }
         if (ring)
             k_finish<true><<<B, FT, smem, st>>>(p);
+        else if (B <= 64)
+            k_finish<false, 256><<<B, 256, smem, st>>>(p);
         else
             k_finish<false><<<B, FT, smem, st>>>(p);
     }
