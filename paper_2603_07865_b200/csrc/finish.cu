@@ -493,7 +493,31 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
     const long long t_b = clock64();
 
     // ---------------- C: top-k by (sim desc, id asc) (index.cpp:320-324), warp 0
-    if (warp == 0) {
+    if (warp == 0 && n <= 32) {
+        // one candidate per lane: its rank is the number of lanes ordered before it (31
+        // independent shuffle rounds, no dependent reduction chain); ranks < k are the hits.
+        // ids are unique, so ranks are distinct.
+        const bool v = lane < n && S.ex[lane] != -DBL_MAX;  // invalid slot / entry without rows
+        const double sv = v ? S.ex[lane] : -DBL_MAX;
+        const uint64_t id = v ? S.id[lane] : ~0ull;
+        int rank = 0;
+#pragma unroll 4
+        for (int r = 1; r < 32; ++r) {
+            const int j = (lane + r) & 31;
+            const double os = __shfl_sync(full, sv, j);
+            const uint64_t oid = __shfl_sync(full, id, j);
+            const bool ov = __shfl_sync(full, v, j);
+            rank += (ov && before(os, oid, sv, id)) ? 1 : 0;
+        }
+        if (v && rank < p.k) {
+            S.sel_slot[rank] = S.slot[lane];
+            S.sel_row[rank] = S.brow[lane];
+            S.sel_sim[rank] = sv;
+            S.sel_idx[rank] = lane;
+        }
+        const int nv = __popc(__ballot_sync(full, v));
+        if (lane == 0) S.nh = min(nv, p.k);
+    } else if (warp == 0) {
         double prev_sim = DBL_MAX;
         uint64_t prev_id = 0;
         bool have_prev = false;
