@@ -69,6 +69,22 @@ def test_search_nonunit_and_near_ties_tc(orc, scale):
     _check_hits(hits, cnt, _arena(c), orc, q, 8)
 
 
+@pytest.mark.parametrize("B", [1, 96])
+@pytest.mark.parametrize("n_dup", [20, 120])
+def test_search_exact_ties_tc(orc, B, n_dup):
+    """Exact ties: n_dup entries share one row bit for bit, so their similarities are equal and
+    the order is by id alone (index.cpp:320-324); 20 duplicates stay inside one warp's rank
+    selection, 120 take the multi-round path; B = 1 runs the 256-thread query CTAs."""
+    c = SynthCache(3000, 128, 1.0, seed=21, clustered=False)
+    c.rows[1:n_dup] = c.rows[0]
+    wc = _cache(c, max_batch=128, tc_always=True)
+    q = perturbed_queries(c, B, scale=0.05, seed=4)
+    q[0] = c.rows[0]
+    for k in (1, 8, 32):
+        hits, cnt = wc.search(q, k)
+        _check_hits(hits, cnt, _arena(c), orc, q, k)
+
+
 def test_search_tc_default_large(orc):
     # 40K entries x 1 row: default mode picks the tcgen05 pre-filter
     c = SynthCache(40000, 512, 1.0, seed=8, clustered=True)
