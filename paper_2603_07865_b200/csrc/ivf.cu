@@ -187,92 +187,73 @@ __global__ void k_farthest(const float* __restrict__ rows, int Df, int D,
     }
 }
 
-// Probe ranking, centroids staged once per block (transposed [D][CP] in smem, conflict-free) and
-// reused for the block's queries: group g of CP threads ranks query b; thread j computes
-// dot(q_b, c_j) sequentially in dimension order, then its rank as below.
+// Probe ranking (index.cpp:295-304), G = 256 / CP queries per block: thread (g, j) computes
+// dot(q_b, c_j) sequentially in dimension order and then its rank = #{i : s_i > s_j or (s_i ==
+// s_j and i < j)}, its position in the reference's partial sort (nprobe first -> probed). The
+// operands are staged in shared memory AS DOUBLES, DH dimensions at a time (centroids
+// transposed [DH][CP + 1], conflict-free for the lane-per-centroid reads; the queries
+// [G][DH]), so the chain is LDS + DFMA only: an fp32 -> fp64 conversion on the chain costs
+// more than the DFMA's latency on this part, and the float staging converted twice per step.
 template <int CP>
 __global__ void __launch_bounds__(256) k_probe_rank_smem(const float* __restrict__ q, int B, int D,
                                                           const float* __restrict__ cent, int Df,
                                                           int C, int np,
                                                           uint8_t* __restrict__ prank,
                                                           uint64_t* __restrict__ pmask) {
-    extern __shared__ float sm[];
-    float* cT = sm;                       // [D][CP]
-    constexpr int G = 256 / CP;           // queries per pass
-    double* sc = reinterpret_cast<double*>(cT + (size_t)D * CP);  // [G][CP]
-    for (int i = threadIdx.x; i < D * CP; i += blockDim.x) {
-        const int d = i / CP, j = i % CP;
-        cT[i] = j < C ? cent[(int64_t)j * Df + d] : 0.0f;
-    }
-    __syncthreads();
+    constexpr int G = 256 / CP;                  // queries per block
+    constexpr int DH = CP <= 64 ? 192 : CP == 128 ? 96 : 48;  // dims per stage (~150 KB)
+    constexpr int CS = CP + 1;                   // padded centroid stride (doubles)
+    extern __shared__ double smd[];
+    double* cT = smd;                            // [DH][CS]
+    double* qs = cT + (size_t)DH * CS;           // [G][DH]
+    double* sc = qs + (size_t)G * DH;            // [G][CP]
     const int g = threadIdx.x / CP, j = threadIdx.x % CP;
-    for (int b0 = blockIdx.x * G; b0 < B; b0 += gridDim.x * G) {
-        const int b = b0 + g;
-        double a = 0.0;
+    const int b = blockIdx.x * G + g;
+    double a = 0.0;
+    for (int d0 = 0; d0 < D; d0 += DH) {
+        const int dn = min(DH, D - d0);
+        __syncthreads();  // previous stage consumed
+        for (int i = threadIdx.x; i < dn * CP; i += 256) {  // coalesced along d
+            const int jj = i / dn, d = i - jj * dn;
+            cT[d * CS + jj] = jj < C ? (double)cent[(int64_t)jj * Df + d0 + d] : 0.0;
+        }
+        for (int i = threadIdx.x; i < G * dn; i += 256) {
+            const int gg = i / dn, d = i - gg * dn;
+            const int bb = blockIdx.x * G + gg;
+            qs[gg * DH + d] = bb < B ? (double)q[(int64_t)bb * D + d0 + d] : 0.0;
+        }
+        __syncthreads();
         if (b < B && j < C) {
-            const float* qb = q + (int64_t)b * D;
-            for (int d = 0; d < D; ++d) a = fma((double)__ldg(qb + d), (double)cT[d * CP + j], a);
+            const double* qg = qs + g * DH;
+#pragma unroll 8
+            for (int d = 0; d < dn; ++d) a = fma(qg[d], cT[d * CS + j], a);
         }
-        sc[g * CP + j] = a;
-        __syncthreads();
-        if (b < B) {
-            uint8_t r = kNotProbed;
-            if (j < C) {
-                int rank = 0;
-                for (int i = 0; i < C; ++i) {
-                    const double si = sc[g * CP + i], sj = sc[g * CP + j];
-                    rank += (si > sj || (si == sj && i < j)) ? 1 : 0;
-                }
-                if (rank < np) r = (uint8_t)rank;
-            }
-            for (int jj = j; jj < kMaxCentroids; jj += CP)
-                prank[(int64_t)b * kMaxCentroids + jj] = jj == j ? r : kNotProbed;
-            const unsigned ballot = __ballot_sync(0xffffffffu, r != kNotProbed);
-            if ((j & 31) == 0) {
-                uint32_t* pm32 = reinterpret_cast<uint32_t*>(pmask + (int64_t)b * 4);
-                pm32[j >> 5] = ballot;
-                if (j == 0)
-                    for (int w = CP / 32; w < 8; ++w) pm32[w] = 0u;
-            }
-        }
-        __syncthreads();
     }
-}
-
-// Probe ranking per query (index.cpp:295-304): thread j computes dot(q, c_j) sequentially, its
-// rank = #{i : s_i > s_j or (s_i == s_j and i < j)} is its position in the partial sort. Writes
-// the rank (255 when not among the first nprobe) and the probed-list bitmask.
-__global__ void k_probe_rank(const float* __restrict__ q, int D, const float* __restrict__ cent,
-                             int Df, int C, int nprobe, uint8_t* __restrict__ prank,
-                             uint64_t* __restrict__ pmask) {
-    __shared__ double s[kMaxCentroids];
-    __shared__ float qs[1024];
-    const int b = blockIdx.x, j = threadIdx.x;
-    const float* qb = q + (int64_t)b * D;
-    for (int d = j; d < D && d < 1024; d += blockDim.x) qs[d] = qb[d];
+    sc[g * CP + j] = a;
     __syncthreads();
-    if (j < C) {
-        const float* c = cent + (int64_t)j * Df;
-        double a = 0.0;
-        for (int d = 0; d < D; ++d) a = fma((double)(d < 1024 ? qs[d] : qb[d]), (double)c[d], a);
-        s[j] = a;
-    }
-    __syncthreads();
-    if (j < kMaxCentroids) {
+    if (b < B) {
         uint8_t r = kNotProbed;
         if (j < C) {
             int rank = 0;
-            for (int i = 0; i < C; ++i) rank += (s[i] > s[j] || (s[i] == s[j] && i < j)) ? 1 : 0;
-            if (rank < nprobe) r = (uint8_t)rank;
+            const double sj = sc[g * CP + j];
+            for (int i = 0; i < C; ++i) {
+                const double si = sc[g * CP + i];
+                rank += (si > sj || (si == sj && i < j)) ? 1 : 0;
+            }
+            if (rank < np) r = (uint8_t)rank;
         }
-        prank[(int64_t)b * kMaxCentroids + j] = r;
+        for (int jj = j; jj < kMaxCentroids; jj += CP)
+            prank[(int64_t)b * kMaxCentroids + jj] = jj == j ? r : kNotProbed;
         const unsigned ballot = __ballot_sync(0xffffffffu, r != kNotProbed);
         if ((j & 31) == 0) {
             uint32_t* pm32 = reinterpret_cast<uint32_t*>(pmask + (int64_t)b * 4);
             pm32[j >> 5] = ballot;
+            if (j == 0)
+                for (int w = CP / 32; w < 8; ++w) pm32[w] = 0u;
         }
     }
 }
+
 
 // rows [nrows[slot], Rp) of each slot belong to no list (pad rows repeat row 0 in the bf16
 // shadow; they must never make an entry eligible through a stale list id)
@@ -828,26 +809,26 @@ bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st) {
     const int np = std::min(c.ivf_nprobe, c.ivf_C);
     if (np >= c.ivf_C) return false;  // every list probed == exhaustive
     const int cp = c.ivf_C <= 32 ? 32 : c.ivf_C <= 64 ? 64 : c.ivf_C <= 128 ? 128 : 256;
-    const size_t smem = sizeof(float) * (size_t)c.D * cp + sizeof(double) * 256;
-    if (smem <= 200 * 1024) {
+    {
+        const int G = 256 / cp, DH = cp <= 64 ? 192 : cp == 128 ? 96 : 48;
+        const size_t smem = sizeof(double) * ((size_t)DH * (cp + 1) + (size_t)G * DH + 256);
+        // one flag per instantiation: the four kernels share a function-pointer type, so a
+        // static inside this (generic) lambda would be shared by all of them
+        static bool attr_set[4] = {false, false, false, false};
+        const int ai = cp == 32 ? 0 : cp == 64 ? 1 : cp == 128 ? 2 : 3;
         auto launch = [&](auto kern) {
-            static bool attr = false;
-            if (!attr) {
+            if (!attr_set[ai]) {
                 SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024));
-                attr = true;
+                attr_set[ai] = true;
             }
-            const int grid = (int)std::min<int64_t>(148, (B + 256 / cp - 1) / (256 / cp));
-            kern<<<grid, 256, smem, st>>>(d_q, B, c.D, c.cent, c.Df, c.ivf_C, np, c.prank,
-                                          c.pmask);
+            kern<<<(B + G - 1) / G, 256, smem, st>>>(d_q, B, c.D, c.cent, c.Df, c.ivf_C, np,
+                                                     c.prank, c.pmask);
         };
         if (cp == 32) launch(k_probe_rank_smem<32>);
         else if (cp == 64) launch(k_probe_rank_smem<64>);
         else if (cp == 128) launch(k_probe_rank_smem<128>);
         else launch(k_probe_rank_smem<256>);
-    } else {
-        k_probe_rank<<<B, kMaxCentroids, 0, st>>>(d_q, c.D, c.cent, c.Df, c.ivf_C, np, c.prank,
-                                                  c.pmask);
     }
     SW_CUDA(cudaGetLastError());
     return true;
