@@ -77,6 +77,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
+// Relaxed remote arrive: no memory ordering. The release form above compiles to MEMBAR.ALL.CTA +
+// MEMBAR.ALL.GPU + ERRBAR before the arrive, i.e. it drains every outstanding global access of
+// the warp. For "the accumulator was read" signals nothing in memory needs ordering: the
+// tcgen05.ld data are already in registers (tcgen05.wait::ld completed in program order).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
