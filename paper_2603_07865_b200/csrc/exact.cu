@@ -30,9 +30,10 @@ __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
     if (b >= B) return;
     for (int i = threadIdx.x; i < kMaxSlices; i += blockDim.x)
         top1[(int64_t)b * kMaxSlices + i] = f2ord(-INFINITY);
-    // the request's selector draw Rng(derive_seed(seed, id, 2)).uniform() (pipeline.cpp:211),
-    // computed here by one lane of warp 1 so its 156-step MT seeding overlaps the conversion
-    if (req && threadIdx.x == 32) u_draw[b] = dev::uniform_draw(dev::derive_seed(seed, req[b].id, 2, 0));
+    // (the request's selector draw is computed in k_finish, overlapping its phase A)
+    (void)req;
+    (void)seed;
+    (void)u_draw;
     __shared__ double red[3][32];
     const float* qb = q + (int64_t)b * D;
     double nn = 0.0, dd = 0.0, bb = 0.0;

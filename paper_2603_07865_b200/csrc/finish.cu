@@ -89,6 +89,7 @@ struct FinSmem {
     float cut;
     int n, ovf, nh, emitted;
     long long t_ta, t_sync;
+    double u;  // the request's selector draw (computed by warp 1 during phase A)
 };
 
 __device__ __forceinline__ bool before(double as, uint64_t aid, double bs, uint64_t bid) {
@@ -252,6 +253,10 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
     }
     const int64_t base = (int64_t)b * kCandCap;
     const long long t_start = clock64();
+    // the request's selector draw Rng(derive_seed(seed, id, 2)).uniform() (pipeline.cpp:211):
+    // a 156-step serial MT64 seeding, run by one lane of warp 1 while warp 0 selects T_a
+    if (p.do_select && t == 32)
+        S.u = dev::uniform_draw(dev::derive_seed(p.sp.seed, p.reqs[b].id, 2, 0));
 
     // ---------------- A: certified candidate set
     if (!p.implicit_all) {
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
 
     // ---------------- E: gate + select + Skip Gater + t* (warp 0)
     if (p.do_select && warp == 0) {  // (phase D covered 8 hits x 8 block sums in one pass)
-        const sw_choice c = dev::select_warp(S.rec, nh_code, p.u_draw[b], p.reqs[b], p.sp, lane);
+        const sw_choice c = dev::select_warp(S.rec, nh_code, S.u, p.reqs[b], p.sp, lane);
         if (lane == 0) p.out[b] = c;
     }
     if (t == 0) {
