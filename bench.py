@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-vocoder", action="store_true",
                    help="skip the phase-vocoder (time_stretch) side measurement")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="run align+noise on the planning stream (no cross-batch overlap)")
     p.add_argument("--ivf", default=None, metavar="C,NPROBE",
                    help="IVF mode (the reference's default index: 64,8): GPU k-means rebuild of "
                         "the synthetic cache, then probe-restricted warm starts")
@@ -349,10 +351,35 @@ def main():
 
     sharded = world > 1 or args.sharded_path
 
+    # A step = sw_plan (prep -> score -> finish) on `stream`, then sw_align_noise of the same
+    # batch on a second stream: batch i's align+noise runs under batch i+1's scoring kernel,
+    # which leaves registers and threads free on every SM (--no-overlap: one stream)
+    overlap = not args.no_overlap and not sharded
+    if overlap:
+        ch_ring = [torch.empty_like(choices) for _ in range(2)]
+        out_ring = [torch.empty_like(out) for _ in range(2)]
+        a_stream = torch.cuda.Stream(dev)
+        a_ev = [torch.cuda.Event() for _ in range(2)]
+        a_done = [torch.cuda.Event() for _ in range(2)]
+        a_used = [False, False]
+
     def step(i):
         q = qpool[i % n_pool]
         r = reqs[i % n_pool]
-        if not sharded:
+        if not sharded and overlap:
+            j = i % 2
+            if a_used[j]:
+                stream.wait_event(a_done[j])  # align(i - 2) has read ch_ring[j]
+            _lib.check(L_.sw_plan(wc._h, q.data_ptr(), r.data_ptr(), B, 1, Cc.byref(csel),
+                                  Cc.byref(cpol), ch_ring[j].data_ptr(), sp), "sw_plan")
+            a_ev[j].record(stream)
+            a_stream.wait_event(a_ev[j])
+            _lib.check(L_.sw_align_noise(wc._h, ch_ring[j].data_ptr(), r.data_ptr(), B, None, 1234,
+                                         out_ring[j].data_ptr(), T_, a_stream.cuda_stream),
+                       "sw_align_noise")
+            a_done[j].record(a_stream)
+            a_used[j] = True
+        elif not sharded:
             _lib.check(L_.sw_warmstart(wc._h, q.data_ptr(), r.data_ptr(), B, 1, Cc.byref(csel),
                                        Cc.byref(cpol), None, 1234, choices.data_ptr(),
                                        out.data_ptr(), T_, sp), "sw_warmstart")
@@ -420,6 +447,10 @@ def main():
     prof_all = wc.profile_read()
     prof = dict(prof_all)
     prof["score_tc"] = prof_timed["score_tc"]  # the roofline kernel: timed-region events
+    last_i = p_steps - 1  # the batch whose choices / requests the side measurements reuse
+    if overlap:
+        choices.copy_(ch_ring[last_i % 2])
+        torch.cuda.synchronize(dev)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cpu" if staged else dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -505,7 +536,7 @@ def main():
         eps_t = torch.randn((B, C_, T_, F_), dtype=torch.float32, device=dev)
         for mode, dptr in (("philox", None), ("eps", eps_t.data_ptr())):
             def al():
-                _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+                _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[last_i % n_pool]
                                              .data_ptr(), B, dptr, 1234, out.data_ptr(), T_, sp),
                            "sw_align_noise")
             for _ in range(3):
@@ -521,12 +552,12 @@ def main():
         del eps_t
         # the reference's alignment (phase vocoder per latent channel) on the same choices
         wc.set_align_mode("vocoder", 128, 32)
-        _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+        _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[last_i % n_pool]
                                      .data_ptr(), B, None, 1234, out.data_ptr(), T_, sp),
                    "sw_align_noise")
         a0.record(stream)
         for _ in range(3):
-            _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[(steps - 1) % n_pool]
+            _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[last_i % n_pool]
                                          .data_ptr(), B, None, 1234, out.data_ptr(), T_, sp),
                        "sw_align_noise")
         a1.record(stream)
@@ -720,7 +751,9 @@ def main():
                    "parallelism": f"entry-sharded x{world}" if sharded else "single",
                    "l2": "inputs larger than L2 (bf16 arena %.0f MB streamed per step)"
                          % (n_rows * D * 2 / 1e6),
-                   "latent_slots": min(args.latent_slots, n_local)},
+                   "latent_slots": min(args.latent_slots, n_local),
+                   "pipelining": ("align+noise of batch i on a second stream, overlapping batch "
+                                  "i+1's scoring" if overlap else "none (one stream)")},
         **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
         "roofline": {"bound": "tensor",
                      "kernel": "k_score_tc (tcgen05.mma %s, TMA)" % (

@@ -283,11 +283,12 @@ int sw_warmstart_host(sw_ctx* ctx, const float* queries, const sw_request* reqs,
                       uint64_t philox_seed, sw_choice* choices, float* d_out,
                       int32_t t_out_max, void* stream);
 /* Pipelined form of sw_warmstart_host for serving loops: enqueues the H2D copies (own copy
- * stream), the warm start (on `stream`) and the D2H of the choices (own copy stream), returns
- * a ticket at once; sw_warmstart_host_wait(ticket) blocks until `choices` has landed. Up to two
- * submissions overlap (batch n+1's copies run under batch n's kernels); `queries`, `reqs` and
- * `choices` must stay valid (and should be pinned) until the wait returns. Results are
- * identical to sw_warmstart_host's. */
+ * stream), the plan (on `stream`), the align + noise (the context's align stream, so it runs
+ * under the next batch's scoring kernel) and the D2H of the choices (own copy stream), and
+ * returns a ticket at once; sw_warmstart_host_wait(ticket) blocks until `choices` has landed
+ * and `d_out` is written. Up to two submissions overlap; `queries`, `reqs` and `choices` must
+ * stay valid (and should be pinned) until the wait returns. Results are identical to
+ * sw_warmstart_host's. */
 int sw_warmstart_host_submit(sw_ctx* ctx, const float* queries, const sw_request* reqs,
                              int32_t B, uint64_t seed, const sw_selector_config* sel,
                              const sw_policy* pol, uint64_t philox_seed, sw_choice* choices,

@@ -76,11 +76,12 @@ static void free_ctx(Ctx& c) {
         if (c.pipe_q[i]) cudaFree(c.pipe_q[i]);
         if (c.pipe_req[i]) cudaFree(c.pipe_req[i]);
         if (c.pipe_ch[i]) cudaFree(c.pipe_ch[i]);
-        for (cudaEvent_t e : {c.pipe_h2d[i], c.pipe_used[i], c.pipe_done[i]})
+        for (cudaEvent_t e : {c.pipe_h2d[i], c.pipe_used[i], c.pipe_done[i], c.pipe_planned[i]})
             if (e) cudaEventDestroy(e);
     }
     if (c.pipe_in) cudaStreamDestroy(c.pipe_in);
     if (c.pipe_out) cudaStreamDestroy(c.pipe_out);
+    if (c.pipe_al) cudaStreamDestroy(c.pipe_al);
     if (c.mstream) cudaStreamDestroy(c.mstream);
 }
 
@@ -875,11 +876,13 @@ int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs
         if (!c.pipe_in) {
             SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_in, cudaStreamNonBlocking));
             SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_out, cudaStreamNonBlocking));
+            SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_al, cudaStreamNonBlocking));
             for (int i = 0; i < Ctx::kPipe; ++i) {
                 SW_CUDA(cudaMalloc(&c.pipe_q[i], sizeof(float) * (size_t)c.Bmax * c.D));
                 SW_CUDA(cudaMalloc(&c.pipe_req[i], sizeof(sw_request) * (size_t)c.Bmax));
                 SW_CUDA(cudaMalloc(&c.pipe_ch[i], sizeof(sw_choice) * (size_t)c.Bmax));
-                for (cudaEvent_t* e : {&c.pipe_h2d[i], &c.pipe_used[i], &c.pipe_done[i]})
+                for (cudaEvent_t* e :
+                     {&c.pipe_h2d[i], &c.pipe_used[i], &c.pipe_done[i], &c.pipe_planned[i]})
                     SW_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
                 SW_CUDA(cudaEventRecord(c.pipe_used[i], c.pipe_in));
             }
@@ -897,14 +900,20 @@ int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs
             SW_CUDA(cudaStreamWaitEvent(st, c.pipe_h2d[slot], 0));
             int kn = plan_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed, sel, pol,
                                c.pipe_ch[slot], st);
-            launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr, philox_seed,
-                               d_out, t_out_max, st);
-            SW_CUDA(cudaEventRecord(c.pipe_used[slot], st));
+            SW_CUDA(cudaEventRecord(c.pipe_planned[slot], st));
             c.last_kernels = kn + 1;
         }
-        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));
+        // align + noise on the context's align stream: it reads only this slot's choices and
+        // requests (and the read-only latent arena), so it runs under the NEXT batch's scoring
+        // kernel (that kernel leaves registers and threads free on every SM)
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_al, c.pipe_planned[slot], 0));
+        launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr, philox_seed,
+                           d_out, t_out_max, c.pipe_al);
+        SW_CUDA(cudaEventRecord(c.pipe_used[slot], c.pipe_al));  // slot free after this
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_planned[slot], 0));
         SW_CUDA(cudaMemcpyAsync(choices, c.pipe_ch[slot], sizeof(sw_choice) * (size_t)B,
                                 cudaMemcpyDeviceToHost, c.pipe_out));
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));  // done = both
         SW_CUDA(cudaEventRecord(c.pipe_done[slot], c.pipe_out));
         *ticket = c.pipe_seq++;
         return SW_OK;

@@ -220,8 +220,9 @@ struct Ctx {
     static constexpr int kPipe = 2;
     std::mutex pipe_mu;
     int64_t pipe_seq = 0;
-    cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
-    cudaEvent_t pipe_h2d[kPipe] = {}, pipe_used[kPipe] = {}, pipe_done[kPipe] = {};
+    cudaStream_t pipe_in = nullptr, pipe_out = nullptr, pipe_al = nullptr;
+    cudaEvent_t pipe_h2d[kPipe] = {}, pipe_used[kPipe] = {}, pipe_done[kPipe] = {},
+                pipe_planned[kPipe] = {};
     float* pipe_q[kPipe] = {};
     sw_request* pipe_req[kPipe] = {};
     sw_choice* pipe_ch[kPipe] = {};
