@@ -17,6 +17,7 @@
 // reductions of the k-means++ seeding (running total, cumulative scan) run on the host in the
 // reference's order. The parallel work (n x C dot products per Lloyd iteration, the per-(cluster,
 // dim) member sums, the farthest-point search) runs on the GPU.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <numeric>
@@ -711,7 +712,15 @@ static void build_sorted(Ctx& c) {
     // chunking: tpc tiles per work item, <= kMaxSlices / nprobe chunks per list
     const int np = std::max(1, std::min(c.ivf_nprobe, C));
     // 16+ tiles per item amortise the per-item pipeline ramp (A load, TMA / MMA fill, drain)
-    c.grp_tpc = std::max(16, (maxt * np + kMaxSlices - 1) / kMaxSlices);
+    // 24 measured best at the reference default (64 lists, nprobe 8, B = 1024, 1M rows):
+    // score 0.285-0.292 ms vs 0.301 (16), 0.308 (28), 0.33 (20, 32), 0.38 (8) — shorter items
+    // pay the per-item ramp (A load, pipeline fill and drain), longer ones balance worse over
+    // the 148 persistent CTAs. SW_IVF_TPC overrides.
+    static const int tpc_min = [] {
+        const char* e = getenv("SW_IVF_TPC");
+        return e ? std::max(1, atoi(e)) : 24;
+    }();
+    c.grp_tpc = std::max(tpc_min, (maxt * np + kMaxSlices - 1) / kMaxSlices);
     c.grp_ch = std::max(1, (maxt + c.grp_tpc - 1) / c.grp_tpc);
     if (c.grp_rows > c.grp_cap_rows) {
         cudaFree(c.d_sorted_slot);
