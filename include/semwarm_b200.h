@@ -276,6 +276,18 @@ int sw_warmstart(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, 
                  uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
                  const float* d_eps, uint64_t philox_seed, sw_choice* d_choices, float* d_out,
                  int32_t t_out_max, void* stream);
+/* Cross-batch pipelined sw_warmstart: prep + scoring of this batch on `stream`, its finish
+ * (filter, exact rescoring, top-k, gate, select, gater) and align + noise on the context's
+ * own stream, so they run under the NEXT call's scoring kernel. d_choices and d_out are
+ * complete, and d_queries / d_reqs / d_eps may be reused, once sw_join(ctx, s) has been
+ * enqueued on a stream s and s reached that point. Results are identical to sw_warmstart's.
+ * In IVF mode (single-buffered probe scratch) it runs like sw_warmstart. */
+int sw_warmstart_async(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, int32_t B,
+                       uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                       const float* d_eps, uint64_t philox_seed, sw_choice* d_choices,
+                       float* d_out, int32_t t_out_max, void* stream);
+/* Makes `stream` wait for every sw_warmstart_async enqueued so far. */
+int sw_join(sw_ctx* ctx, void* stream);
 /* End-to-end from host buffers (pinned or pageable): H2D prompts+requests, warm start,
  * D2H choices; the noised latents stay on the device in d_out. Synchronous. */
 int sw_warmstart_host(sw_ctx* ctx, const float* queries, const sw_request* reqs, int32_t B,

@@ -123,6 +123,9 @@ def lib() -> C.CDLL:
                           C.POINTER(SwPolicy), vp, u64, vp, vp, i32, vp], C.c_int),
         "sw_warmstart_host": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
                                C.POINTER(SwPolicy), u64, vp, vp, i32, vp], C.c_int),
+        "sw_warmstart_async": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
+                                C.POINTER(SwPolicy), vp, u64, vp, vp, i32, vp], C.c_int),
+        "sw_join": ([vp, vp], C.c_int),
         "sw_warmstart_host_submit": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
                                       C.POINTER(SwPolicy), u64, vp, vp, i32, vp,
                                       C.POINTER(C.c_int64)], C.c_int),
@@ -185,7 +188,8 @@ EXPORTED = [
     "sw_arena_remove", "sw_arena_replace", "sw_arena_entry_count", "sw_arena_contains",
     "sw_arena_fill_synthetic", "sw_arena_read_rows", "sw_search", "sw_search_host", "sw_plan",
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host",
-    "sw_warmstart_host_submit", "sw_warmstart_host_wait", "sw_local_topk", "sw_merge_select",
+    "sw_warmstart_host_submit", "sw_warmstart_host_wait", "sw_warmstart_async", "sw_join",
+    "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
     "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",

@@ -59,6 +59,19 @@ static void default_schedule(std::vector<double>& abar) {
 }
 
 static void free_ctx(Ctx& c) {
+    if (c.async_st) {  // the scratch fields hold parity 0 again; free parity 1 separately
+        c.q_eps = c.q_eps_p[0];
+        c.slice_cnt = c.slice_cnt_p[0];
+        c.cta_topk = c.cta_topk_p[0];
+        c.cand_slot = c.cand_slot_p[0];
+        c.cand_score = c.cand_score_p[0];
+        for (void* q : {(void*)c.q_eps_p[1], (void*)c.slice_cnt_p[1], (void*)c.cta_topk_p[1],
+                        (void*)c.cand_slot_p[1], (void*)c.cand_score_p[1]})
+            if (q) cudaFree(q);
+        for (cudaEvent_t e : {c.async_score_ev, c.async_join_ev, c.async_done[0], c.async_done[1]})
+            if (e) cudaEventDestroy(e);
+        cudaStreamDestroy(c.async_st);
+    }
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
                     c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
@@ -794,10 +807,62 @@ static void check_sel(const sw_selector_config* sel, const sw_policy* pol) {
 
 static int plan_impl(Ctx& c, const float* d_q, const sw_request* d_req, int B, uint64_t seed,
                      const sw_selector_config* sel, const sw_policy* pol, sw_choice* d_out,
-                     cudaStream_t st) {
+                     cudaStream_t st, cudaStream_t st_finish = nullptr) {
     check_sel(sel, pol);
     const dev::SelParams sp = dev::make_sel_params(c, seed, *sel, *pol);
-    return launch_search_fused(c, d_q, B, sel->top_k, 0, d_req, &sp, d_out, st);
+    return launch_search_fused(c, d_q, B, sel->top_k, 0, d_req, &sp, d_out, st,
+                               st_finish ? st_finish : st);
+}
+
+// ---------------------------------------------------------------- cross-batch pipelining
+static void set_par(Ctx& c, int par) {
+    c.q_eps = c.q_eps_p[par];
+    c.slice_cnt = c.slice_cnt_p[par];
+    c.cta_topk = c.cta_topk_p[par];
+    c.cand_slot = c.cand_slot_p[par];
+    c.cand_score = c.cand_score_p[par];
+    c.cur_par = par;
+}
+
+static void ensure_async(Ctx& c) {
+    if (c.async_st) return;
+    SW_CUDA(cudaStreamCreateWithFlags(&c.async_st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c.async_score_ev, &c.async_join_ev, &c.async_done[0], &c.async_done[1]})
+        SW_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    c.q_eps_p[0] = c.q_eps;
+    c.slice_cnt_p[0] = c.slice_cnt;
+    c.cta_topk_p[0] = c.cta_topk;
+    c.cand_slot_p[0] = c.cand_slot;
+    c.cand_score_p[0] = c.cand_score;
+    dalloc(&c.q_eps_p[1], (size_t)c.Bmax);
+    dalloc(&c.slice_cnt_p[1], (size_t)c.Bmax * kMaxSlices);
+    dalloc(&c.cta_topk_p[1], (size_t)c.Bmax * kMaxSlices * kMaxTopK);
+    dalloc(&c.cand_slot_p[1], (size_t)c.Bmax * kCandCap);
+    dalloc(&c.cand_score_p[1], (size_t)c.Bmax * kCandCap);
+    c.cur_par = 0;
+}
+
+// Batch i: prep + scoring on S, finish + align + noise on c.async_st. The buffers finish(i)
+// reads alternate parity, so scoring(i + 1) on S overlaps finish(i) (the scoring kernel is
+// capped at 4 ring stages, leaving shared memory for one finish CTA per SM) and align(i).
+// Caller holds c.mu (shared) and c.scratch_mu. Returns the kernel count.
+static int warmstart_async_impl(Ctx& c, const float* d_q, const sw_request* d_req, int B,
+                                uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                                const float* d_eps, uint64_t philox_seed, sw_choice* d_ch,
+                                float* d_out, int t_out_max, cudaStream_t S) {
+    ensure_async(c);
+    const int par = c.async_par;
+    if (c.async_used[par]) SW_CUDA(cudaStreamWaitEvent(S, c.async_done[par], 0));
+    if (!c.last_user_async && c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
+    set_par(c, par);
+    const int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, S, c.async_st);
+    launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, c.async_st);
+    SW_CUDA(cudaEventRecord(c.async_done[par], c.async_st));
+    if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, c.async_st));  // for later sync users
+    c.async_used[par] = true;
+    c.async_par = par ^ 1;
+    c.last_user_async = true;
+    return kn + 1;
 }
 
 int sw_plan(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, uint64_t seed,
@@ -876,7 +941,6 @@ int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs
         if (!c.pipe_in) {
             SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_in, cudaStreamNonBlocking));
             SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_out, cudaStreamNonBlocking));
-            SW_CUDA(cudaStreamCreateWithFlags(&c.pipe_al, cudaStreamNonBlocking));
             for (int i = 0; i < Ctx::kPipe; ++i) {
                 SW_CUDA(cudaMalloc(&c.pipe_q[i], sizeof(float) * (size_t)c.Bmax * c.D));
                 SW_CUDA(cudaMalloc(&c.pipe_req[i], sizeof(sw_request) * (size_t)c.Bmax));
@@ -890,30 +954,43 @@ int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs
         const int slot = (int)(c.pipe_seq % Ctx::kPipe);
         cudaStream_t st = as_stream(stream);
         SW_CUDA(cudaStreamWaitEvent(c.pipe_in, c.pipe_used[slot], 0));
+        SW_CUDA(cudaStreamWaitEvent(c.pipe_in, c.pipe_done[slot], 0));  // its choices are home
         SW_CUDA(cudaMemcpyAsync(c.pipe_q[slot], q, sizeof(float) * (size_t)B * c.D,
                                 cudaMemcpyHostToDevice, c.pipe_in));
         SW_CUDA(cudaMemcpyAsync(c.pipe_req[slot], reqs, sizeof(sw_request) * (size_t)B,
                                 cudaMemcpyHostToDevice, c.pipe_in));
         SW_CUDA(cudaEventRecord(c.pipe_h2d[slot], c.pipe_in));
         {
-            HotGuard lk(c, st);
+            // plan's prep + scoring on the caller's stream; finish, align + noise on the
+            // context's async stream (under the next batch's scoring)
+            std::shared_lock<std::shared_mutex> rd(c.mu);
+            std::unique_lock<std::mutex> sc(c.scratch_mu);
             SW_CUDA(cudaStreamWaitEvent(st, c.pipe_h2d[slot], 0));
-            int kn = plan_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed, sel, pol,
-                               c.pipe_ch[slot], st);
-            SW_CUDA(cudaEventRecord(c.pipe_planned[slot], st));
-            c.last_kernels = kn + 1;
+            cudaEvent_t done;
+            if (c.ivf) {  // single-buffered IVF scratch: everything on the caller's stream
+                if (c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(st, c.scratch_ev, 0));
+                int kn = plan_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed, sel, pol,
+                                   c.pipe_ch[slot], st);
+                launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr,
+                                   philox_seed, d_out, t_out_max, st);
+                if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, st));
+                c.last_user_async = false;
+                c.last_kernels = kn + 1;
+                SW_CUDA(cudaEventRecord(c.pipe_planned[slot], st));
+                done = c.pipe_planned[slot];
+            } else {
+                const int par = c.async_st ? c.async_par : 0;
+                c.last_kernels = warmstart_async_impl(c, c.pipe_q[slot], c.pipe_req[slot], B,
+                                                      seed, sel, pol, nullptr, philox_seed,
+                                                      c.pipe_ch[slot], d_out, t_out_max, st);
+                done = c.async_done[par];
+            }
+            SW_CUDA(cudaEventRecord(c.pipe_used[slot], c.async_st ? c.async_st : st));
+            SW_CUDA(cudaStreamWaitEvent(c.pipe_out, done, 0));
+            if (c.async_st) SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));
         }
-        // align + noise on the context's align stream: it reads only this slot's choices and
-        // requests (and the read-only latent arena), so it runs under the NEXT batch's scoring
-        // kernel (that kernel leaves registers and threads free on every SM)
-        SW_CUDA(cudaStreamWaitEvent(c.pipe_al, c.pipe_planned[slot], 0));
-        launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr, philox_seed,
-                           d_out, t_out_max, c.pipe_al);
-        SW_CUDA(cudaEventRecord(c.pipe_used[slot], c.pipe_al));  // slot free after this
-        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_planned[slot], 0));
         SW_CUDA(cudaMemcpyAsync(choices, c.pipe_ch[slot], sizeof(sw_choice) * (size_t)B,
                                 cudaMemcpyDeviceToHost, c.pipe_out));
-        SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));  // done = both
         SW_CUDA(cudaEventRecord(c.pipe_done[slot], c.pipe_out));
         *ticket = c.pipe_seq++;
         return SW_OK;
@@ -933,6 +1010,46 @@ int sw_warmstart_host_wait(sw_ctx* ctx, int64_t ticket) {
             e = c.pipe_done[ticket % Ctx::kPipe];
         }
         SW_CUDA(cudaEventSynchronize(e));
+        return SW_OK;
+    });
+}
+
+int sw_warmstart_async(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B,
+                       uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
+                       const float* d_eps, uint64_t philox_seed, sw_choice* d_ch, float* d_out,
+                       int32_t t_out_max, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_req && d_ch && d_out)), "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock<std::shared_mutex> rd(c.mu);
+        std::unique_lock<std::mutex> sc(c.scratch_mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t S = as_stream(stream);
+        if (c.ivf) {  // probe ranks and list groups are single-buffered: no overlap in IVF mode
+            if (c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
+            int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, S);
+            launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, S);
+            if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, S));
+            c.last_user_async = false;
+            c.last_kernels = kn + 1;
+            return SW_OK;
+        }
+        c.last_kernels = warmstart_async_impl(c, d_q, d_req, B, seed, sel, pol, d_eps,
+                                              philox_seed, d_ch, d_out, t_out_max, S);
+        return SW_OK;
+    });
+}
+
+int sw_join(sw_ctx* ctx, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock<std::mutex> sc(c.scratch_mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        if (c.async_st) {
+            SW_CUDA(cudaEventRecord(c.async_join_ev, c.async_st));
+            SW_CUDA(cudaStreamWaitEvent(as_stream(stream), c.async_join_ev, 0));
+        }
         return SW_OK;
     });
 }

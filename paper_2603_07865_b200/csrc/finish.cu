@@ -655,6 +655,14 @@ bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
 // Search (+ optionally select) for B queries. Results land in c.hits / c.nhits (and d_out).
 int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
                         const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st) {
+    return launch_search_fused(c, d_q, B, k, rank, d_req, sp, d_out, st, st);
+}
+
+// st_finish != st: prep, probe ranking and scoring on st, the finish kernel on st_finish after
+// an event (cross-batch pipelining; the caller manages the scratch parities)
+int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
+                        const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st,
+                        cudaStream_t st_finish) {
     SW_REQUIRE(k >= 1, "search k must be >= 1");  // index.cpp:291
     SW_REQUIRE(k <= kMaxTopK, "top-k above 32 is not supported");
     SW_REQUIRE(B >= 0 && B <= c.Bmax, "batch exceeds the context's max_batch");
@@ -724,6 +732,11 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.row_list = c.row_list;
     p.prank = c.prank;
     c.last_ivf = ivf;
+    if (st_finish != st) {
+        SW_CUDA(cudaEventRecord(c.async_score_ev, st));
+        SW_CUDA(cudaStreamWaitEvent(st_finish, c.async_score_ev, 0));
+        st = st_finish;
+    }
     {
         StageScope sc(c, SW_STAGE_FINISH, st);
         static const bool ring = [] {

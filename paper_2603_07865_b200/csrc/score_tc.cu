@@ -873,7 +873,15 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     } else if (pair) {
         stage_bytes = B_HALF;
     }
-    p.n_stages = std::min(max_stages, (budget - a_bytes) / stage_bytes);
+    // CTA pairs keep 4 B stages: measured as fast as 6 (0.711 vs 0.708-0.729 ms; 3 stages lose
+    // 12%), and the ~35 KB of shared memory it frees per SM lets one k_finish CTA of the
+    // previous batch co-run with this kernel (sw_warmstart_async). SW_SCORE_STAGES overrides.
+    static const int stage_env = [] {
+        const char* e = getenv("SW_SCORE_STAGES");
+        return e ? std::max(2, atoi(e)) : 0;
+    }();
+    const int stage_cap = stage_env ? stage_env : (pair ? 4 : 64);
+    p.n_stages = std::min(std::min(max_stages, stage_cap), (budget - a_bytes) / stage_bytes);
     SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
     const int tbn = ts ? BN_TS : BN;
     const int64_t rows_hw = c.high_water * c.Rp;

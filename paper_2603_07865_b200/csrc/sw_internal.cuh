@@ -215,6 +215,22 @@ struct Ctx {
     // scratch_ev, so concurrent readers on different streams never overlap on it.
     std::mutex scratch_mu;
     cudaEvent_t scratch_ev = nullptr;
+    // Cross-batch pipelining (sw_warmstart_async): prep + score of batch i+1 run on the caller's
+    // stream while finish + align of batch i run on async_st. The buffers the finish reads and
+    // the next scoring writes alternate between two parities; the rest of the scratch is only
+    // touched by one of the two streams.
+    cudaStream_t async_st = nullptr;
+    cudaEvent_t async_score_ev = nullptr, async_join_ev = nullptr;
+    cudaEvent_t async_done[2] = {};
+    bool async_used[2] = {false, false};
+    bool last_user_async = false;
+    int async_par = 0;
+    int cur_par = 0;  // parity the scratch pointers below currently hold
+    float* q_eps_p[2] = {};
+    int32_t* slice_cnt_p[2] = {};
+    float* cta_topk_p[2] = {};
+    int32_t* cand_slot_p[2] = {};
+    float* cand_score_p[2] = {};
     // pipelined host path (sw_warmstart_host_submit / _wait): kPipe staging slots, H2D on
     // pipe_in, D2H on pipe_out, so batch i+1's copies overlap batch i's kernels
     static constexpr int kPipe = 2;
@@ -249,6 +265,7 @@ struct HotGuard {
     HotGuard(Ctx& c_, cudaStream_t st_) : rd(c_.mu), sc(c_.scratch_mu), c(c_), st(st_) {
         cudaSetDevice(c.device);
         if (c.scratch_ev) cudaStreamWaitEvent(st, c.scratch_ev, 0);
+        c.last_user_async = false;
     }
     ~HotGuard() {
         if (c.scratch_ev) cudaEventRecord(c.scratch_ev, st);
@@ -293,6 +310,9 @@ void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, 
 int launch_prep(Ctx& c, const float* d_q, int B, const sw_request* d_req, uint64_t seed,
                 cudaStream_t st);
 int launch_search(Ctx& c, const float* d_q, int B, int k, int rank, cudaStream_t st);
+int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
+                        const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st,
+                        cudaStream_t st_finish);
 int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const sw_request* d_req,
                         const dev::SelParams* sp, sw_choice* d_out, cudaStream_t st);
 void launch_hits_to_public(Ctx& c, int B, int k, sw_hit* d_out, int32_t* d_n, cudaStream_t st);

@@ -57,3 +57,69 @@ def test_pipelined_wait_rejects_unknown_ticket():
     wc = WarmStartCache(64, rows_per_entry=1, max_entries=64, max_batch=8)
     with pytest.raises(ValueError):
         wc.warmstart_host_wait(5)
+
+
+def _async_case(ivf=False):
+    from paper_2603_07865_b200 import _lib
+    from paper_2603_07865_b200.warmstart import (Policy, SelectorConfig, WarmStartCache, requests)
+    c = SynthCache(30000, 256, 1.0, seed=73, clustered=True)
+    latent = (4, 64, 16)
+    wc = WarmStartCache(256, rows_per_entry=1, max_entries=30000, max_batch=512,
+                        latent_shape=latent, latent_slots=4096)
+    if ivf:  # configured on the empty arena (IvfIndex::build({}, ...)), rebuilt after inserts
+        wc.ivf_configure(16, 4, 1 << 30, seed=3)
+    wc.insert_batch(c.ids, c.off, c.rows, c.levels, c.starts, c.lengths)
+    if ivf:
+        wc.ivf_rebuild()
+    sel, pol = SelectorConfig(8), Policy("exploit")
+    dev = torch.device("cuda", 0)
+    nb, B, T = 6, 512, 64
+    qs, rqs = [], []
+    for j in range(nb):
+        qs.append(torch.from_numpy(perturbed_queries(c, B, frac_random=0.1, seed=300 + j)).to(dev))
+        ids = np.arange(1 + j * B, 1 + (j + 1) * B, dtype=np.uint64)
+        rq = requests(ids, request_durations(B, 4.0, 10.0, seed=400 + j), np.full(B, 100, np.int32))
+        rqs.append(torch.from_numpy(rq.view(np.uint8)).to(dev))
+    return c, wc, sel, pol, dev, nb, B, T, latent, qs, rqs, _lib
+
+
+@pytest.mark.parametrize("ivf", [False, True])
+def test_warmstart_async_matches_sync(ivf):
+    """sw_warmstart_async (prep + scoring on the caller's stream, finish + align + noise on the
+    context's stream under the next batch's scoring, alternating scratch parities) returns
+    exactly sw_warmstart's choices and latents; a synchronous search after it sees the whole
+    pipeline finished (scratch ordering)."""
+    import ctypes as C
+    c, wc, sel, pol, dev, nb, B, T, latent, qs, rqs, _lib = _async_case(ivf)
+    L = _lib.lib()
+    st = torch.cuda.current_stream(dev).cuda_stream
+    ref_ch, ref_lat = [], []
+    for j in range(nb):
+        ch = torch.zeros(B * _lib.CHOICE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        out = torch.zeros((B, latent[0], T, latent[2]), dtype=torch.float32, device=dev)
+        _lib.check(L.sw_warmstart(wc._h, qs[j].data_ptr(), rqs[j].data_ptr(), B, 9,
+                                  C.byref(sel.c()), C.byref(pol.c()), None, 4321, ch.data_ptr(),
+                                  out.data_ptr(), T, st), "sw_warmstart")
+        ref_ch.append(ch.cpu().numpy().view(_lib.CHOICE_DTYPE))
+        ref_lat.append(out.cpu().numpy())
+    chs = [torch.zeros(B * _lib.CHOICE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+           for _ in range(nb)]
+    outs = [torch.zeros((B, latent[0], T, latent[2]), dtype=torch.float32, device=dev)
+            for _ in range(nb)]
+    for j in range(nb):
+        _lib.check(L.sw_warmstart_async(wc._h, qs[j].data_ptr(), rqs[j].data_ptr(), B, 9,
+                                        C.byref(sel.c()), C.byref(pol.c()), None, 4321,
+                                        chs[j].data_ptr(), outs[j].data_ptr(), T, st),
+                   "sw_warmstart_async")
+    hits_after, n_after = wc.search(qs[0].cpu().numpy(), 8)  # synchronous user after async ones
+    _lib.check(L.sw_join(wc._h, st), "sw_join")
+    torch.cuda.synchronize(dev)
+    for j in range(nb):
+        got = chs[j].cpu().numpy().view(_lib.CHOICE_DTYPE)
+        assert ref_ch[j]["hit"].any()
+        for f in ref_ch[j].dtype.names:
+            np.testing.assert_array_equal(got[f], ref_ch[j][f], err_msg=f"batch {j} {f}")
+        np.testing.assert_array_equal(outs[j].cpu().numpy(), ref_lat[j])
+    hits_ref, n_ref = wc.search(qs[0].cpu().numpy(), 8)
+    np.testing.assert_array_equal(n_after, n_ref)
+    np.testing.assert_array_equal(hits_after["entry_id"], hits_ref["entry_id"])
