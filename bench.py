@@ -715,6 +715,8 @@ def main():
 
     # ---- roofline of the dominant kernel (tcgen05 scoring), timed live on its stream
     pk_burst, pk_sust, hbm, pk_src = peaks()
+    default_workload = (args.entries == 1_000_000 and B == 1024 and K == 8 and R == 1
+                        and not ivf and world == 1 and not sharded)
     sc_ms, sc_n = prof["score_tc"]
     n_rows = n_local * R
     flops = 2.0 * B * n_rows * D
@@ -777,8 +779,11 @@ def main():
                      "unit": "TFLOP/s", "frac": round(achieved / pk_burst, 4) if achieved else None,
                      "frac_of_sustained": round(achieved / pk_sust, 4) if achieved and pk_sust else None,
                      "peak_source": pk_src,
-                     "traffic": ncu_traffic("k_score_tc")[0],
-                     "traffic_source": "profiles/ncu_latest.json (ncu --set full, one launch)",
+                     # the committed capture profiles the default workload only
+                     "traffic": ncu_traffic("k_score_tc")[0] if default_workload else None,
+                     "traffic_source": ("profiles/ncu_latest.json (ncu --set full, one launch)"
+                                        if default_workload else
+                                        "not captured for this configuration"),
                      "algorithmic": f"2*B*N*D = {flops:.4g} flop per launch",
                      "kernel_ms": round(score_ms, 4),
                      "share_of_step": round(score_ms / total_ms_step, 3),
