@@ -73,7 +73,7 @@ static void free_ctx(Ctx& c) {
         cudaStreamDestroy(c.async_st);
     }
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
-                    c.slice_cnt, c.cta_topk, c.u_draw, c.dbg, c.tsrc,
+                    c.slice_cnt, c.cta_topk, c.dbg, c.tsrc,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
@@ -148,7 +148,6 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.cand_n, (size_t)3 * c.Bmax);
     dalloc(&c.slice_cnt, (size_t)c.Bmax * kMaxSlices);
     dalloc(&c.cta_topk, (size_t)c.Bmax * kMaxSlices * kMaxTopK);
-    dalloc(&c.u_draw, (size_t)c.Bmax);
     dalloc(&c.dbg, (size_t)c.Bmax * 8);
     dalloc(&c.cand_slot, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_score, (size_t)c.Bmax * kCandCap);

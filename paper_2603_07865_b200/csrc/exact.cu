@@ -23,17 +23,12 @@ __device__ __forceinline__ double clamp_cos(double v) {
 __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
                        __nv_bfloat16* __restrict__ q_bf, float* __restrict__ q_norm,
                        float* __restrict__ q_eps, const uint32_t* __restrict__ norms,
-                       uint32_t* __restrict__ thr, uint32_t* __restrict__ top1,
-                       const sw_request* __restrict__ req, uint64_t seed,
-                       double* __restrict__ u_draw) {
+                       uint32_t* __restrict__ thr, uint32_t* __restrict__ top1) {
     const int b = blockIdx.x;
     if (b >= B) return;
     for (int i = threadIdx.x; i < kMaxSlices; i += blockDim.x)
         top1[(int64_t)b * kMaxSlices + i] = f2ord(-INFINITY);
     // (the request's selector draw is computed in k_finish, overlapping its phase A)
-    (void)req;
-    (void)seed;
-    (void)u_draw;
     __shared__ double red[3][32];
     const float* qb = q + (int64_t)b * D;
     double nn = 0.0, dd = 0.0, bb = 0.0;
@@ -97,8 +92,7 @@ __global__ void k_hits_to_public(int B, int k, const HitRec* __restrict__ hits,
 int launch_prep(Ctx& c, const float* d_q, int B, const sw_request* d_req, uint64_t seed,
                 cudaStream_t st) {
     StageScope sc(c, SW_STAGE_PREP, st);
-    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.q_eps, c.norms, c.thr, c.top1, d_req,
-                              seed, c.u_draw);
+    k_prep<<<B, 128, 0, st>>>(d_q, B, c.D, c.Dp, c.q_bf, c.q_norm, c.q_eps, c.norms, c.thr, c.top1);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

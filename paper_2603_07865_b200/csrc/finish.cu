@@ -64,7 +64,6 @@ struct FinishParams {
     int32_t* best_row;
     HitRec* hits;
     int32_t* nhits;
-    const double* u_draw;
     int32_t* dbg;  // [B][8]: emitted, kept, then clock64 deltas per phase (debug stats)
     dev::SelParams sp;
     const sw_request* reqs;
@@ -723,7 +722,6 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.best_row = c.cand_row;
     p.hits = c.hits;
     p.nhits = c.nhits;
-    p.u_draw = c.u_draw;
     p.dbg = c.dbg;
     if (sp) p.sp = *sp;
     p.reqs = d_req;

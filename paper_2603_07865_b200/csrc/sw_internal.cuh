@@ -132,7 +132,6 @@ struct Ctx {
     int32_t* cand_n = nullptr;      // [3][Bmax]: unused | compacted count | overflow flag
     int32_t* slice_cnt = nullptr;   // [Bmax][kMaxSlices] emissions per (query, CTA, group)
     float* cta_topk = nullptr;      // [Bmax][kMaxSlices][32] each slice's final top-k (approx)
-    double* u_draw = nullptr;       // [Bmax] per-request selector draw
     int32_t* dbg = nullptr;         // [Bmax][8] per-query finish stats (sw_debug_query_stats)
     int last_chunks = 1;
     bool last_ivf = false;         // last search probed IVF lists (nprobe < C)
