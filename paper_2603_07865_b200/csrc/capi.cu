@@ -58,6 +58,14 @@ static void default_schedule(std::vector<double>& abar) {
     }
 }
 
+// Arena mutations (exclusive on the host) must also come after every reader's device work:
+// hot-path calls return before their kernels run (the async path's finish and align even run
+// on the context's own stream), and every one of them ends with scratch_ev.
+// (host-side wait: the mutation paths use several streams and synchronous copies)
+static void wait_readers(Ctx& c) {
+    if (c.scratch_ev) SW_CUDA(cudaEventSynchronize(c.scratch_ev));
+}
+
 static void free_ctx(Ctx& c) {
     if (c.async_st) {  // the scratch fields hold parity 0 again; free parity 1 separately
         c.q_eps = c.q_eps_p[0];
@@ -411,6 +419,7 @@ int sw_set_negative(sw_ctx* ctx, const float* neg) {
         SW_REQUIRE(ctx && neg, "null argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         SW_CUDA(cudaMemcpyAsync(c.neg, neg, sizeof(float) * c.D, cudaMemcpyHostToDevice, c.mstream));
         c.have_neg = true;
@@ -426,6 +435,7 @@ int sw_set_gater(sw_ctx* ctx, const float* theta, const float* psi, int32_t fd, 
         SW_REQUIRE(fd == kFeatureDim, "feature dim mismatch");  // gater.cpp:62
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         SW_CUDA(cudaMemcpyAsync(c.theta, theta, sizeof(float) * kNumArms * fd, cudaMemcpyHostToDevice, c.mstream));
         SW_CUDA(cudaMemcpyAsync(c.psi, psi, sizeof(float) * kNumArms * fd, cudaMemcpyHostToDevice, c.mstream));
@@ -441,6 +451,7 @@ int sw_set_schedule(sw_ctx* ctx, const double* abar, int32_t n) {
         SW_REQUIRE(ctx && abar && n >= 2, "schedule needs >= 2 entries");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         if (n != c.n_abar) {
             cudaFree(c.abar);
@@ -461,6 +472,7 @@ int sw_arena_insert(sw_ctx* ctx, uint64_t id, int32_t n_rows, const float* rows,
         if (n_rows == 0) return SW_OK;  // IvfIndex::insert of nothing (index.cpp:227)
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         int64_t off[2] = {0, n_rows};
         int64_t loff = 0;
@@ -477,6 +489,7 @@ int sw_arena_insert_batch(sw_ctx* ctx, int64_t n, const uint64_t* ids, const int
         if (n <= 0) return SW_OK;
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         do_insert(c, n, ids, row_off, rows, segs, latents, lat_off, t_src, on_device != 0);
         return SW_OK;
@@ -488,6 +501,7 @@ int sw_arena_remove(sw_ctx* ctx, uint64_t id) {
         SW_REQUIRE(ctx, "null argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         bool found = false;
         do_remove(c, id, &found);
@@ -505,6 +519,7 @@ int sw_arena_replace(sw_ctx* ctx, uint64_t id, int32_t n_rows, const float* rows
         SW_REQUIRE(ctx && rows && segs && n_rows >= 1, "bad argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         auto it = c.slot_of.find(id);
         if (it == c.slot_of.end()) {
@@ -541,6 +556,7 @@ int sw_arena_fill_synthetic(sw_ctx* ctx, int64_t n, uint64_t first_id, uint64_t 
         SW_REQUIRE(ctx && n >= 0, "bad argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         SW_REQUIRE(c.free_slots.empty(), "synthetic fill needs a compact arena");
         SW_REQUIRE(c.high_water + n <= c.S, "arena full (max_entries reached)");
@@ -578,6 +594,7 @@ int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t re
         SW_REQUIRE(rebuild_interval >= 1, "rebuild interval must be >= 1");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_REQUIRE(c.slot_of.empty(), "configure the IVF index on an empty arena");
         c.ivf = true;
         c.ivf_target = centroids;
@@ -596,6 +613,7 @@ int sw_ivf_set_nprobe(sw_ctx* ctx, int32_t nprobe) {
     return guarded([&] {
         SW_REQUIRE(ctx && nprobe >= 1, "bad argument");
         std::unique_lock lk(ctx->c.mu);
+        wait_readers(ctx->c);
         ctx->c.ivf_nprobe = nprobe;
         return SW_OK;
     });
@@ -606,6 +624,7 @@ int sw_ivf_rebuild(sw_ctx* ctx) {
         SW_REQUIRE(ctx, "null argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_REQUIRE(c.ivf, "the context is not in IVF mode (sw_ivf_configure)");
         SW_CUDA(cudaSetDevice(c.device));
         ivf_rebuild(c);
@@ -641,6 +660,7 @@ int sw_ivf_set_centroids(sw_ctx* ctx, const float* centroids, int32_t n) {
         SW_REQUIRE(n >= 0 && n <= kMaxCentroids, "at most 256 centroids are supported");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_REQUIRE(c.ivf, "the context is not in IVF mode (sw_ivf_configure)");
         SW_CUDA(cudaSetDevice(c.device));
         ivf_set_centroids(c, centroids, n);
@@ -672,6 +692,7 @@ int sw_set_align_mode(sw_ctx* ctx, int32_t mode, int32_t window, int32_t hop) {
         SW_REQUIRE(hop >= 1 && hop <= window, "stft hop must be in (0, window_size]");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         c.align_mode = mode;
         c.voc_win = window;
         c.voc_hop = hop;
@@ -699,6 +720,7 @@ int sw_swix_load(sw_ctx* ctx, const char* path) {
         SW_REQUIRE(ctx && path, "null argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         swix_load(c, path, &bulk_insert);
         return SW_OK;
@@ -710,6 +732,7 @@ int sw_swix_save(sw_ctx* ctx, const char* path) {
         SW_REQUIRE(ctx && path, "null argument");
         Ctx& c = ctx->c;
         std::unique_lock lk(c.mu);
+        wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         swix_save(c, path);
         return SW_OK;
