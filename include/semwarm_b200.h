@@ -280,8 +280,8 @@ int sw_warmstart(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, 
  * (filter, exact rescoring, top-k, gate, select, gater) and align + noise on the context's
  * own stream, so they run under the NEXT call's scoring kernel. d_choices and d_out are
  * complete, and d_queries / d_reqs / d_eps may be reused, once sw_join(ctx, s) has been
- * enqueued on a stream s and s reached that point. Results are identical to sw_warmstart's.
- * In IVF mode (single-buffered probe scratch) it runs like sw_warmstart. */
+ * enqueued on a stream s and s reached that point. Results are identical to sw_warmstart's,
+ * in exhaustive and IVF mode. */
 int sw_warmstart_async(sw_ctx* ctx, const float* d_queries, const sw_request* d_reqs, int32_t B,
                        uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,
                        const float* d_eps, uint64_t philox_seed, sw_choice* d_choices,

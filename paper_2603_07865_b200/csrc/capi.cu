@@ -73,8 +73,9 @@ static void free_ctx(Ctx& c) {
         c.cta_topk = c.cta_topk_p[0];
         c.cand_slot = c.cand_slot_p[0];
         c.cand_score = c.cand_score_p[0];
+        c.prank = c.prank_p[0];
         for (void* q : {(void*)c.q_eps_p[1], (void*)c.slice_cnt_p[1], (void*)c.cta_topk_p[1],
-                        (void*)c.cand_slot_p[1], (void*)c.cand_score_p[1]})
+                        (void*)c.cand_slot_p[1], (void*)c.cand_score_p[1], (void*)c.prank_p[1]})
             if (q) cudaFree(q);
         for (cudaEvent_t e : {c.async_score_ev, c.async_join_ev, c.async_done[0], c.async_done[1]})
             if (e) cudaEventDestroy(e);
@@ -843,6 +844,7 @@ static void set_par(Ctx& c, int par) {
     c.cta_topk = c.cta_topk_p[par];
     c.cand_slot = c.cand_slot_p[par];
     c.cand_score = c.cand_score_p[par];
+    c.prank = c.prank_p[par];
     c.cur_par = par;
 }
 
@@ -856,6 +858,8 @@ static void ensure_async(Ctx& c) {
     c.cta_topk_p[0] = c.cta_topk;
     c.cand_slot_p[0] = c.cand_slot;
     c.cand_score_p[0] = c.cand_score;
+    c.prank_p[0] = c.prank;
+    dalloc(&c.prank_p[1], (size_t)c.Bmax * kMaxCentroids);
     dalloc(&c.q_eps_p[1], (size_t)c.Bmax);
     dalloc(&c.slice_cnt_p[1], (size_t)c.Bmax * kMaxSlices);
     dalloc(&c.cta_topk_p[1], (size_t)c.Bmax * kMaxSlices * kMaxTopK);
@@ -988,25 +992,11 @@ int sw_warmstart_host_submit(sw_ctx* ctx, const float* q, const sw_request* reqs
             std::shared_lock<std::shared_mutex> rd(c.mu);
             std::unique_lock<std::mutex> sc(c.scratch_mu);
             SW_CUDA(cudaStreamWaitEvent(st, c.pipe_h2d[slot], 0));
-            cudaEvent_t done;
-            if (c.ivf) {  // single-buffered IVF scratch: everything on the caller's stream
-                if (c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(st, c.scratch_ev, 0));
-                int kn = plan_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed, sel, pol,
-                                   c.pipe_ch[slot], st);
-                launch_align_noise(c, c.pipe_ch[slot], c.pipe_req[slot], B, -1, nullptr,
-                                   philox_seed, d_out, t_out_max, st);
-                if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, st));
-                c.last_user_async = false;
-                c.last_kernels = kn + 1;
-                SW_CUDA(cudaEventRecord(c.pipe_planned[slot], st));
-                done = c.pipe_planned[slot];
-            } else {
-                const int par = c.async_st ? c.async_par : 0;
-                c.last_kernels = warmstart_async_impl(c, c.pipe_q[slot], c.pipe_req[slot], B,
-                                                      seed, sel, pol, nullptr, philox_seed,
-                                                      c.pipe_ch[slot], d_out, t_out_max, st);
-                done = c.async_done[par];
-            }
+            const int par = c.async_st ? c.async_par : 0;
+            c.last_kernels = warmstart_async_impl(c, c.pipe_q[slot], c.pipe_req[slot], B, seed,
+                                                  sel, pol, nullptr, philox_seed,
+                                                  c.pipe_ch[slot], d_out, t_out_max, st);
+            const cudaEvent_t done = c.async_done[par];
             SW_CUDA(cudaEventRecord(c.pipe_used[slot], c.async_st ? c.async_st : st));
             SW_CUDA(cudaStreamWaitEvent(c.pipe_out, done, 0));
             if (c.async_st) SW_CUDA(cudaStreamWaitEvent(c.pipe_out, c.pipe_used[slot], 0));
@@ -1047,15 +1037,6 @@ int sw_warmstart_async(sw_ctx* ctx, const float* d_q, const sw_request* d_req, i
         std::unique_lock<std::mutex> sc(c.scratch_mu);
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t S = as_stream(stream);
-        if (c.ivf) {  // probe ranks and list groups are single-buffered: no overlap in IVF mode
-            if (c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
-            int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, S);
-            launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, S);
-            if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, S));
-            c.last_user_async = false;
-            c.last_kernels = kn + 1;
-            return SW_OK;
-        }
         c.last_kernels = warmstart_async_impl(c, d_q, d_req, B, seed, sel, pol, d_eps,
                                               philox_seed, d_ch, d_out, t_out_max, S);
         return SW_OK;

@@ -230,6 +230,7 @@ struct Ctx {
     float* cta_topk_p[2] = {};
     int32_t* cand_slot_p[2] = {};
     float* cand_score_p[2] = {};
+    uint8_t* prank_p[2] = {};  // IVF probe ranks (read by the finish kernel)
     // pipelined host path (sw_warmstart_host_submit / _wait): kPipe staging slots, H2D on
     // pipe_in, D2H on pipe_out, so batch i+1's copies overlap batch i's kernels
     static constexpr int kPipe = 2;
