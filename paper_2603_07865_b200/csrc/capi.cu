@@ -879,6 +879,9 @@ static int warmstart_async_impl(Ctx& c, const float* d_q, const sw_request* d_re
     ensure_async(c);
     const int par = c.async_par;
     if (c.async_used[par]) SW_CUDA(cudaStreamWaitEvent(S, c.async_done[par], 0));
+    // the previous async call's prep + scoring may sit on another caller stream: the single-
+    // buffered scoring scratch (bf16 queries, thresholds, slice bests) is reused right away
+    if (c.async_used[par ^ 1]) SW_CUDA(cudaStreamWaitEvent(S, c.async_score_ev, 0));
     if (!c.last_user_async && c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
     set_par(c, par);
     const int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, S, c.async_st);
