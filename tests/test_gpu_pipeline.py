@@ -83,8 +83,8 @@ def _async_case(ivf=False):
     return c, wc, sel, pol, dev, nb, B, T, latent, qs, rqs, _lib
 
 
-@pytest.mark.parametrize("ivf", [False, True])
-def test_warmstart_async_matches_sync(ivf):
+@pytest.mark.parametrize("ivf,two_streams", [(False, False), (True, False), (False, True)])
+def test_warmstart_async_matches_sync(ivf, two_streams):
     """sw_warmstart_async (prep + scoring on the caller's stream, finish + align + noise on the
     context's stream under the next batch's scoring, alternating scratch parities) returns
     exactly sw_warmstart's choices and latents; a synchronous search after it sees the whole
@@ -106,10 +106,12 @@ def test_warmstart_async_matches_sync(ivf):
            for _ in range(nb)]
     outs = [torch.zeros((B, latent[0], T, latent[2]), dtype=torch.float32, device=dev)
             for _ in range(nb)]
+    side = torch.cuda.Stream(dev)
     for j in range(nb):
+        sj = side.cuda_stream if (two_streams and j % 2) else st  # callers on two streams
         _lib.check(L.sw_warmstart_async(wc._h, qs[j].data_ptr(), rqs[j].data_ptr(), B, 9,
                                         C.byref(sel.c()), C.byref(pol.c()), None, 4321,
-                                        chs[j].data_ptr(), outs[j].data_ptr(), T, st),
+                                        chs[j].data_ptr(), outs[j].data_ptr(), T, sj),
                    "sw_warmstart_async")
     hits_after, n_after = wc.search(qs[0].cpu().numpy(), 8)  # synchronous user after async ones
     _lib.check(L.sw_join(wc._h, st), "sw_join")
