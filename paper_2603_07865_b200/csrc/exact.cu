@@ -14,12 +14,6 @@ namespace sw {
 namespace {
 
 
-__device__ __forceinline__ double clamp_cos(double v) {
-    if (v > 1.0) v = 1.0;
-    if (v < -1.0) v = -1.0;
-    return v;
-}
-
 __global__ void k_prep(const float* __restrict__ q, int B, int D, int Dp,
                        __nv_bfloat16* __restrict__ q_bf, float* __restrict__ q_norm,
                        float* __restrict__ q_eps, const uint32_t* __restrict__ norms,

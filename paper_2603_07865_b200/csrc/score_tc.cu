@@ -441,13 +441,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (TS) {
             // this warp's 32 query rows -> TMEM lanes [32 quarter, +32), columns [2 TBN, 2 TBN +
             // Dp / 2): lane = query, column = bf16 pair (k, k+1) of the row, K-major
-            const uint4* qrow = reinterpret_cast<const uint4*>(
+            const uint4* qsrc = reinterpret_cast<const uint4*>(
                 p.q_bf + (int64_t)(qrow + quarter * 32 + lane) * (p.kch * 64));
             for (int cb = 0; cb < p.kch * 32; cb += 32) {
                 uint32_t v[32];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const uint4 w = __ldg(qrow + cb / 4 + u);
+                    const uint4 w = __ldg(qsrc + cb / 4 + u);
                     v[4 * u] = w.x;
                     v[4 * u + 1] = w.y;
                     v[4 * u + 2] = w.z;
@@ -813,7 +813,6 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     c.last_score_ts = false;
     p.experiment = 0;
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 512;
-    static bool attr_set = false;
     auto kern = [&](auto rp_tag, auto kl_tag) {
         constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
         auto kf = k_score_tc<RPv, KLv, false, false>;
@@ -823,7 +822,6 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
         kf<<<dim3((unsigned)std::min<int64_t>(max_items, c.num_sms), 1), THREADS, smem, st>>>(
             c.tm_qg, c.tm_sorted, p);
     };
-    (void)attr_set;
     SW_REQUIRE(c.Rp == 1, "grouped IVF search needs one row per entry");
     if (k <= 8)
         kern(std::integral_constant<int, 1>{}, std::integral_constant<int, 8>{});
