@@ -356,11 +356,19 @@ def main():
     # (4 B stages leave shared memory for a finish CTA per SM; align CTAs use none). The timed
     # region ends with sw_join. --no-overlap: sw_warmstart, everything on one stream.
     overlap = not args.no_overlap and not sharded
-    if overlap:
+    # sharded step, pipelined the same way (sw_local_topk_async): the finish, the gather,
+    # merge + select and owner align of batch i run on the context's stream under batch i+1's
+    # scoring (not in the gloo host-staged validation mode)
+    overlap_sh = not args.no_overlap and sharded and not staged
+    if overlap or overlap_sh:
         ch_ring = [torch.empty_like(choices) for _ in range(2)]
+    if overlap_sh:
+        a_ptr = Cc.c_void_p()
+        _lib.check(L_.sw_async_stream(wc._h, Cc.byref(a_ptr)), "sw_async_stream")
+        a_stream = torch.cuda.ExternalStream(a_ptr.value, device=dev)
 
     def join():
-        if overlap:
+        if overlap or overlap_sh:
             _lib.check(L_.sw_join(wc._h, sp), "sw_join")
 
     def step(i):
@@ -375,6 +383,25 @@ def main():
             _lib.check(L_.sw_warmstart(wc._h, q.data_ptr(), r.data_ptr(), B, 1, Cc.byref(csel),
                                        Cc.byref(cpol), None, 1234, choices.data_ptr(),
                                        out.data_ptr(), T_, sp), "sw_warmstart")
+        elif overlap_sh:
+            j = i % 2
+            _lib.check(L_.sw_local_topk_async(wc._h, q.data_ptr(), B, K, rank,
+                                              rec_local.data_ptr(), n_local_t.data_ptr(), sp),
+                       "sw_local_topk_async")
+            with torch.cuda.stream(a_stream):
+                if world == 1:
+                    rec_all.copy_(rec_local)
+                    n_all.copy_(n_local_t)
+                else:
+                    dist.all_gather_into_tensor(rec_all, rec_local)
+                    dist.all_gather_into_tensor(n_all, n_local_t)
+            _lib.check(L_.sw_merge_select(wc._h, rec_all.data_ptr(), n_all.data_ptr(), world,
+                                          q.data_ptr(), r.data_ptr(), B, K, 1, Cc.byref(csel),
+                                          Cc.byref(cpol), ch_ring[j].data_ptr(), a_ptr),
+                       "sw_merge_select")
+            _lib.check(L_.sw_align_noise_owned(wc._h, ch_ring[j].data_ptr(), r.data_ptr(), B,
+                                               rank, None, 1234, out.data_ptr(), T_, a_ptr),
+                       "align")
         else:
             _lib.check(L_.sw_local_topk(wc._h, q.data_ptr(), B, K, rank, rec_local.data_ptr(),
                                         n_local_t.data_ptr(), sp), "sw_local_topk")
@@ -443,6 +470,9 @@ def main():
     last_i = p_steps - 1  # the batch whose choices / requests the side measurements reuse
     score_alone_ms = None
     stage_ms_overlapped = None
+    if overlap_sh:
+        choices.copy_(ch_ring[last_i % 2])
+        torch.cuda.synchronize(dev)
     if overlap:
         choices.copy_(ch_ring[last_i % 2])
         torch.cuda.synchronize(dev)
@@ -769,7 +799,10 @@ def main():
                          % (n_rows * D * 2 / 1e6),
                    "latent_slots": min(args.latent_slots, n_local),
                    "pipelining": ("finish + align+noise of batch i on a second stream (sw_warmstart_async), overlapping batch "
-                                  "i+1's scoring" if overlap else "none (one stream)")},
+                                  "i+1's scoring" if overlap else
+                                  "finish + gather + merge/select + owner align of batch i on a "
+                                  "second stream (sw_local_topk_async), overlapping batch i+1's "
+                                  "scoring" if overlap_sh else "none (one stream)")},
         **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
         "roofline": {"bound": "tensor",
                      "kernel": "k_score_tc (tcgen05.mma %s, TMA)" % (

@@ -314,6 +314,13 @@ int sw_local_topk(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, int
                   void* d_records, int32_t* d_n, void* stream);
 /* Deterministic merge of world x (B x k) gathered records (sim desc, id asc) followed by
  * score_candidates / select / gater / t* (replicated on every rank; no broadcast needed). */
+/* Pipelined sw_local_topk: prep + scoring on `stream`; the finish and the record copies on the
+ * context's async stream (sw_async_stream), where the caller also enqueues the all-gather,
+ * sw_merge_select and sw_align_noise_owned of the same batch — they then overlap the next
+ * batch's scoring. sw_join closes the pipeline. */
+int sw_local_topk_async(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, int32_t rank,
+                        void* d_records, int32_t* d_n, void* stream);
+int sw_async_stream(sw_ctx* ctx, void** stream);
 int sw_merge_select(sw_ctx* ctx, const void* d_gathered, const int32_t* d_gathered_n,
                     int32_t world, const float* d_queries, const sw_request* d_reqs, int32_t B,
                     int32_t k, uint64_t seed, const sw_selector_config* sel,

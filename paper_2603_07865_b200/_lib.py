@@ -126,6 +126,8 @@ def lib() -> C.CDLL:
         "sw_warmstart_async": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
                                 C.POINTER(SwPolicy), vp, u64, vp, vp, i32, vp], C.c_int),
         "sw_join": ([vp, vp], C.c_int),
+        "sw_local_topk_async": ([vp, vp, i32, i32, i32, vp, vp, vp], C.c_int),
+        "sw_async_stream": ([vp, C.POINTER(vp)], C.c_int),
         "sw_warmstart_host_submit": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
                                       C.POINTER(SwPolicy), u64, vp, vp, i32, vp,
                                       C.POINTER(C.c_int64)], C.c_int),
@@ -189,6 +191,7 @@ EXPORTED = [
     "sw_arena_fill_synthetic", "sw_arena_read_rows", "sw_search", "sw_search_host", "sw_plan",
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host",
     "sw_warmstart_host_submit", "sw_warmstart_host_wait", "sw_warmstart_async", "sw_join",
+    "sw_local_topk_async", "sw_async_stream",
     "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",

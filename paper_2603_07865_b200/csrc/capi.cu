@@ -1105,6 +1105,54 @@ int sw_local_topk(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, int32_t r
     });
 }
 
+// Sharded step, pipelined like sw_warmstart_async: prep + scoring on `stream`, the finish (local
+// exact top-k, no select) and the record copies on the context's async stream, whose handle
+// sw_async_stream returns — the caller enqueues the gather, sw_merge_select and
+// sw_align_noise_owned there, and they overlap the next batch's scoring.
+int sw_local_topk_async(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, int32_t rank,
+                        void* d_records, int32_t* d_n, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_q && d_records && d_n)), "null argument");
+        SW_REQUIRE(k >= 1 && k <= kMaxTopK, "k must be in [1, 32]");
+        Ctx& c = ctx->c;
+        std::shared_lock<std::shared_mutex> rd(c.mu);
+        std::unique_lock<std::mutex> sc(c.scratch_mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        cudaStream_t S = as_stream(stream);
+        ensure_async(c);
+        const int par = c.async_par;
+        if (c.async_used[par]) SW_CUDA(cudaStreamWaitEvent(S, c.async_done[par], 0));
+        if (c.async_used[par ^ 1]) SW_CUDA(cudaStreamWaitEvent(S, c.async_score_ev, 0));
+        if (!c.last_user_async && c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
+        set_par(c, par);
+        const int kn = launch_search_fused(c, d_q, B, k, rank, nullptr, nullptr, nullptr, S,
+                                           c.async_st);
+        SW_CUDA(cudaMemcpy2DAsync(d_records, sizeof(HitRec) * k, c.hits, sizeof(HitRec) * kMaxTopK,
+                                  sizeof(HitRec) * k, B, cudaMemcpyDeviceToDevice, c.async_st));
+        SW_CUDA(cudaMemcpyAsync(d_n, c.nhits, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice,
+                                c.async_st));
+        SW_CUDA(cudaEventRecord(c.async_done[par], c.async_st));
+        if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, c.async_st));
+        c.async_used[par] = true;
+        c.async_par = par ^ 1;
+        c.last_user_async = true;
+        c.last_kernels = kn;
+        return SW_OK;
+    });
+}
+
+int sw_async_stream(sw_ctx* ctx, void** stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && stream, "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock<std::mutex> sc(c.scratch_mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        ensure_async(c);
+        *stream = reinterpret_cast<void*>(c.async_st);
+        return SW_OK;
+    });
+}
+
 int sw_merge_select(sw_ctx* ctx, const void* d_gathered, const int32_t* d_gn, int32_t world,
                     const float* d_q, const sw_request* d_req, int32_t B, int32_t k,
                     uint64_t seed, const sw_selector_config* sel, const sw_policy* pol,

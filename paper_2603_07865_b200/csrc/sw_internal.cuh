@@ -265,7 +265,9 @@ struct HotGuard {
     HotGuard(Ctx& c_, cudaStream_t st_) : rd(c_.mu), sc(c_.scratch_mu), c(c_), st(st_) {
         cudaSetDevice(c.device);
         if (c.scratch_ev) cudaStreamWaitEvent(st, c.scratch_ev, 0);
-        c.last_user_async = false;
+        // a call enqueued on the async stream (the sharded merge / align after
+        // sw_local_topk_async) is part of that pipeline, not a synchronous user
+        if (st != c.async_st) c.last_user_async = false;
     }
     ~HotGuard() {
         if (c.scratch_ev) cudaEventRecord(c.scratch_ev, st);

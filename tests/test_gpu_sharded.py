@@ -13,8 +13,8 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.mark.parametrize("tc", [False, True])
-def test_two_shards_equal_single_context(tc):
+@pytest.mark.parametrize("tc,async_topk", [(False, False), (True, False), (True, True)])
+def test_two_shards_equal_single_context(tc, async_topk):
     import ctypes as C
 
     from paper_2603_07865_b200.warmstart import Policy, SelectorConfig, WarmStartCache, requests
@@ -55,8 +55,14 @@ def test_two_shards_equal_single_context(tc):
     for r, wc in enumerate(shards):
         rec = torch.empty(B * k * 128, dtype=torch.uint8, device=dev)
         n = torch.empty(B, dtype=torch.int32, device=dev)
-        _lib.check(_lib.lib().sw_local_topk(wc._h, qd.data_ptr(), B, k, r, rec.data_ptr(),
-                                            n.data_ptr(), st), "local_topk")
+        if async_topk:  # finish + record copies on the shard's own stream, joined back
+            _lib.check(_lib.lib().sw_local_topk_async(wc._h, qd.data_ptr(), B, k, r,
+                                                      rec.data_ptr(), n.data_ptr(), st),
+                       "local_topk_async")
+            _lib.check(_lib.lib().sw_join(wc._h, st), "join")
+        else:
+            _lib.check(_lib.lib().sw_local_topk(wc._h, qd.data_ptr(), B, k, r, rec.data_ptr(),
+                                                n.data_ptr(), st), "local_topk")
         recs.append(rec)
         cnts.append(n)
     rec_all = torch.cat(recs)
