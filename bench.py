@@ -435,9 +435,20 @@ def main():
 
     steps = 3 if args.profile_only else args.steps
     warm = max(3, args.warmup) if not args.profile_only else 2
-    for i in range(warm):
-        step(i)
-    barrier()
+    pipeline_note = None
+    try:
+        for i in range(warm):
+            step(i)
+        barrier()
+    except Exception as e:  # the overlapped sharded step (NCCL on the context stream) as insurance
+        if not overlap_sh:
+            raise
+        pipeline_note = f"pipelined sharded step failed in warm-up ({type(e).__name__}: {e}); one stream"
+        overlap_sh = False
+        torch.cuda.synchronize(dev)
+        for i in range(warm):
+            step(i)
+        barrier()
     # timed region: only the dominant kernel carries stage events (2 per step), so `value` is
     # not inflated by event records between the other launches
     wc.profile(True, stages=["score_tc"])
@@ -816,7 +827,7 @@ def main():
                                   "i+1's scoring" if overlap else
                                   "finish + gather + merge/select + owner align of batch i on a "
                                   "second stream (sw_local_topk_async), overlapping batch i+1's "
-                                  "scoring" if overlap_sh else "none (one stream)")},
+                                  "scoring" if overlap_sh else (pipeline_note or "none (one stream)"))},
         **({"validation_only": "gloo host-staged gather, all ranks on one GPU"} if staged else {}),
         "roofline": (roof_ivf if ivf else {"bound": "tensor",
                      "kernel": "k_score_tc (tcgen05.mma %s, TMA)" % (
