@@ -524,7 +524,7 @@ def main():
         qh = [torch.empty((B, D), dtype=torch.float32).pin_memory() for _ in range(n_pool)]
         rh = [torch.empty((B * 24,), dtype=torch.uint8).pin_memory() for _ in range(n_pool)]
         chh = [torch.empty((B * CHOICE_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
-               for _ in range(2)]
+               for _ in range(3)]
         for j in range(n_pool):
             qh[j].copy_(qpool[j].cpu())
             rh[j].copy_(reqs[j].cpu())
@@ -544,18 +544,21 @@ def main():
             j = i % n_pool
             _lib.check(L_.sw_warmstart_host_submit(
                 wc._h, qh[j].data_ptr(), rh[j].data_ptr(), B, 1, Cc.byref(csel), Cc.byref(cpol),
-                1234, chh[i % 2].data_ptr(), out.data_ptr(), T_, sp, Cc.byref(tk)),
+                1234, chh[i % 3].data_ptr(), out.data_ptr(), T_, sp, Cc.byref(tk)),
                 "sw_warmstart_host_submit")
             return tk.value
 
+        depth = 2  # batches waited for behind the newest submission (3 in flight)
+
         def run_pipelined(n):
-            prev = None
+            pend = []
             for i in range(n):
-                t = psubmit(i)
-                if prev is not None:
-                    _lib.check(L_.sw_warmstart_host_wait(wc._h, prev), "sw_warmstart_host_wait")
-                prev = t
-            _lib.check(L_.sw_warmstart_host_wait(wc._h, prev), "sw_warmstart_host_wait")
+                pend.append(psubmit(i))
+                if len(pend) > depth:
+                    _lib.check(L_.sw_warmstart_host_wait(wc._h, pend.pop(0)),
+                               "sw_warmstart_host_wait")
+            for t in pend:
+                _lib.check(L_.sw_warmstart_host_wait(wc._h, t), "sw_warmstart_host_wait")
 
         e_steps = max(20, steps // 2)
 
@@ -579,7 +582,7 @@ def main():
         e2e = {"value": round(B / (e2e_ms / 1000.0), 1), "unit": "requests/s",
                "h2d_bytes_per_step": B * D * 4 + B * 24,
                "d2h_bytes_per_step": B * CHOICE_DTYPE.itemsize, "ms_per_step": round(e2e_ms, 4),
-               "path": "sw_warmstart_host_submit/_wait, 2 batches in flight (pinned host "
+               "path": "sw_warmstart_host_submit/_wait, 3 batches in flight (pinned host "
                        "prompts/requests -> choices; H2D/D2H on copy streams)",
                "sync_call": {"value": round(B / (sync_ms / 1000.0), 1),
                              "ms_per_step": round(sync_ms, 4),

@@ -298,7 +298,8 @@ int sw_warmstart_host(sw_ctx* ctx, const float* queries, const sw_request* reqs,
  * stream), the plan (on `stream`), the align + noise (the context's align stream, so it runs
  * under the next batch's scoring kernel) and the D2H of the choices (own copy stream), and
  * returns a ticket at once; sw_warmstart_host_wait(ticket) blocks until `choices` has landed
- * and `d_out` is written. Up to two submissions overlap; `queries`, `reqs` and `choices` must
+ * and `d_out` is written. Up to three submissions are in flight; `queries`, `reqs` and
+ * `choices` must
  * stay valid (and should be pinned) until the wait returns. Results are identical to
  * sw_warmstart_host's. */
 int sw_warmstart_host_submit(sw_ctx* ctx, const float* queries, const sw_request* reqs,

@@ -233,7 +233,7 @@ struct Ctx {
     uint8_t* prank_p[2] = {};  // IVF probe ranks (read by the finish kernel)
     // pipelined host path (sw_warmstart_host_submit / _wait): kPipe staging slots, H2D on
     // pipe_in, D2H on pipe_out, so batch i+1's copies overlap batch i's kernels
-    static constexpr int kPipe = 2;
+    static constexpr int kPipe = 3;
     std::mutex pipe_mu;
     int64_t pipe_seq = 0;
     cudaStream_t pipe_in = nullptr, pipe_out = nullptr, pipe_al = nullptr;
