@@ -89,6 +89,8 @@ struct FinSmem {
     int n, ovf, nh, emitted;
     long long t_ta, t_sync;
     double u;  // the request's selector draw (computed by warp 1 during phase A)
+    uint32_t tsv[256];  // wide-grid T_a: each warp's survivors (>= its local k-th best)
+    int tsn;
 };
 
 __device__ __forceinline__ bool before(double as, uint64_t aid, double bs, uint64_t bid) {
@@ -197,6 +199,29 @@ __device__ __forceinline__ double chain_dot_any(const float4* __restrict__ rp,
     return s;
 }
 
+// k-th largest key (duplicates counted) of a warp's register-held ordered keys (0 = no value):
+// descending distinct keys by a warp max (REDUX) below the previous one, then a warp count of
+// its copies. 0 when fewer than k keys are real. Warp-uniform result.
+template <int NV>
+__device__ __forceinline__ uint32_t kth_key(const uint32_t (&key)[NV], int k) {
+    const unsigned full = 0xffffffffu;
+    uint32_t prev = 0xFFFFFFFFu;
+    int total = 0;
+    for (;;) {
+        uint32_t lm = 0u;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) lm = max(lm, key[u] < prev ? key[u] : 0u);
+        const uint32_t cur = __reduce_max_sync(full, lm);
+        if (cur == 0u) return 0u;
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) c += key[u] == cur ? 1 : 0;
+        total += (int)__reduce_add_sync(full, (unsigned)c);
+        prev = cur;
+        if (total >= k) return cur;
+    }
+}
+
 // k-th largest (duplicates counted) of the m <= 32 NV values tk[(i / k) * kMaxTopK + i % k],
 // by descending distinct values: a warp max (REDUX) of the keys below the previous one, then a
 // warp count of its copies. -inf when fewer than k values are real. Warp-uniform result.
@@ -279,7 +304,58 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
             }
             if (lane == 0) S.pre[p.n_chunks] = carry;
         }
-        if (warp == 0) {  // T_a over the union of the scoring CTAs' final lists
+        bool ta_done = false;
+        if constexpr (FTT >= 256) {
+            // wide grids (small batches: 148 slices x k): the 8 warps each take 256 of the
+            // m <= 2048 slice scores, keep those >= their local k-th best (a superset of the
+            // global top-k), and warp 0 selects the exact k-th largest among the survivors
+            const int m = p.n_chunks * p.k;
+            if (m > 32 * 16 && m <= 8 * 256) {
+                const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
+                if (t == 0) S.tsn = 0;
+                const bool pow2 = (p.k & (p.k - 1)) == 0;
+                const int lk = __ffs(p.k) - 1;
+                uint32_t key[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = warp * 256 + lane + 32 * u;
+                    key[u] = 0u;
+                    if (i < m) {
+                        const int sl = pow2 ? i >> lk : i / p.k;
+                        const float v = tk[sl * kMaxTopK + (i - sl * p.k)];
+                        if (v != -INFINITY) key[u] = f2ord(v);
+                    }
+                }
+                __syncthreads();  // S.tsn reset
+                const uint32_t lw = kth_key<8>(key, p.k);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (key[u] != 0u && key[u] >= lw) {
+                        const int pos = atomicAdd(&S.tsn, 1);
+                        if (pos < 256) S.tsv[pos] = key[u];
+                    }
+                __syncthreads();
+                if (S.tsn <= 256) {  // else (many ties) the single-warp path below
+                    if (warp == 0) {
+                        const int ns = S.tsn;
+                        uint32_t sv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int i = lane + 32 * u;
+                            sv[u] = i < ns ? S.tsv[i] : 0u;
+                        }
+                        const uint32_t c = kth_key<8>(sv, p.k);
+                        const float kth = c ? ord2f(c) : -INFINITY;
+                        if (lane == 0) {
+                            S.cut = kth - 2.0f * p.q_eps[b];
+                            S.t_ta = clock64();
+                        }
+                    }
+                    ta_done = true;
+                }
+            }
+        }
+        if (warp == 0 && !ta_done) {  // T_a over the union of the scoring CTAs' final lists
             const int m = p.n_chunks * p.k;
             const float* tk = p.cta_topk + (int64_t)b * p.n_chunks * kMaxTopK;
             float kth = -INFINITY;
