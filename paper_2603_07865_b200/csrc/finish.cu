@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
                 const float4* rp4 = reinterpret_cast<const float4*>(p.rows + row * p.Df);
                 if (fast_phi) {
                     switch (p.D) {
-                        case 512: s = chain_dot_phi<128, 8>(rp4, qd, phi); break;
+                        // 16 float4 in flight per lane where registers allow (the 8-warp
+                        // small-batch CTAs: B=1 phase B 28K -> 22K cycles); 8 in the 2-warp
+                        // CTAs held to 128 registers (16 measured 30K -> 40K there)
+                        case 512: s = chain_dot_phi<128, (FTT >= 256 ? 16 : 8)>(rp4, qd, phi); break;
                         case 256: s = chain_dot_phi<64, 8>(rp4, qd, phi); break;
                         case 128: s = chain_dot_phi<32, 4>(rp4, qd, phi); break;
                         default: s = chain_dot_phi<16, 2>(rp4, qd, phi); break;
