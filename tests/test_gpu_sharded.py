@@ -88,3 +88,66 @@ def test_two_shards_equal_single_context(tc, async_topk):
         _lib.check(_lib.lib().sw_align_noise_owned(wc._h, got_buf.data_ptr(), rd.data_ptr(), B,
                                                    r, None, 9, out.data_ptr(), 256, st), "owned")
     np.testing.assert_array_equal(out.cpu().numpy(), out_ref)
+
+
+def test_pipelined_sharded_step_one_rank_equals_warmstart():
+    """The bench's pipelined sharded step at world 1: sw_local_topk_async, then the 'gather'
+    (a copy), sw_merge_select and sw_align_noise_owned enqueued on the context's async stream
+    (sw_async_stream), several batches back to back — equal to sw_warmstart per batch."""
+    import ctypes as C
+
+    from paper_2603_07865_b200.warmstart import Policy, SelectorConfig, WarmStartCache, requests
+    B, k, dim, T = 256, 8, 128, 64
+    c = SynthCache(20000, dim, 1.0, seed=35, clustered=True)
+    wc = WarmStartCache(dim, rows_per_entry=1, max_entries=20000, max_batch=B,
+                        latent_shape=(4, 64, 16), latent_slots=4096, tc_always=True)
+    wc.insert_batch(c.ids, c.off, c.rows, c.levels, c.starts, c.lengths)
+    sel, pol = SelectorConfig(k), Policy("exploit")
+    L = _lib.lib()
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream(dev).cuda_stream
+    a_ptr = C.c_void_p()
+    _lib.check(L.sw_async_stream(wc._h, C.byref(a_ptr)), "sw_async_stream")
+    a_stream = torch.cuda.ExternalStream(a_ptr.value, device=dev)
+    nb = 4
+    qs, rqs, ref_ch, ref_lat = [], [], [], []
+    for j in range(nb):
+        q = torch.from_numpy(perturbed_queries(c, B, frac_random=0.1, seed=50 + j)).to(dev)
+        rq = requests(np.arange(1 + j * B, 1 + (j + 1) * B, dtype=np.uint64),
+                      request_durations(B, 4.0, 10.0, seed=60 + j), np.full(B, 100, np.int32))
+        rqd = torch.from_numpy(rq.view(np.uint8)).to(dev)
+        qs.append(q)
+        rqs.append(rqd)
+        ch = torch.zeros(B * _lib.CHOICE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        out = torch.zeros((B, 4, T, 16), dtype=torch.float32, device=dev)
+        _lib.check(L.sw_warmstart(wc._h, q.data_ptr(), rqd.data_ptr(), B, 1, C.byref(sel.c()),
+                                  C.byref(pol.c()), None, 77, ch.data_ptr(), out.data_ptr(), T,
+                                  st), "sw_warmstart")
+        ref_ch.append(ch.cpu().numpy().view(_lib.CHOICE_DTYPE))
+        ref_lat.append(out.cpu().numpy())
+    rec = torch.empty(B * k * 128, dtype=torch.uint8, device=dev)
+    n = torch.empty(B, dtype=torch.int32, device=dev)
+    rec_all, n_all = torch.empty_like(rec), torch.empty_like(n)
+    chs = [torch.zeros(B * _lib.CHOICE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+           for _ in range(nb)]
+    outs = [torch.zeros((B, 4, T, 16), dtype=torch.float32, device=dev) for _ in range(nb)]
+    for j in range(nb):
+        _lib.check(L.sw_local_topk_async(wc._h, qs[j].data_ptr(), B, k, 0, rec.data_ptr(),
+                                         n.data_ptr(), st), "sw_local_topk_async")
+        with torch.cuda.stream(a_stream):
+            rec_all.copy_(rec)
+            n_all.copy_(n)
+        _lib.check(L.sw_merge_select(wc._h, rec_all.data_ptr(), n_all.data_ptr(), 1,
+                                     qs[j].data_ptr(), rqs[j].data_ptr(), B, k, 1,
+                                     C.byref(sel.c()), C.byref(pol.c()), chs[j].data_ptr(),
+                                     a_ptr), "sw_merge_select")
+        _lib.check(L.sw_align_noise_owned(wc._h, chs[j].data_ptr(), rqs[j].data_ptr(), B, 0,
+                                          None, 77, outs[j].data_ptr(), T, a_ptr), "align")
+    _lib.check(L.sw_join(wc._h, st), "sw_join")
+    torch.cuda.synchronize(dev)
+    for j in range(nb):
+        got = chs[j].cpu().numpy().view(_lib.CHOICE_DTYPE)
+        assert ref_ch[j]["hit"].any()
+        for f in ("hit", "arm", "steps_skipped", "entry_id", "similarity"):
+            np.testing.assert_array_equal(got[f], ref_ch[j][f], err_msg=f"batch {j} {f}")
+        np.testing.assert_array_equal(outs[j].cpu().numpy(), ref_lat[j])
