@@ -35,3 +35,29 @@ def test_reference_arm_json_contract():
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0
     assert e["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_ours_arm_json_contract():
+    """The default arm on a small cache: every key the driver reads, with the kernel roofline,
+    the pipelined e2e (H2D + D2H counted), the launch count and the clock sample."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--entries", "20000",
+                          "--steps", "5", "--warmup", "3", "--no-vocoder", "--no-batcher",
+                          "--no-cpu-baseline", "--no-latency"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [x for x in out.stdout.splitlines() if x.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 4 * d["steps"]
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
