@@ -40,7 +40,8 @@ extern "C" {
 /* sw_choice.flags */
 #define SW_CHOICE_AMBIGUOUS_DRAW 0x1u  /* |acc - target| within exp() ulp slack (H3) */
 #define SW_CHOICE_NONFINITE_PHI 0x2u   /* non-finite features -> arm 0 (gater.cpp:71-76) */
-#define SW_CHOICE_INCOMPLETE 0x4u      /* candidate buffer overflow: search not certified */
+#define SW_CHOICE_INCOMPLETE 0x4u      /* search not certified (never set: overflowing queries
+                                          are re-searched exactly, see sw_overflow_stats) */
 #define SW_CHOICE_AMBIGUOUS_ARM 0x8u   /* explore-mode softplus within ulp slack of a tie */
 
 typedef struct sw_ctx sw_ctx;
@@ -164,6 +165,9 @@ int sw_arena_replace(sw_ctx* ctx, uint64_t entry_id, int32_t n_rows, const float
                      const sw_segment* segs, const float* latent, int32_t t_src);
 int64_t sw_arena_entry_count(const sw_ctx* ctx);  /* IvfIndex::entry_count (index.hpp:74) */
 int sw_arena_contains(const sw_ctx* ctx, uint64_t entry_id); /* index.hpp:75 */
+/* Entry slots the arena holds: max_entries + 1 (CacheManager::admit inserts before it evicts,
+ * cache.cpp:30-52) rounded up to whole 256-row tiles. */
+int64_t sw_arena_capacity(const sw_ctx* ctx);
 /* Benchmark fill: n entries with ids first_id.. of seeded iid unit rows generated on the
  * device (Philox normals, fp64 normalise, fp32 round), durations U[4,12] s, pyramid rows per
  * the context's rows_per_entry, latents N(0,1). Deterministic in seed. */
@@ -250,7 +254,10 @@ int64_t sw_swem_read(const char* path, float* out, int64_t cap_floats, int32_t* 
 
 /* ---------------------------------------------------------------- batched hot path
  * IvfIndex::search (index.cpp:289-326) in exhaustive mode for B queries: exact fp64 cosine,
- * best segment per entry, (sim desc, id asc), truncated to k. d_out: B x k, d_n: B. */
+ * best segment per entry, (sim desc, id asc), truncated to k. d_out: B x k, d_n: B. Always
+ * certified: queries whose tcgen05 candidate slices overflow are re-searched by exact brute
+ * force on the device. (A negative d_n[b] = -n - 1 would flag an uncertified result;
+ * sw_search_host turns it into SW_ERUNTIME.) */
 int sw_search(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, sw_hit* d_out,
               int32_t* d_n, void* stream);
 int sw_search_host(sw_ctx* ctx, const float* queries, int32_t B, int32_t k, sw_hit* out,
@@ -364,6 +371,10 @@ int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats);
  * pairs with the queries resident in TMEM). */
 int sw_last_launch_info(const sw_ctx* ctx, int32_t* kernels, int32_t* used_tensor_cores,
                         int32_t* candidates_max);
+/* Queries so far whose tcgen05 candidate slices overflowed and that the certified fallback (an
+ * exact fp64 brute-force IvfIndex::search of the whole arena) answered instead. Results are
+ * exact either way; this counts how often the slow path ran. Synchronizes the device. */
+int sw_overflow_stats(sw_ctx* ctx, int64_t* fallback_queries);
 
 /* ---------------------------------------------------------------- Cache Manager (host policy)
  * CacheManager (cache.hpp:45-106) over a context's arena: the policy stays on the host exactly

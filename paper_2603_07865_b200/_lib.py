@@ -175,6 +175,8 @@ def lib() -> C.CDLL:
         "sw_swix_save": ([vp, C.c_char_p], C.c_int),
         "sw_swem_read": ([C.c_char_p, vp, i64, C.POINTER(i32), C.POINTER(i32)], i64),
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+        "sw_overflow_stats": ([vp, C.POINTER(C.c_int64)], C.c_int),
+        "sw_arena_capacity": ([vp], C.c_int64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -195,6 +197,7 @@ EXPORTED = [
     "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
+    "sw_overflow_stats", "sw_arena_capacity",
     "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",
     "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
     "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",

@@ -85,7 +85,7 @@ static void free_ctx(Ctx& c) {
                     c.slice_cnt, c.cta_topk, c.dbg, c.tsrc,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
-                    c.cand_list, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
+                    c.cand_list, c.ovf_state, c.ovf_ring, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
                     c.cent, c.row_list, c.prank, c.pmask, c.d_sorted_slot, c.d_rows_sorted,
                     c.d_sorted_vbits, c.d_list_tile0, c.d_list_ntiles, c.d_qcnt, c.d_qlist,
                     c.d_qbase, c.d_qg, c.d_qmap, c.d_items, c.d_voc};
@@ -124,9 +124,11 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     c.Rp = next_pow2(cfg.rows_per_entry);
     c.logRp = 0;
     while ((1 << c.logRp) < c.Rp) ++c.logRp;
-    // round capacity up to whole 256-row tiles so TMA boxes never straddle the allocation
+    // round capacity up to whole 256-row tiles so TMA boxes never straddle the allocation. One
+    // spare slot beyond max_entries: CacheManager::admit inserts BEFORE it evicts (cache.cpp:
+    // 30-52), so a full cache holds capacity + 1 entries for the duration of an admit.
     const int64_t per_tile = std::max(1, 256 / c.Rp);
-    c.S = (cfg.max_entries + per_tile - 1) / per_tile * per_tile;
+    c.S = (cfg.max_entries + 1 + per_tile - 1) / per_tile * per_tile;
     c.C = cfg.latent_c;
     c.Tmax = cfg.latent_t_max;
     c.F = cfg.latent_f;
@@ -164,6 +166,16 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.cand_row, (size_t)c.Bmax * kCandCap);
     dalloc(&c.cand_list, (size_t)c.Bmax * kCandCap);
     dalloc(&c.hits, (size_t)c.Bmax * kMaxTopK);
+    {
+        const int64_t chunks = (c.Bmax + kOvfQG - 1) / kOvfQG;
+        const size_t words = (size_t)kOvfHdr + (size_t)c.Bmax + 2 * (size_t)chunks;
+        dalloc(&c.ovf_state, words);
+        SW_CUDA(cudaMemset(c.ovf_state, 0, sizeof(int32_t) * words));
+        int nsm = 0;
+        SW_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        const size_t rec = 16;  // {double sim, int32 slot, int32 row}
+        SW_CUDA(cudaMalloc(&c.ovf_ring, rec * kOvfRing * kOvfQG * (size_t)nsm * kOvfWarps * kMaxTopK));
+    }
     dalloc(&c.nhits, (size_t)c.Bmax);
     dalloc(&c.d_q_stage, (size_t)c.Bmax * c.D);
     dalloc(&c.d_req_stage, (size_t)c.Bmax);
@@ -249,6 +261,13 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
                    "entry has more rows than the arena's rows_per_entry");
         pending[h_ids[e]] += (int32_t)nr;
     }
+    // slots: every id not yet in the arena takes one; check they exist before any mutation
+    // (a partial batch would leave ids in slot_of whose rows were never written)
+    int64_t new_ids = 0;
+    for (const auto& kv : pending)
+        if (!c.slot_of.count(kv.first)) ++new_ids;
+    if ((int64_t)c.free_slots.size() + (c.S - c.high_water) < new_ids)
+        throw Error(SW_ENOMEM, "arena full (max_entries reached)");
     for (int64_t e = 0; e < n; ++e) {
         const int64_t nr = h_off[e + 1] - h_off[e];
         auto it = c.slot_of.find(h_ids[e]);
@@ -546,6 +565,8 @@ int64_t sw_arena_entry_count(const sw_ctx* ctx) {
     return (int64_t)ctx->c.slot_of.size();
 }
 
+int64_t sw_arena_capacity(const sw_ctx* ctx) { return ctx ? ctx->c.S : 0; }
+
 int sw_arena_contains(const sw_ctx* ctx, uint64_t id) {
     if (!ctx) return 0;
     std::shared_lock lk(ctx->c.mu);
@@ -808,6 +829,12 @@ int sw_search_host(sw_ctx* ctx, const float* q, int32_t B, int32_t k, sw_hit* ou
             SW_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
             SW_CUDA(cudaStreamSynchronize(st));
             rc = SW_OK;
+            for (int b = 0; b < B; ++b)
+                if (n[b] < 0) {  // never expected: the fallback certifies every overflow
+                    n[b] = -n[b] - 1;
+                    set_last_error("search result not certified (candidate overflow)");
+                    rc = SW_ERUNTIME;
+                }
         }
         cudaStreamDestroy(st);
         cudaFree(d_out);
@@ -1287,6 +1314,19 @@ int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats) {
         SW_CUDA(cudaSetDevice(ctx->c.device));
         SW_CUDA(cudaDeviceSynchronize());
         SW_CUDA(cudaMemcpy(stats, ctx->c.dbg, sizeof(int32_t) * 8 * B, cudaMemcpyDeviceToHost));
+        return SW_OK;
+    });
+}
+
+int sw_overflow_stats(sw_ctx* ctx, int64_t* fallback_queries) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && fallback_queries, "null argument");
+        Ctx& c = ctx->c;
+        SW_CUDA(cudaSetDevice(c.device));
+        SW_CUDA(cudaDeviceSynchronize());
+        unsigned long long v = 0;
+        SW_CUDA(cudaMemcpy(&v, c.ovf_state + 2, sizeof(v), cudaMemcpyDeviceToHost));
+        *fallback_queries = (int64_t)v;
         return SW_OK;
     });
 }

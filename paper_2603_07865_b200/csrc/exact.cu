@@ -65,9 +65,11 @@ __global__ void k_hits_to_public(int B, int k, const HitRec* __restrict__ hits,
                                  int32_t* __restrict__ out_n) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
-    int nh = nhits[b];
-    if (nh < 0) nh = -nh - 1;
-    out_n[b] = nh;
+    // a negative count (-n - 1) would mark an uncertified result; the certified-overflow
+    // fallback (k_overflow) rewrites every such query first, so it is passed through as-is
+    const int code = nhits[b];
+    const int nh = code < 0 ? -code - 1 : code;
+    out_n[b] = code;
     for (int i = 0; i < nh; ++i) {
         const HitRec& h = hits[(int64_t)b * kMaxTopK + i];
         sw_hit o;

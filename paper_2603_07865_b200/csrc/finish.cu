@@ -71,6 +71,17 @@ struct FinishParams {
     int ivf;                  // IVF mode: rows outside the query's probed lists do not count
     const int16_t* row_list;  // [rows] list of each stored row
     const uint8_t* prank;     // [B][kMaxCentroids] probe rank of each list (255: not probed)
+    // certified-overflow fallback (k_overflow)
+    int32_t* ovf;             // state: header, flagged queries [bmax], chunk done / merged flags
+    struct OvfRec* ovf_ring;  // [kOvfRing][kOvfQG][n_warps][kMaxTopK]
+    int bmax;
+};
+
+// One entry of a fallback top-k list: exact clamped similarity, arena slot, best pyramid row.
+struct OvfRec {
+    double sim;
+    int32_t slot;
+    int32_t row;
 };
 
 struct FinSmem {
@@ -696,6 +707,9 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
     }
     const int nh_code = S.ovf ? -nh - 1 : nh;
     if (t == 0) p.nhits[b] = nh_code;
+    // an overflowing slice dropped candidates: hand the query to the exact fallback (k_overflow,
+    // next on this stream), which replaces its records and choice with a certified result
+    if (t == 0 && S.ovf) p.ovf[kOvfHdr + atomicAdd(&p.ovf[0], 1)] = b;
     __syncthreads();
     {  // copy the smem records out (16-byte words)
         const int nw = nh * (int)(sizeof(HitRec) / 16);
@@ -721,6 +735,262 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
         if (!p.implicit_all) {  // phase A split: T_a selection, barrier wait
             d[6] = (int32_t)(S.t_ta - t_start);
             d[7] = (int32_t)(S.t_sync - t_start);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Certified-overflow fallback. A query whose candidate slices overflowed (more emissions than a
+// slice holds, e.g. thousands of identical rows in its range) lost candidates, so k_finish's
+// result for it is not certified. This kernel recomputes such queries exactly: every stored row's
+// fp64 sequential dot (core.cpp:26-37), best row per entry by strict '>' in list order
+// (index.cpp:306-311), top-k by (sim desc, id asc) (index.cpp:320-324) — IvfIndex::search by
+// brute force, so it is correct for any data. kOvfQG flagged queries per pass share each row
+// read (kOvfQG independent chains per lane). Each warp keeps its own top-k lists (lane i holds
+// the i-th best); they go to a ring in global memory and the LAST CTA to finish a pass merges
+// them, enriches the hits (segment, s_neg, gater block sums) and re-runs the gate / select /
+// gater for those queries — replacing k_finish's records, count and choice. With no flagged
+// query (the normal case) every CTA returns at once.
+// ------------------------------------------------------------------------------------------
+struct WL {  // lane-distributed sorted list entry
+    double s;
+    uint64_t id;
+    int32_t slot, row;
+};
+
+__device__ __forceinline__ void wl_empty(WL& l) {
+    l.s = -INFINITY;
+    l.id = ~0ull;
+    l.slot = -1;
+    l.row = 0;
+}
+
+// inserts the warp-uniform candidate (s, id, slot, row) into the k-entry list (no-op if it is not
+// before the k-th entry); the list stays sorted by (sim desc, id asc)
+__device__ __forceinline__ void wl_insert(WL& l, double s, uint64_t id, int slot, int row, int k,
+                                          int lane) {
+    const unsigned full = 0xffffffffu;
+    const bool cb = lane < k && before(s, id, l.s, l.id);
+    const unsigned m = __ballot_sync(full, cb);
+    if (!m) return;
+    const int pos = __ffs(m) - 1;  // sorted: every lane from pos on is after the candidate
+    const double us = __shfl_up_sync(full, l.s, 1);
+    const uint64_t uid = __shfl_up_sync(full, l.id, 1);
+    const int uslot = __shfl_up_sync(full, l.slot, 1);
+    const int urow = __shfl_up_sync(full, l.row, 1);
+    if (lane == pos) {
+        l.s = s;
+        l.id = id;
+        l.slot = slot;
+        l.row = row;
+    } else if (lane > pos && lane < k) {
+        l.s = us;
+        l.id = uid;
+        l.slot = uslot;
+        l.row = urow;
+    }
+}
+
+// offers each lane's candidate (valid where `has`) to the list, lowest lane first
+__device__ __forceinline__ void wl_offer(WL& l, bool has, double s, uint64_t id, int slot, int row,
+                                         int k, int lane) {
+    const unsigned full = 0xffffffffu;
+    const double ks = __shfl_sync(full, l.s, k - 1);
+    const uint64_t kid = __shfl_sync(full, l.id, k - 1);
+    unsigned m = __ballot_sync(full, has && before(s, id, ks, kid));
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        wl_insert(l, __shfl_sync(full, s, src), __shfl_sync(full, id, src),
+                  __shfl_sync(full, slot, src), __shfl_sync(full, row, src), k, lane);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kOvfWarps, 1) k_overflow(const FinishParams p) {
+    extern __shared__ double qd[];  // [Df][kOvfQG] flagged queries as doubles, dimension-major
+    __shared__ uint8_t prs[kOvfQG][kMaxCentroids];
+    __shared__ int last;
+    const unsigned full = 0xffffffffu;
+    const int nflag = __ldcg(&p.ovf[0]);
+    if (nflag == 0) return;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int nwarps = gridDim.x * kOvfWarps, gw = blockIdx.x * kOvfWarps + warp;
+    const int nchunks = (nflag + kOvfQG - 1) / kOvfQG;
+    const int chunk_cap = (p.bmax + kOvfQG - 1) / kOvfQG;
+    int32_t* done = p.ovf + kOvfHdr + p.bmax;  // [chunk_cap] CTAs finished with the pass
+    int32_t* merged = done + chunk_cap;         // [chunk_cap] pass merged (its ring slot free)
+    const int64_t rows_total = p.n_slots << p.logRp;
+    const int k = p.k;
+    for (int c = 0; c < nchunks; ++c) {
+        const int nq = min(kOvfQG, nflag - c * kOvfQG);
+        int qb[kOvfQG];
+#pragma unroll
+        for (int j = 0; j < kOvfQG; ++j) qb[j] = j < nq ? __ldcg(&p.ovf[kOvfHdr + c * kOvfQG + j]) : -1;
+        __syncthreads();  // the previous pass is done with qd / prs
+        for (int i = t; i < p.Df * kOvfQG; i += blockDim.x) {
+            const int d = i / kOvfQG, j = i - d * kOvfQG;
+            qd[i] = (qb[j] >= 0 && d < p.D) ? (double)p.q[(int64_t)qb[j] * p.D + d] : 0.0;
+        }
+        if (p.ivf)
+            for (int i = t; i < kOvfQG * kMaxCentroids; i += blockDim.x) {
+                const int j = i / kMaxCentroids, l = i - j * kMaxCentroids;
+                prs[j][l] = qb[j] >= 0 ? p.prank[(int64_t)qb[j] * kMaxCentroids + l] : kNotProbed;
+            }
+        __syncthreads();
+        WL L[kOvfQG];
+#pragma unroll
+        for (int j = 0; j < kOvfQG; ++j) wl_empty(L[j]);
+        // ---- scan: warp gw takes 32-row groups gw, gw + nwarps, ...; lane = row
+        for (int64_t g = gw; g * 32 < rows_total; g += nwarps) {
+            const int64_t row = g * 32 + lane;
+            const int64_t slot = row >> p.logRp;
+            const int r = (int)(row & (p.Rp - 1));
+            const bool ok = row < rows_total && p.valid[slot] && r < p.nrows[slot];
+            double s[kOvfQG];
+#pragma unroll
+            for (int j = 0; j < kOvfQG; ++j) s[j] = 0.0;
+            if (ok) {
+                const float4* rp4 = reinterpret_cast<const float4*>(p.rows + row * p.Df);
+                const double2* q2 = reinterpret_cast<const double2*>(qd);
+#pragma unroll 2
+                for (int i4 = 0; i4 < (p.Df >> 2); ++i4) {
+                    const float4 x = __ldg(rp4 + i4);
+                    const double xs[4] = {(double)x.x, (double)x.y, (double)x.z, (double)x.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {  // dimension 4 i4 + u, in order
+#pragma unroll
+                        for (int j2 = 0; j2 < kOvfQG / 2; ++j2) {
+                            const double2 qq = q2[(4 * i4 + u) * (kOvfQG / 2) + j2];
+                            s[2 * j2] = fma(qq.x, xs[u], s[2 * j2]);
+                            s[2 * j2 + 1] = fma(qq.y, xs[u], s[2 * j2 + 1]);
+                        }
+                    }
+                }
+            }
+            int l = -1;
+            if (ok && p.ivf) l = p.row_list[row];
+            uint64_t id = 0;
+            if (ok && r == 0) id = p.ids[slot];
+#pragma unroll
+            for (int j = 0; j < kOvfQG; ++j) {
+                bool el = ok && j < nq;
+                int key = r;
+                if (el && p.ivf) {  // rows of lists the query does not probe are not scanned
+                    const int pr = l >= 0 ? prs[j][l] : kNotProbed;
+                    el = pr != kNotProbed;
+                    key = (pr << 6) | r;  // scan order: probe rank, then pyramid row
+                }
+                double sim = el ? fmin(1.0, fmax(-1.0, s[j])) : -DBL_MAX;  // core.cpp:35-36
+                int kw = el ? key : 0x7fffffff;
+                for (int o = 1; o < p.Rp; o <<= 1) {  // best row: max, ties -> lowest key
+                    const double os = __shfl_xor_sync(full, sim, o);
+                    const int ok2 = __shfl_xor_sync(full, kw, o);
+                    if (os > sim || (os == sim && ok2 < kw)) {
+                        sim = os;
+                        kw = ok2;
+                    }
+                }
+                const bool has = r == 0 && kw != 0x7fffffff;
+                wl_offer(L[j], has, sim, id, (int)slot, kw & 63, k, lane);
+            }
+        }
+        // ---- this warp's lists -> ring slot c % kOvfRing (free once pass c - kOvfRing merged)
+        if (c >= kOvfRing) {
+            if (lane == 0)
+                while (atomicAdd(&merged[c - kOvfRing], 0) == 0) __nanosleep(256);
+            __syncwarp();
+        }
+        OvfRec* ring = p.ovf_ring + (int64_t)(c % kOvfRing) * kOvfQG * nwarps * kMaxTopK;
+#pragma unroll
+        for (int j = 0; j < kOvfQG; ++j)
+            if (lane < k) {
+                OvfRec o;
+                o.sim = L[j].s;
+                o.slot = L[j].slot;
+                o.row = L[j].row;
+                ring[((int64_t)j * nwarps + gw) * kMaxTopK + lane] = o;
+            }
+        __threadfence();
+        __syncthreads();
+        if (t == 0) last = atomicAdd(&done[c], 1) == (int)gridDim.x - 1;
+        __syncthreads();
+        if (!last) continue;
+        __threadfence();  // every CTA's lists are visible
+        // ---- merge (warp j: query j of the pass), enrich, select
+        if (warp < nq) {
+            const int j = warp, b = qb[j];
+            WL F;
+            wl_empty(F);
+            for (int i0 = 0; i0 < nwarps * k; i0 += 32) {
+                const int i = i0 + lane;
+                double os = -INFINITY;
+                int oslot = -1, orow = 0;
+                if (i < nwarps * k) {  // L2 reads: the lists were written by other CTAs
+                    const OvfRec* o = ring + ((int64_t)j * nwarps + i / k) * kMaxTopK + i % k;
+                    os = __ldcg(&o->sim);
+                    oslot = __ldcg(&o->slot);
+                    orow = __ldcg(&o->row);
+                }
+                const bool has = oslot >= 0;
+                const uint64_t id = has ? p.ids[oslot] : ~0ull;
+                wl_offer(F, has, os, id, oslot, orow, k, lane);
+            }
+            const int nh = __popc(__ballot_sync(full, lane < k && F.slot >= 0));
+            // enrichment (phase D): segment, s_neg, owner; then the 8 gater block sums
+            HitRec* hb = p.hits + (int64_t)b * kMaxTopK;
+            if (lane < nh) {
+                const int64_t row = (int64_t)F.slot * p.Rp + F.row;
+                const sw_segment sg = p.segs[row];
+                HitRec& o = hb[lane];
+                o.sim = F.s;
+                o.entry_id = F.id;
+                o.level = sg.level;
+                o.slot = F.slot;
+                o.start_s = sg.start_s;
+                o.length_s = sg.length_s;
+                o.s_neg = p.sneg[row];
+                o.row = F.row;
+                o.owner = p.rank;
+            }
+            __syncwarp();
+            // block sums: each lane computes (hit h, block blk) pairs; slots and rows from the list
+            for (int base = 0; base < nh * 8; base += 32) {
+                const int hj = base + lane;
+                const int h = min(hj >> 3, 31);
+                const int slot_h = __shfl_sync(full, F.slot, h);
+                const int row_h = __shfl_sync(full, F.row, h);
+                if (hj < nh * 8) {
+                    const int blk = hj & 7;
+                    const float* rp = p.rows + ((int64_t)slot_h * p.Rp + row_h) * p.Df;
+                    const size_t lo = (size_t)blk * p.D / 8, hi = (size_t)(blk + 1) * p.D / 8;
+                    double bs = 0.0;
+                    for (size_t i = lo; i < hi; ++i) bs = fma(qd[i * kOvfQG + j], (double)rp[i], bs);
+                    hb[h].phi[blk] = bs;
+                }
+            }
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) p.nhits[b] = nh;
+            if (p.do_select) {
+                const double u = dev::uniform_draw(dev::derive_seed(p.sp.seed, p.reqs[b].id, 2, 0));
+                const sw_choice ch = dev::select_warp(hb, nh, u, p.reqs[b], p.sp, lane);
+                if (lane == 0) p.out[b] = ch;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            atomicExch(&merged[c], 1);
+            if (atomicAdd(&p.ovf[1], 1) == nchunks - 1) {  // the last pass: reset for the next batch
+                for (int i = 0; i < nchunks; ++i) {
+                    done[i] = 0;
+                    merged[i] = 0;
+                }
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.ovf + 2), (unsigned long long)nflag);
+                p.ovf[1] = 0;
+                __threadfence();
+                atomicExch(&p.ovf[0], 0);
+            }
         }
     }
 }
@@ -808,6 +1078,9 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.ivf = ivf ? 1 : 0;
     p.row_list = c.row_list;
     p.prank = c.prank;
+    p.ovf = c.ovf_state;
+    p.ovf_ring = reinterpret_cast<OvfRec*>(c.ovf_ring);
+    p.bmax = c.Bmax;
     c.last_ivf = ivf;
     if (st_finish != st) {
         SW_CUDA(cudaEventRecord(c.async_score_ev, st));
@@ -822,22 +1095,24 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
         }();
         const size_t smem =
             sizeof(double) * c.Df + (ring ? sizeof(float) * NWARP * NST * 32 * SP : 0);
-        static size_t attr = 0;
-        if (smem > attr) {
-            SW_CUDA(cudaFuncSetAttribute(k_finish<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            SW_CUDA(cudaFuncSetAttribute(k_finish<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            SW_CUDA(cudaFuncSetAttribute(k_finish<false, 256>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = smem;
-        }
+        ensure_smem_attr(c, k_finish<true>, smem);
+        ensure_smem_attr(c, k_finish<false>, smem);
+        ensure_smem_attr(c, k_finish<false, 256>, smem);
         if (ring)
             k_finish<true><<<B, FT, smem, st>>>(p);
         else if (B <= 64)
             k_finish<false, 256><<<B, 256, smem, st>>>(p);
         else
             k_finish<false><<<B, FT, smem, st>>>(p);
+        SW_CUDA(cudaGetLastError());
+        if (tc) {
+            // certified fallback for queries whose candidate slices overflowed (returns at once
+            // when none did); ~18 KB of shared memory, so it co-runs with the next scoring kernel
+            const size_t osmem = sizeof(double) * (size_t)c.Df * kOvfQG;
+            ensure_smem_attr(c, k_overflow, osmem);
+            k_overflow<<<c.num_sms, 32 * kOvfWarps, osmem, st>>>(p);
+            ++kernels;
+        }
     }
     SW_CUDA(cudaGetLastError());
     c.last_tc = tc ? (c.last_score_ts ? 3 : c.last_score_pair ? 2 : 1) : 0;  // 2: pairs, 3: +TS

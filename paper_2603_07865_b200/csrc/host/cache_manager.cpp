@@ -190,6 +190,8 @@ extern "C" {
 
 int swcm_create(sw_ctx* ctx, int32_t dim, const swcm_config* cfg, swcm_cache** out) {
     if (!ctx || !cfg || !out || dim < 1 || cfg->capacity < 1) return SW_EINVAL;
+    // admit inserts before it evicts (cache.cpp:30-52): the arena must hold capacity + 1 entries
+    if (sw_arena_capacity(ctx) < (int64_t)cfg->capacity + 1) return SW_ENOMEM;
     auto* h = new swcm_cache;
     h->ctx = ctx;
     h->dim = dim;
@@ -212,7 +214,7 @@ int swcm_admit(swcm_cache* h, const float* clip_embedding, double duration_s,
     if (quality < h->cfg.quality_floor) return 0;  // rejected: not an error
     if (!(duration_s > 0.0)) return SW_EINVAL;     // pyramid_segments (index.cpp:17-19)
     Entry e;
-    e.id = h->next_id++;
+    e.id = h->next_id;
     e.duration_s = duration_s;
     if (prompt_embedding) e.prompt.assign(prompt_embedding, prompt_embedding + h->dim);
     e.quality = quality;
@@ -221,7 +223,8 @@ int swcm_admit(swcm_cache* h, const float* clip_embedding, double duration_s,
     e.admitted_h = now_h;
     const std::vector<float> full(clip_embedding, clip_embedding + h->dim);
     int rc = h->write_rows(false, e.id, full, duration_s, latent, t_src);
-    if (rc < 0) return rc;
+    if (rc < 0) return rc;  // nothing stored: the id is not consumed
+    ++h->next_id;
     const uint64_t id = e.id;
     h->entries.emplace(id, std::move(e));
     rc = h->evict_if_full(now_h, h->last_evicted);
@@ -312,10 +315,10 @@ int swcm_refine(swcm_cache* h, uint64_t id, uint64_t rng_seed, swcm_regenerate_f
         }
     }
     if (best_q <= e.quality) return SW_OK;
-    e.quality = best_q;
     const int rc = h->write_rows(true, e.id, best_emb, e.duration_s,
                                  lat_cap && best_t > 0 ? best_lat.data() : nullptr, best_t);
-    if (rc < 0) return rc;
+    if (rc < 0) return rc;  // the ledger keeps the quality the arena still holds
+    e.quality = best_q;
     e.recent_skips.clear();
     *replaced = 1;
     return SW_OK;

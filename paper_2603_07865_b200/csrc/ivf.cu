@@ -821,16 +821,8 @@ bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st) {
     {
         const int G = 256 / cp, DH = cp <= 64 ? 192 : cp == 128 ? 96 : 48;
         const size_t smem = sizeof(double) * ((size_t)DH * (cp + 1) + (size_t)G * DH + 256);
-        // one flag per instantiation: the four kernels share a function-pointer type, so a
-        // static inside this (generic) lambda would be shared by all of them
-        static bool attr_set[4] = {false, false, false, false};
-        const int ai = cp == 32 ? 0 : cp == 64 ? 1 : cp == 128 ? 2 : 3;
         auto launch = [&](auto kern) {
-            if (!attr_set[ai]) {
-                SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024));
-                attr_set[ai] = true;
-            }
+            ensure_smem_attr(c, kern, (size_t)200 * 1024);  // per context (= per device)
             kern<<<(B + G - 1) / G, 256, smem, st>>>(d_q, B, c.D, c.cent, c.Df, c.ivf_C, np,
                                                      c.prank, c.pmask);
         };

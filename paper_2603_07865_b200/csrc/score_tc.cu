@@ -721,13 +721,8 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32
 
 template <int RP, int KL, bool PAIR, bool TS>
 void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-    static bool attr_set = false;
     auto kern = k_score_tc<RP, KL, PAIR, TS>;
-    if (!attr_set) {
-        SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     c.smem_optin));
-        attr_set = true;
-    }
+    ensure_smem_attr(c, kern, (size_t)c.smem_optin);
     if (PAIR) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
@@ -816,8 +811,7 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     auto kern = [&](auto rp_tag, auto kl_tag) {
         constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
         auto kf = k_score_tc<RPv, KLv, false, false>;
-        SW_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     c.smem_optin));
+        ensure_smem_attr(c, kf, (size_t)c.smem_optin);
         // persistent: one CTA per SM walks the items (max_items only bounds the grid)
         kf<<<dim3((unsigned)std::min<int64_t>(max_items, c.num_sms), 1), THREADS, smem, st>>>(
             c.tm_qg, c.tm_sorted, p);

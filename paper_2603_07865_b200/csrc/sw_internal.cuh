@@ -50,6 +50,13 @@ constexpr int kMaxSlices = 2 * 148;   // (scoring CTA, epilogue group) emission 
 constexpr int kMaxRowsPad = 32;       // delta >= 1/16 -> at most 31 rows (index.cpp:20-21)
 constexpr int kMaxCentroids = 256;    // IVF lists (index.centroids; reference default 64)
 constexpr uint8_t kNotProbed = 255;   // probe-rank sentinel
+// Certified-overflow fallback: queries whose candidate slices overflowed are re-searched by an
+// exact fp64 scan of the whole arena, kOvfQG queries per pass, one k_overflow CTA of kOvfWarps
+// warps per SM. State header: [0] flagged count, [1] chunks merged, [2..3] lifetime total (u64).
+constexpr int kOvfQG = 4;
+constexpr int kOvfWarps = 8;
+constexpr int kOvfRing = 4;
+constexpr int kOvfHdr = 4;
 // Certified error of a tcgen05 score: |q.e - q~.e~| <= |q| |e - e~| + |q - q~| |e~|
 // (Cauchy-Schwarz on q.e - q~.e~ = q.(e - e~) + (q - q~).e~, ~ = bf16) plus the fp32 tensor-core
 // accumulation slack kAccSlack * |q~| |e~| (K <= 512 additions at <= 2^-23 relative each, x2).
@@ -142,6 +149,10 @@ struct Ctx {
     double* cand_exact = nullptr;   // [Bmax][kCandCap]
     int32_t* cand_row = nullptr;    // [Bmax][kCandCap]
     int32_t* cand_list = nullptr;   // [Bmax][kCandCap] compacted certified candidates
+    // certified-overflow fallback (finish.cu k_overflow): flagged queries, chunk counters and
+    // the ring of per-warp exact top-k lists (see kOvf* below)
+    int32_t* ovf_state = nullptr;   // [kOvfHdr + Bmax + 2 * ovf_chunks]
+    void* ovf_ring = nullptr;       // [kOvfRing][kOvfQG][num_sms * kOvfWarps][kMaxTopK] records
     HitRec* hits = nullptr;         // [Bmax][kMaxTopK]
     int32_t* nhits = nullptr;       // [Bmax]
     float* d_q_stage = nullptr;     // [Bmax][D] (host e2e staging)
@@ -252,7 +263,21 @@ struct Ctx {
     int64_t prof_n[SW_NUM_STAGES] = {};
     // last launch info
     int last_kernels = 0, last_tc = 0, last_cand_max = 0;
+    // dynamic shared-memory opt-ins already applied on this context's device (the attribute is
+    // per device, so it cannot be a process-wide static)
+    std::mutex attr_mu;
+    std::map<const void*, size_t> smem_attr;
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (context, kernel, size high-water).
+template <class K>
+inline void ensure_smem_attr(Ctx& c, K* kern, size_t bytes) {
+    std::lock_guard<std::mutex> lk(c.attr_mu);
+    size_t& have = c.smem_attr[reinterpret_cast<const void*>(kern)];
+    if (bytes <= have) return;
+    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+}
 
 // Reader guard of the hot path: shared with other readers against arena mutations, exclusive
 // with them on the batch scratch (host enqueue under scratch_mu, device work after the previous

@@ -381,8 +381,7 @@ const int32_t* launch_align_vocoder(Ctx& c, const sw_choice* d_ch, const sw_requ
     const size_t smem = sizeof(double2) * n + 2 * sizeof(double) * nat_bound;
     SW_REQUIRE(smem <= 200 * 1024, "vocoder alignment: stretched latent too long for smem");
     auto go = [&](auto kern) {
-        SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+        ensure_smem_attr(c, kern, smem);
         kern<<<dim3(c.C * c.F, B), VT, smem, st>>>(c.latent, vr, c.C, c.Tmax, c.F, t_out_max,
                                                     d_out, n, logn, hop_a, tb.window, tb.tw_fwd,
                                                     tb.tw_inv);

@@ -81,6 +81,37 @@ class SynthCache:
         return self.rows[self.off[e]:self.off[e + 1]]
 
 
+def clustered_rows(n: int, dim: int = 512, seed: int = 1, n_clusters: int = 16,
+                   spread: float = 0.5, dup_rate: float = 0.9, dup_spread: float = 0.16,
+                   block: int = 65536) -> np.ndarray:
+    """Vectorised §8d(ii) clustered near-duplicates at any size: like SynthCache(clustered=True)
+    (16 centres, spread 0.5, dup rate 0.9, dup spread 0.16; synth_workload, simgen.hpp:87-98),
+    except that a duplicate's parent is drawn from the rows of EARLIER blocks (the first block
+    is generated row by row), so 1M rows take seconds instead of minutes."""
+    rng = np.random.default_rng(seed)
+    centres = normalize_rows(rng.standard_normal((n_clusters, dim)))
+    out = np.empty((n, dim), np.float32)
+    first = min(n, 256)
+    for i in range(first):
+        if i > 0 and rng.random() < dup_rate:
+            base, s = out[int(rng.integers(0, i))], dup_spread
+        else:
+            base, s = centres[i % n_clusters], spread
+        g = normalize_rows(rng.standard_normal((1, dim)))[0]
+        out[i] = normalize_rows((base.astype(np.float64) + s * g)[None])[0]
+    i0 = first
+    while i0 < n:
+        m = min(block, n - i0, i0)
+        dup = rng.random(m) < dup_rate
+        parent = rng.integers(0, i0, m)
+        base = np.where(dup[:, None], out[parent], centres[(np.arange(i0, i0 + m)) % n_clusters])
+        sc = np.where(dup, dup_spread, spread)[:, None]
+        g = normalize_rows(rng.standard_normal((m, dim), dtype=np.float32))
+        out[i0:i0 + m] = normalize_rows(base.astype(np.float64) + sc * g.astype(np.float64))
+        i0 += m
+    return out
+
+
 def perturbed_queries(cache: SynthCache, B: int, scale: float = 0.3, seed: int = 7,
                       frac_random: float = 0.0) -> np.ndarray:
     """perturb(row, scale) of random cached full embeddings (core.cpp:116-124 shape)."""

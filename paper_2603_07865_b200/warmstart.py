@@ -247,6 +247,15 @@ class WarmStartCache:
         check(_lib.lib().sw_debug_query_stats(self._h, B, ptr(out)), "query_stats")
         return out
 
+    def overflow_fallbacks(self) -> int:
+        """Queries so far answered by the certified exact fallback (candidate overflow)."""
+        v = C.c_int64()
+        check(_lib.lib().sw_overflow_stats(self._h, C.byref(v)), "sw_overflow_stats")
+        return v.value
+
+    def arena_capacity(self) -> int:
+        return int(_lib.lib().sw_arena_capacity(self._h))
+
     def launch_info(self):
         k, t, m = C.c_int32(), C.c_int32(), C.c_int32()
         _lib.lib().sw_last_launch_info(self._h, C.byref(k), C.byref(t), C.byref(m))
@@ -271,7 +280,10 @@ class WarmStartCache:
         st = torch.cuda.current_stream(q.device).cuda_stream
         check(_lib.lib().sw_search(self._h, ptr(q), B, k, ptr(out), ptr(n), st), "sw_search")
         hits = out.cpu().numpy().view(HIT_DTYPE).reshape(B, k)
-        return hits, n.cpu().numpy()
+        n = n.cpu().numpy()
+        if (n < 0).any():  # never expected: overflowing queries are re-searched exactly
+            raise RuntimeError("search result not certified (candidate overflow)")
+        return hits, n
 
     def search_host(self, queries: np.ndarray, k: int):
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
