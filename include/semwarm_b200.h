@@ -36,6 +36,8 @@ extern "C" {
 /* sw_config.flags */
 #define SW_FLAG_EXACT_ONLY 0x1u   /* never use the tcgen05 pre-filter: fp64 brute force only */
 #define SW_FLAG_TC_ALWAYS 0x2u    /* use the tcgen05 pre-filter even for tiny caches (tests) */
+#define SW_FLAG_GROW 0x4u         /* inserts grow a full arena (capacity doubles) instead of
+                                     failing — the unbounded IvfIndex the C++ adapter mirrors */
 
 /* sw_choice.flags */
 #define SW_CHOICE_AMBIGUOUS_DRAW 0x1u  /* |acc - target| within exp() ulp slack (H3) */
@@ -168,6 +170,19 @@ int sw_arena_contains(const sw_ctx* ctx, uint64_t entry_id); /* index.hpp:75 */
 /* Entry slots the arena holds: max_entries + 1 (CacheManager::admit inserts before it evicts,
  * cache.cpp:30-52) rounded up to whole 256-row tiles. */
 int64_t sw_arena_capacity(const sw_ctx* ctx);
+/* Grows the arena to at least max_entries (+1 spare) entry slots, keeping every entry. */
+int sw_arena_reserve(sw_ctx* ctx, int64_t max_entries);
+/* IvfIndex::total_vectors (index.hpp:70): stored rows over all entries. */
+int64_t sw_arena_row_count(const sw_ctx* ctx);
+/* Host copy of `count` live entries starting at the first-th in slot order: ids, row counts,
+ * and (if non-NULL) rows [count][rows_per_entry_pad][D] fp32 and segs [count][pad]. Returns the
+ * number copied. For checkers and re-layouts; synchronous. */
+int64_t sw_arena_export(sw_ctx* ctx, int64_t first, int64_t count, uint64_t* ids,
+                        int32_t* nrows, float* rows, sw_segment* segs);
+/* IvfIndex::check_consistent (index.cpp:334-343) + the arena bookkeeping: 1 if every stored row
+ * is in exactly the list of its nearest centroid (recomputed on the device in fp64), per-entry
+ * row counts match the index ledger and the validity flags match the id map, else 0. */
+int sw_index_check_consistent(sw_ctx* ctx);
 /* Benchmark fill: n entries with ids first_id.. of seeded iid unit rows generated on the
  * device (Philox normals, fp64 normalise, fp32 round), durations U[4,12] s, pyramid rows per
  * the context's rows_per_entry, latents N(0,1). Deterministic in seed. */
@@ -184,6 +199,13 @@ int sw_arena_read_rows(sw_ctx* ctx, uint64_t entry_id, float* rows, int32_t n_ro
  * Empty arena only. centroids < 1 -> SW_EINVAL (index.cpp:191); at most 256 lists. */
 int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t rebuild_interval,
                      uint64_t seed);
+/* IvfIndex::set_rebuild_interval (index.hpp:76; pipeline.cpp:81). */
+int sw_ivf_set_rebuild_interval(sw_ctx* ctx, uint64_t rebuild_interval);
+/* IvfIndex::build(vecs, C, seed, nprobe) with non-empty vecs (index.cpp:186-208) on a configured,
+ * empty arena: bulk-inserts the entries (no mutation counting), then k-means over the rows in
+ * the given order with the configured seed itself; C is reduced to the row count. */
+int sw_ivf_build(sw_ctx* ctx, int64_t n, const uint64_t* ids, const int64_t* row_off,
+                 const float* rows, const sw_segment* segs);
 /* IvfIndex::set_nprobe (index.hpp:74). */
 int sw_ivf_set_nprobe(sw_ctx* ctx, int32_t nprobe);
 /* IvfIndex::rebuild (index.cpp:257-283): k-means++ and Lloyd over every stored row in
@@ -262,6 +284,10 @@ int sw_search(sw_ctx* ctx, const float* d_queries, int32_t B, int32_t k, sw_hit*
               int32_t* d_n, void* stream);
 int sw_search_host(sw_ctx* ctx, const float* queries, int32_t B, int32_t k, sw_hit* out,
                    int32_t* n);
+/* IvfIndex::search(q, k, nprobe) (index.hpp:67): nprobe > 0 overrides the index's nprobe for
+ * this call (0: the index's own). Host buffers, synchronous, no allocation per call. */
+int sw_search_host_ex(sw_ctx* ctx, const float* queries, int32_t B, int32_t k, int32_t nprobe,
+                      sw_hit* out, int32_t* n);
 
 /* Pipeline::plan_request + pick_arm + t* (pipeline.cpp:91-202, simgen.cpp:70) for B requests:
  * search -> score_candidates -> select (Rng(derive_seed(seed, id, 2)), pipeline.cpp:211) ->
@@ -344,6 +370,20 @@ int sw_align_noise_owned(sw_ctx* ctx, const sw_choice* d_choices, const sw_reque
 int sw_score_select_host(sw_ctx* ctx, int32_t n, const double* sims, const double* s_neg,
                          const double* durations, double L, const sw_selector_config* sel,
                          uint64_t rng_seed, double* scores_out, int32_t* pick);
+/* score_candidates (selector.cpp:24-58) alone: n <= 32 candidates with their index similarity,
+ * matched-segment embedding (n x dim) and duration; s_neg = clamp01(cos(audio, negative)) with
+ * `negative` (dim floats) or, if NULL, the context's negative embedding. Writes n x {s_pos,
+ * s_neg, a, b, q}. */
+int sw_score_candidates_host(sw_ctx* ctx, int32_t n, int32_t dim, const double* sims,
+                             const float* audio, const double* durations, double L,
+                             const float* negative, double* scores_out);
+/* select (selector.cpp:60-85) alone, given the gate scores and the caller's draw
+ * u = rng.uniform() (a caller draws it only when some q >= threshold, as the reference does).
+ * *pick = chosen index or -1; *flags = SW_CHOICE_AMBIGUOUS_DRAW if the cumulative weight lands
+ * within exp()'s ulp slack of the target. */
+int sw_select_host(sw_ctx* ctx, int32_t n, const double* s_pos, const double* q,
+                   double temperature, double threshold, double u, int32_t* pick,
+                   uint32_t* flags);
 /* context_features + choose_arm (gater.cpp:13-92) for B (prompt, segment) pairs. */
 int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const int32_t* T,
                   int32_t B, int32_t explore, double* phi_out, int32_t* arm_out);

@@ -23,6 +23,7 @@ SW_WARN_UNKNOWN_ID = 1
 
 SW_FLAG_EXACT_ONLY = 0x1
 SW_FLAG_TC_ALWAYS = 0x2
+SW_FLAG_GROW = 0x4
 
 SW_CHOICE_AMBIGUOUS_DRAW = 0x1
 SW_CHOICE_NONFINITE_PHI = 0x2
@@ -177,6 +178,15 @@ def lib() -> C.CDLL:
         "sw_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
         "sw_overflow_stats": ([vp, C.POINTER(C.c_int64)], C.c_int),
         "sw_arena_capacity": ([vp], C.c_int64),
+        "sw_arena_reserve": ([vp, i64], C.c_int),
+        "sw_arena_row_count": ([vp], C.c_int64),
+        "sw_arena_export": ([vp, i64, i64, vp, vp, vp, vp], C.c_int64),
+        "sw_index_check_consistent": ([vp], C.c_int),
+        "sw_ivf_set_rebuild_interval": ([vp, u64], C.c_int),
+        "sw_ivf_build": ([vp, i64, vp, vp, vp, vp], C.c_int),
+        "sw_search_host_ex": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
+        "sw_score_candidates_host": ([vp, i32, i32, vp, vp, vp, f64, vp, vp], C.c_int),
+        "sw_select_host": ([vp, i32, vp, vp, f64, f64, f64, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -197,7 +207,9 @@ EXPORTED = [
     "sw_local_topk", "sw_merge_select",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
-    "sw_overflow_stats", "sw_arena_capacity",
+    "sw_overflow_stats", "sw_arena_capacity", "sw_arena_reserve", "sw_arena_row_count",
+    "sw_arena_export", "sw_index_check_consistent", "sw_ivf_set_rebuild_interval", "sw_ivf_build",
+    "sw_search_host_ex", "sw_score_candidates_host", "sw_select_host",
     "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",
     "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
     "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",

@@ -105,6 +105,8 @@ static void free_ctx(Ctx& c) {
     if (c.pipe_out) cudaStreamDestroy(c.pipe_out);
     if (c.pipe_al) cudaStreamDestroy(c.pipe_al);
     if (c.mstream) cudaStreamDestroy(c.mstream);
+    if (c.host_st) cudaStreamDestroy(c.host_st);
+    if (c.host_stage) cudaFree(c.host_stage);
 }
 
 static void create(Ctx& c, const sw_config& cfg, int device) {
@@ -217,6 +219,50 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     SW_CUDA(cudaEventCreateWithFlags(&c.scratch_ev, cudaEventDisableTiming));
 }
 
+// Reallocates a device array from n_old to n_new elements, keeping the first n_old and
+// filling the tail with byte `fill`.
+template <class T>
+static void regrow(T** p, size_t n_old, size_t n_new, int fill) {
+    T* q = nullptr;
+    dalloc(&q, n_new);
+    if (*p && n_old) SW_CUDA(cudaMemcpy(q, *p, sizeof(T) * n_old, cudaMemcpyDeviceToDevice));
+    SW_CUDA(cudaMemset(q + n_old, fill, sizeof(T) * (n_new - n_old)));
+    if (*p) cudaFree(*p);
+    *p = q;
+}
+
+// Grows the arena to hold at least `entries` entries (+1 spare, whole tiles): every per-slot and
+// per-row array is reallocated and copied, the TMA descriptors re-encoded. Caller holds c.mu
+// exclusively with no reader in flight.
+static void grow_arena(Ctx& c, int64_t entries) {
+    const int64_t per_tile = std::max(1, 256 / c.Rp);
+    const int64_t S2 = (entries + 1 + per_tile - 1) / per_tile * per_tile;
+    if (S2 <= c.S) return;
+    const int64_t S = c.S, nrow = S * c.Rp, nrow2 = S2 * c.Rp;
+    regrow(&c.rows, (size_t)nrow * c.Df, (size_t)nrow2 * c.Df, 0);
+    regrow(&c.rows_bf, (size_t)nrow * c.Dp, (size_t)nrow2 * c.Dp, 0);
+    regrow(&c.sneg, (size_t)nrow, (size_t)nrow2, 0);
+    regrow(&c.segs, (size_t)nrow, (size_t)nrow2, 0);
+    regrow(&c.row_list, (size_t)nrow, (size_t)nrow2, 0xFF);
+    regrow(&c.ids, (size_t)S, (size_t)S2, 0);
+    regrow(&c.nrows, (size_t)S, (size_t)S2, 0);
+    regrow(&c.valid, (size_t)S, (size_t)S2, 0);
+    regrow(&c.tsrc, (size_t)S, (size_t)S2, 0);
+    regrow(&c.valid_bits, (size_t)(S / 32 + 16), (size_t)(S2 / 32 + 16), 0);
+    const int64_t L2 = c.cfg.latent_slots > 0 ? std::min<int64_t>(c.cfg.latent_slots, S2) : S2;
+    if (c.latent && L2 != c.Lslots) {  // slot % Lslots is unchanged for every stored slot
+        const size_t per = (size_t)c.C * c.Tmax * c.F;
+        regrow(&c.latent, (size_t)c.Lslots * per, (size_t)L2 * per, 0);
+    }
+    c.Lslots = L2;
+    c.S = S2;
+    c.h_nrows.resize((size_t)S2, 0);
+    c.ivf_rows.resize((size_t)S2, 0);
+    c.grp_dirty = true;
+    const int major_ok = c.tc_ok;
+    c.tc_ok = major_ok && encode_tensor_maps(c);
+}
+
 // Reserve slots for n new entries (lowest free slot first) and update host bookkeeping.
 static int64_t take_slot(Ctx& c) {
     if (!c.free_slots.empty()) {
@@ -266,8 +312,11 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
     int64_t new_ids = 0;
     for (const auto& kv : pending)
         if (!c.slot_of.count(kv.first)) ++new_ids;
-    if ((int64_t)c.free_slots.size() + (c.S - c.high_water) < new_ids)
-        throw Error(SW_ENOMEM, "arena full (max_entries reached)");
+    if ((int64_t)c.free_slots.size() + (c.S - c.high_water) < new_ids) {
+        if (!(c.cfg.flags & SW_FLAG_GROW)) throw Error(SW_ENOMEM, "arena full (max_entries reached)");
+        const int64_t need = c.high_water + new_ids - (int64_t)c.free_slots.size();
+        grow_arena(c, std::max<int64_t>(2 * c.S, need));  // SW_FLAG_GROW: double (amortised)
+    }
     for (int64_t e = 0; e < n; ++e) {
         const int64_t nr = h_off[e + 1] - h_off[e];
         auto it = c.slot_of.find(h_ids[e]);
@@ -565,7 +614,101 @@ int64_t sw_arena_entry_count(const sw_ctx* ctx) {
     return (int64_t)ctx->c.slot_of.size();
 }
 
-int64_t sw_arena_capacity(const sw_ctx* ctx) { return ctx ? ctx->c.S : 0; }
+int64_t sw_arena_capacity(const sw_ctx* ctx) {
+    if (!ctx) return 0;
+    std::shared_lock lk(ctx->c.mu);
+    return ctx->c.S;
+}
+
+int sw_arena_reserve(sw_ctx* ctx, int64_t max_entries) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && max_entries >= 1, "bad argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        wait_readers(c);
+        SW_CUDA(cudaSetDevice(c.device));
+        grow_arena(c, max_entries);
+        return SW_OK;
+    });
+}
+
+int64_t sw_arena_row_count(const sw_ctx* ctx) {  // IvfIndex::total_vectors (index.hpp:70)
+    if (!ctx) return 0;
+    std::shared_lock lk(ctx->c.mu);
+    int64_t n = 0;
+    for (const auto& kv : ctx->c.slot_of) n += ctx->c.h_nrows[(size_t)kv.second];
+    return n;
+}
+
+int64_t sw_arena_export(sw_ctx* ctx, int64_t first, int64_t count, uint64_t* ids,
+                        int32_t* nrows, float* rows, sw_segment* segs) {
+    try {
+        SW_REQUIRE(ctx && ids && nrows, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        // live entries in slot order; count is how many to return starting at the first-th
+        std::vector<std::pair<int64_t, uint64_t>> live;
+        live.reserve(c.slot_of.size());
+        for (const auto& kv : c.slot_of) live.emplace_back(kv.second, kv.first);
+        std::sort(live.begin(), live.end());
+        const int64_t total = (int64_t)live.size();
+        if (first >= total || count <= 0) return 0;
+        const int64_t n = std::min(count, total - first);
+        const int64_t s0 = live[(size_t)first].first, s1 = live[(size_t)(first + n - 1)].first + 1;
+        std::vector<float> blk;
+        std::vector<sw_segment> sblk;
+        if (rows) blk.resize((size_t)(s1 - s0) * c.Rp * c.Df);
+        if (segs) sblk.resize((size_t)(s1 - s0) * c.Rp);
+        if (rows)
+            SW_CUDA(cudaMemcpy(blk.data(), c.rows + s0 * c.Rp * c.Df, sizeof(float) * blk.size(),
+                               cudaMemcpyDeviceToHost));
+        if (segs)
+            SW_CUDA(cudaMemcpy(sblk.data(), c.segs + s0 * c.Rp, sizeof(sw_segment) * sblk.size(),
+                               cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t slot = live[(size_t)(first + i)].first;
+            ids[i] = live[(size_t)(first + i)].second;
+            nrows[i] = c.h_nrows[(size_t)slot];
+            for (int r = 0; r < c.Rp; ++r) {
+                const size_t src = (size_t)((slot - s0) * c.Rp + r);
+                if (rows)
+                    std::memcpy(rows + ((size_t)i * c.Rp + r) * c.D, blk.data() + src * c.Df,
+                                sizeof(float) * c.D);
+                if (segs) segs[(size_t)i * c.Rp + r] = sblk[src];
+            }
+        }
+        return n;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SW_ERUNTIME;
+    }
+}
+
+int sw_index_check_consistent(sw_ctx* ctx) {
+    try {
+        if (!ctx) return 0;
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        wait_readers(c);
+        SW_CUDA(cudaSetDevice(c.device));
+        int64_t valid = 0;
+        for (const auto& kv : c.slot_of) valid += c.h_nrows[(size_t)kv.second] > 0 ? 1 : 0;
+        std::vector<uint8_t> v((size_t)c.high_water);
+        if (c.high_water)
+            SW_CUDA(cudaMemcpy(v.data(), c.valid, (size_t)c.high_water, cudaMemcpyDeviceToHost));
+        int64_t dv = 0;
+        for (uint8_t x : v) dv += x ? 1 : 0;
+        if (dv != valid) return 0;
+        return ivf_check_consistent(c) ? 1 : 0;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return 0;
+    }
+}
 
 int sw_arena_contains(const sw_ctx* ctx, uint64_t id) {
     if (!ctx) return 0;
@@ -627,6 +770,51 @@ int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t re
         c.ivf_mutations = 0;
         c.ivf_rebuilds = 0;
         c.h_cent.clear();
+        return SW_OK;
+    });
+}
+
+int sw_ivf_set_rebuild_interval(sw_ctx* ctx, uint64_t interval) {
+    return guarded([&] {  // IvfIndex::set_rebuild_interval (index.hpp:76)
+        SW_REQUIRE(ctx && interval >= 1, "rebuild interval must be >= 1");
+        std::unique_lock lk(ctx->c.mu);
+        wait_readers(ctx->c);
+        ctx->c.ivf_interval = interval;
+        return SW_OK;
+    });
+}
+
+int sw_ivf_build(sw_ctx* ctx, int64_t n, const uint64_t* ids, const int64_t* row_off,
+                 const float* rows, const sw_segment* segs) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (n == 0 || (ids && row_off && rows && segs)), "null argument");
+        Ctx& c = ctx->c;
+        std::unique_lock lk(c.mu);
+        wait_readers(c);
+        SW_REQUIRE(c.ivf, "the context is not in IVF mode (sw_ivf_configure)");
+        SW_REQUIRE(c.slot_of.empty(), "IvfIndex::build needs an empty arena");
+        SW_CUDA(cudaSetDevice(c.device));
+        if (n > 0) {
+            c.ivf = false;  // a bulk load: no mutation counting, no list assignment yet
+            try {
+                do_insert(c, n, ids, row_off, rows, segs, nullptr, nullptr, nullptr, false);
+            } catch (...) {
+                c.ivf = true;
+                throw;
+            }
+            c.ivf = true;
+        }
+        std::vector<int64_t> perm;  // rows in the vecs order
+        std::unordered_map<uint64_t, int32_t> seen;
+        for (int64_t e = 0; e < n; ++e) {
+            const int64_t slot = c.slot_of.at(ids[e]);
+            const int32_t nr = (int32_t)(row_off[e + 1] - row_off[e]);
+            const int32_t b = seen[ids[e]];
+            for (int r = 0; r < nr; ++r) perm.push_back(slot * c.Rp + b + r);
+            seen[ids[e]] = b + nr;
+            c.ivf_rows[(size_t)slot] = b + nr;
+        }
+        ivf_build_from(c, perm);
         return SW_OK;
     });
 }
@@ -805,41 +993,76 @@ int sw_search(sw_ctx* ctx, const float* d_q, int32_t B, int32_t k, sw_hit* d_out
     });
 }
 
+// Persistent staging for the synchronous host entry points (grows, never shrinks). Caller
+// holds c.host_mu.
+static void* host_stage(Ctx& c, size_t bytes) {
+    if (!c.host_st) SW_CUDA(cudaStreamCreateWithFlags(&c.host_st, cudaStreamNonBlocking));
+    if (bytes > c.host_stage_bytes) {
+        if (c.host_stage) cudaFree(c.host_stage);
+        c.host_stage = nullptr;
+        c.host_stage_bytes = 0;
+        const size_t nb = std::max<size_t>(bytes, 64 * 1024);
+        SW_CUDA(cudaMalloc(&c.host_stage, nb));
+        c.host_stage_bytes = nb;
+    }
+    return c.host_stage;
+}
+
+static int search_host_impl(Ctx& c, const float* q, int32_t B, int32_t k, int32_t nprobe,
+                            sw_hit* out, int32_t* n) {
+    SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
+    SW_REQUIRE(k >= 1, "search k must be >= 1");  // index.cpp:291
+    SW_CUDA(cudaSetDevice(c.device));
+    std::lock_guard<std::mutex> hl(c.host_mu);
+    const size_t hit_bytes = sizeof(sw_hit) * (size_t)std::max(1, B * k);
+    char* stage = static_cast<char*>(host_stage(c, hit_bytes + sizeof(int32_t) * (size_t)B + 256));
+    sw_hit* d_out = reinterpret_cast<sw_hit*>(stage);
+    int32_t* d_n = reinterpret_cast<int32_t*>(stage + (hit_bytes + 255) / 256 * 256);
+    cudaStream_t st = c.host_st;
+    int rc = SW_OK;
+    {
+        HotGuard lk(c, st);
+        SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
+                                cudaMemcpyHostToDevice, st));
+        c.nprobe_override = nprobe;
+        int kn;
+        try {
+            kn = launch_search(c, c.d_q_stage, B, k, 0, st);
+        } catch (...) {
+            c.nprobe_override = 0;
+            throw;
+        }
+        c.nprobe_override = 0;
+        launch_hits_to_public(c, B, k, d_out, d_n, st);
+        c.last_kernels = kn + 1;
+        SW_CUDA(cudaMemcpyAsync(out, d_out, sizeof(sw_hit) * (size_t)B * k, cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    }
+    SW_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b)
+        if (n[b] < 0) {  // never expected: the fallback certifies every overflow
+            n[b] = -n[b] - 1;
+            set_last_error("search result not certified (candidate overflow)");
+            rc = SW_ERUNTIME;
+        }
+    return rc;
+}
+
 int sw_search_host(sw_ctx* ctx, const float* q, int32_t B, int32_t k, sw_hit* out, int32_t* n) {
     return guarded([&] {
         SW_REQUIRE(ctx && (B == 0 || (q && out && n)), "null argument");
-        Ctx& c = ctx->c;
-        SW_REQUIRE(B <= c.Bmax, "batch exceeds the context's max_batch");
-        SW_CUDA(cudaSetDevice(c.device));
-        sw_hit* d_out = nullptr;
-        int32_t* d_n = nullptr;
-        dalloc(&d_out, (size_t)std::max(1, B * k));
-        dalloc(&d_n, (size_t)std::max(1, B));
-        cudaStream_t st = nullptr;
-        SW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        int rc;
-        {
-            HotGuard lk(c, st);
-            SW_CUDA(cudaMemcpyAsync(c.d_q_stage, q, sizeof(float) * (size_t)B * c.D,
-                                    cudaMemcpyHostToDevice, st));
-            int kn = launch_search(c, c.d_q_stage, B, k, 0, st);
-            launch_hits_to_public(c, B, k, d_out, d_n, st);
-            c.last_kernels = kn + 1;
-            SW_CUDA(cudaMemcpyAsync(out, d_out, sizeof(sw_hit) * (size_t)B * k, cudaMemcpyDeviceToHost, st));
-            SW_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
-            SW_CUDA(cudaStreamSynchronize(st));
-            rc = SW_OK;
-            for (int b = 0; b < B; ++b)
-                if (n[b] < 0) {  // never expected: the fallback certifies every overflow
-                    n[b] = -n[b] - 1;
-                    set_last_error("search result not certified (candidate overflow)");
-                    rc = SW_ERUNTIME;
-                }
-        }
-        cudaStreamDestroy(st);
-        cudaFree(d_out);
-        cudaFree(d_n);
-        return rc;
+        if (B == 0) return SW_OK;
+        return search_host_impl(ctx->c, q, B, k, 0, out, n);
+    });
+}
+
+int sw_search_host_ex(sw_ctx* ctx, const float* q, int32_t B, int32_t k, int32_t nprobe,
+                      sw_hit* out, int32_t* n) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (q && out && n)), "null argument");
+        SW_REQUIRE(nprobe >= 0, "nprobe must be >= 0");
+        if (B == 0) return SW_OK;
+        return search_host_impl(ctx->c, q, B, k, nprobe, out, n);
     });
 }
 
@@ -1212,21 +1435,80 @@ int sw_score_select_host(sw_ctx* ctx, int32_t n, const double* sims, const doubl
                    "selector quality threshold must be in [0, 1]");
         Ctx& c = ctx->c;
         SW_CUDA(cudaSetDevice(c.device));
-        double *d_in = nullptr, *d_sc = nullptr;
-        int32_t* d_pick = nullptr;
-        dalloc(&d_in, (size_t)3 * n);
-        dalloc(&d_sc, (size_t)5 * n);
-        dalloc(&d_pick, 2);
-        SW_CUDA(cudaMemcpy(d_in, sims, sizeof(double) * n, cudaMemcpyHostToDevice));
-        SW_CUDA(cudaMemcpy(d_in + n, s_neg, sizeof(double) * n, cudaMemcpyHostToDevice));
-        SW_CUDA(cudaMemcpy(d_in + 2 * n, durations, sizeof(double) * n, cudaMemcpyHostToDevice));
+        std::lock_guard<std::mutex> hl(c.host_mu);
+        double* d_in = static_cast<double*>(host_stage(c, sizeof(double) * 8 * (size_t)n + 64));
+        double* d_sc = d_in + 3 * n;
+        int32_t* d_pick = reinterpret_cast<int32_t*>(d_in + 8 * n);
+        cudaStream_t st = c.host_st;
+        SW_CUDA(cudaMemcpyAsync(d_in, sims, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_in + n, s_neg, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_in + 2 * n, durations, sizeof(double) * n, cudaMemcpyHostToDevice, st));
         launch_score_select_one(c, n, d_in, d_in + n, d_in + 2 * n, L, *sel, rng_seed, d_sc,
-                                d_pick, nullptr);
-        SW_CUDA(cudaMemcpy(scores_out, d_sc, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(pick, d_pick, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost));
-        cudaFree(d_in);
-        cudaFree(d_sc);
-        cudaFree(d_pick);
+                                d_pick, st);
+        SW_CUDA(cudaMemcpyAsync(scores_out, d_sc, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaMemcpyAsync(pick, d_pick, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaStreamSynchronize(st));
+        return SW_OK;
+    });
+}
+
+int sw_score_candidates_host(sw_ctx* ctx, int32_t n, int32_t dim, const double* sims,
+                             const float* audio, const double* durations, double L,
+                             const float* negative, double* scores_out) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && sims && audio && durations && scores_out, "null argument");
+        SW_REQUIRE(n >= 1, "score_candidates: empty candidate list");  // selector.cpp:28
+        SW_REQUIRE(n <= kMaxTopK, "at most 32 candidates");
+        SW_REQUIRE(L > 0.0, "requested duration must be positive");    // selector.cpp:29-31
+        SW_REQUIRE(dim >= 1, "dim must be >= 1");
+        Ctx& c = ctx->c;
+        SW_REQUIRE(negative || dim == c.D, "dot: dimension mismatch");
+        SW_CUDA(cudaSetDevice(c.device));
+        std::lock_guard<std::mutex> hl(c.host_mu);
+        const size_t ab = sizeof(float) * (size_t)n * dim, nb = sizeof(float) * (size_t)dim;
+        char* base = static_cast<char*>(host_stage(c, sizeof(double) * 7 * (size_t)n + ab + nb + 512));
+        double* d_sims = reinterpret_cast<double*>(base);
+        double* d_dur = d_sims + n;
+        double* d_sc = d_dur + n;
+        float* d_audio = reinterpret_cast<float*>(d_sc + 5 * n);
+        float* d_neg = negative ? d_audio + (size_t)n * dim : c.neg;
+        cudaStream_t st = c.host_st;
+        SW_CUDA(cudaMemcpyAsync(d_sims, sims, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_dur, durations, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_audio, audio, ab, cudaMemcpyHostToDevice, st));
+        if (negative) SW_CUDA(cudaMemcpyAsync(d_neg, negative, nb, cudaMemcpyHostToDevice, st));
+        launch_score_candidates(n, dim, d_sims, d_audio, d_dur, d_neg, L, d_sc, st);
+        SW_CUDA(cudaMemcpyAsync(scores_out, d_sc, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaStreamSynchronize(st));
+        return SW_OK;
+    });
+}
+
+int sw_select_host(sw_ctx* ctx, int32_t n, const double* s_pos, const double* q,
+                   double temperature, double threshold, double u, int32_t* pick,
+                   uint32_t* flags) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && s_pos && q && pick, "null argument");
+        SW_REQUIRE(n >= 0 && n <= kMaxTopK, "at most 32 candidates");
+        SW_REQUIRE(temperature > 0.0, "selector temperature must be > 0");  // selector.cpp:10
+        SW_REQUIRE(threshold >= 0.0 && threshold <= 1.0,
+                   "selector quality threshold must be in [0, 1]");
+        Ctx& c = ctx->c;
+        SW_CUDA(cudaSetDevice(c.device));
+        std::lock_guard<std::mutex> hl(c.host_mu);
+        double* d_in = static_cast<double*>(host_stage(c, sizeof(double) * (2 * (size_t)n + 2) + 64));
+        int32_t* d_pick = reinterpret_cast<int32_t*>(d_in + 2 * n);
+        cudaStream_t st = c.host_st;
+        if (n > 0) {
+            SW_CUDA(cudaMemcpyAsync(d_in, s_pos, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+            SW_CUDA(cudaMemcpyAsync(d_in + n, q, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        }
+        launch_select_draw(n, d_in, d_in + n, temperature, threshold, u, d_pick, st);
+        int32_t h[2];
+        SW_CUDA(cudaMemcpyAsync(h, d_pick, sizeof(h), cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaStreamSynchronize(st));
+        *pick = h[0];
+        if (flags) *flags = (uint32_t)h[1];
         return SW_OK;
     });
 }
@@ -1238,25 +1520,25 @@ int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const in
         Ctx& c = ctx->c;
         std::shared_lock lk(c.mu);
         SW_CUDA(cudaSetDevice(c.device));
-        float *d_p = nullptr, *d_s = nullptr;
-        int32_t *d_T = nullptr, *d_arm = nullptr;
-        double* d_phi = nullptr;
-        dalloc(&d_p, (size_t)B * c.D);
-        dalloc(&d_s, (size_t)B * c.D);
-        dalloc(&d_T, (size_t)B);
-        dalloc(&d_arm, (size_t)B);
-        dalloc(&d_phi, (size_t)B * kFeatureDim);
-        SW_CUDA(cudaMemcpy(d_p, prompts, sizeof(float) * B * c.D, cudaMemcpyHostToDevice));
-        SW_CUDA(cudaMemcpy(d_s, segs, sizeof(float) * B * c.D, cudaMemcpyHostToDevice));
-        SW_CUDA(cudaMemcpy(d_T, T, sizeof(int32_t) * B, cudaMemcpyHostToDevice));
-        launch_gater(c, d_p, d_s, d_T, B, explore, d_phi, d_arm, nullptr);
-        SW_CUDA(cudaMemcpy(phi_out, d_phi, sizeof(double) * B * kFeatureDim, cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(arm_out, d_arm, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
-        cudaFree(d_p);
-        cudaFree(d_s);
-        cudaFree(d_T);
-        cudaFree(d_arm);
-        cudaFree(d_phi);
+        if (B <= 0) return SW_OK;
+        std::lock_guard<std::mutex> hl(c.host_mu);
+        const size_t fb = sizeof(float) * (size_t)B * c.D;
+        char* base = static_cast<char*>(
+            host_stage(c, 2 * fb + sizeof(double) * (size_t)B * kFeatureDim + 8 * (size_t)B + 1024));
+        float* d_p = reinterpret_cast<float*>(base);
+        float* d_s = reinterpret_cast<float*>(base + fb);
+        double* d_phi = reinterpret_cast<double*>(base + (2 * fb + 255) / 256 * 256);
+        int32_t* d_T = reinterpret_cast<int32_t*>(d_phi + (size_t)B * kFeatureDim);
+        int32_t* d_arm = d_T + B;
+        cudaStream_t st = c.host_st;
+        SW_CUDA(cudaMemcpyAsync(d_p, prompts, fb, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_s, segs, fb, cudaMemcpyHostToDevice, st));
+        SW_CUDA(cudaMemcpyAsync(d_T, T, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+        launch_gater(c, d_p, d_s, d_T, B, explore, d_phi, d_arm, st);
+        SW_CUDA(cudaMemcpyAsync(phi_out, d_phi, sizeof(double) * B * kFeatureDim,
+                                cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaMemcpyAsync(arm_out, d_arm, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+        SW_CUDA(cudaStreamSynchronize(st));
         return SW_OK;
     });
 }

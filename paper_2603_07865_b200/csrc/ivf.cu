@@ -609,6 +609,64 @@ void ivf_rebuild(Ctx& c) {
     SW_CUDA(cudaStreamSynchronize(c.mstream));
 }
 
+// IvfIndex::build(vecs, C, seed, nprobe) (index.cpp:186-208) over rows already in the arena:
+// kmeans over `perm` (the vecs order) with the build seed itself (no rebuild derivation),
+// C reduced to the row count, every row assigned to its nearest centroid; no mutation counted.
+void ivf_build_from(Ctx& c, const std::vector<int64_t>& perm) {
+    c.grp_dirty = true;
+    c.ivf_mutations = 0;
+    c.ivf_rebuilds = 0;
+    if (perm.empty()) {
+        c.ivf_C = 0;
+        c.h_cent.clear();
+        return;
+    }
+    const int cnum = (int)std::min<int64_t>((int64_t)perm.size(), std::max(c.ivf_target, 1));
+    kmeans(c, perm, cnum, c.ivf_seed);
+    DBuf<int64_t> d_perm(perm.size());
+    SW_CUDA(cudaMemcpy(d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice));
+    argmax_rows(c, d_perm.p, (int64_t)perm.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+}
+
+// IvfIndex::check_consistent (index.cpp:334-343): every stored row sits in the list of its
+// nearest centroid (recomputed here with the same fp64 chains), rows beyond an entry's count
+// in no list, and (exhaustive mode) no row carries a list.
+bool ivf_check_consistent(Ctx& c) {
+    std::vector<int64_t> rows;
+    std::vector<int16_t> want;
+    for (auto& kv : c.slot_of) {
+        const int64_t slot = kv.second;
+        const int nr = c.h_nrows[(size_t)slot];
+        if (c.ivf && c.ivf_rows[(size_t)slot] != nr) return false;
+        for (int r = 0; r < nr; ++r) rows.push_back(slot * c.Rp + r);
+    }
+    if (rows.empty()) return true;
+    std::vector<int16_t> have(rows.size());
+    {
+        std::vector<int16_t> all((size_t)c.high_water * c.Rp);
+        SW_CUDA(cudaMemcpy(all.data(), c.row_list, sizeof(int16_t) * all.size(),
+                           cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < rows.size(); ++i) have[i] = all[(size_t)rows[i]];
+    }
+    if (!c.ivf) {
+        for (int16_t l : have)
+            if (l != -1) return false;
+        return true;
+    }
+    if (c.ivf_C == 0) return false;
+    DBuf<int64_t> d_rows(rows.size());
+    DBuf<int32_t> d_as(rows.size());
+    SW_CUDA(cudaMemcpy(d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice));
+    argmax_rows(c, d_rows.p, (int64_t)rows.size(), c.ivf_C, nullptr, d_as.p, c.mstream);
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+    std::vector<int32_t> as(rows.size());
+    SW_CUDA(cudaMemcpy(as.data(), d_as.p, sizeof(int32_t) * as.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < rows.size(); ++i)
+        if ((int32_t)have[i] != as[i]) return false;
+    return true;
+}
+
 // IvfIndex::insert (index.cpp:224-234) for entries just written to the arena, in order: entry e
 // added rows [base[e], base[e] + nr[e]) of slot[e]. Rebuilds trigger between entries exactly
 // where the reference's per-entry insert calls trigger them.
@@ -710,7 +768,7 @@ static void build_sorted(Ctx& c) {
         if (valid[(size_t)i] && rl[(size_t)i] >= 0 && rl[(size_t)i] < C)
             sorted[(size_t)pos[(size_t)rl[(size_t)i]]++] = (int32_t)i;
     // chunking: tpc tiles per work item, <= kMaxSlices / nprobe chunks per list
-    const int np = std::max(1, std::min(c.ivf_nprobe, C));
+    const int np = std::max(1, std::min(eff_nprobe(c), C));
     // 16+ tiles per item amortise the per-item pipeline ramp (A load, TMA / MMA fill, drain)
     // 24 measured best at the reference default (64 lists, nprobe 8, B = 1024, 1M rows):
     // score 0.285-0.292 ms vs 0.301 (16), 0.308 (28), 0.33 (20, 32), 0.38 (8) — shorter items
@@ -771,7 +829,7 @@ int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st) {
         return !(e && e[0] == '0');
     }();
     if (!enabled || !c.ivf || c.ivf_C == 0 || c.Rp != 1 || !c.tc_ok) return 0;
-    const int np = std::min(c.ivf_nprobe, c.ivf_C);
+    const int np = std::min(eff_nprobe(c), c.ivf_C);
     if (np >= c.ivf_C) return 0;
     if (c.grp_dirty || c.grp_C != c.ivf_C) build_sorted(c);
     if (c.grp_rows == 0) return 0;
@@ -815,7 +873,7 @@ bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st) {
         SW_CUDA(cudaMemsetAsync(c.pmask, 0, sizeof(uint64_t) * 4 * (size_t)B, st));
         return true;
     }
-    const int np = std::min(c.ivf_nprobe, c.ivf_C);
+    const int np = std::min(eff_nprobe(c), c.ivf_C);
     if (np >= c.ivf_C) return false;  // every list probed == exhaustive
     const int cp = c.ivf_C <= 32 ? 32 : c.ivf_C <= 64 ? 64 : c.ivf_C <= 128 ? 128 : 256;
     {

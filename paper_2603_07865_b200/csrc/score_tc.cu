@@ -800,7 +800,7 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.prank = c.prank;
     p.grp_ch = c.grp_ch;
     p.n_items = c.d_qbase + kMaxCentroids + 1;  // device count written by k_group_plan
-    p.n_chunks = std::min(c.ivf_nprobe, c.ivf_C) * c.grp_ch;
+    p.n_chunks = std::min(eff_nprobe(c), c.ivf_C) * c.grp_ch;
     SW_REQUIRE(p.n_chunks <= kMaxSlices, "grouped IVF: too many slices per query");
     p.cap_local = (kCandCap / p.n_chunks) & ~3;
     c.last_chunks = p.n_chunks;

@@ -72,6 +72,36 @@ __global__ void k_score_select_one(int n, const double* sims, const double* sneg
     }
 }
 
+// score_candidates (selector.cpp:24-58) with s_neg = clamp01(cosine(audio_i, negative)) computed
+// here (sequential fp64 dot, core.cpp:26-37); lane i = candidate i
+__global__ void k_score_candidates(int n, int D, const double* __restrict__ sims,
+                                   const float* __restrict__ audio,
+                                   const double* __restrict__ durs, const float* __restrict__ neg,
+                                   double L, double* __restrict__ scores) {
+    __shared__ double sn[kMaxTopK];
+    const int i = threadIdx.x;
+    if (i < n) {
+        const float* a = audio + (int64_t)i * D;
+        double s = 0.0;
+        for (int d = 0; d < D; ++d) s = fma((double)a[d], (double)neg[d], s);
+        sn[i] = clamp01(fmin(1.0, fmax(-1.0, s)));
+    }
+    __syncthreads();
+    if (i == 0) {
+        // gate values only: thr = 2 admits no candidate, so no draw is consumed
+        gate_select(n, sims, sn, durs, L, 1.0, 2.0, 0.0, scores);
+    }
+}
+
+__global__ void k_select_draw(int n, const double* __restrict__ s_pos, const double* __restrict__ q,
+                              double temp, double thr, double u, int32_t* __restrict__ pick) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const GateOut g = select_draw(n, s_pos, q, temp, thr, u);
+        pick[0] = g.pick;
+        pick[1] = (int32_t)g.flags;
+    }
+}
+
 __global__ void k_gater(const float* __restrict__ P, const float* __restrict__ Sg,
                         const int32_t* __restrict__ T, int B, int D, const float* theta,
                         const float* psi, int fd, double beta, int explore, double* phi_out,
@@ -147,6 +177,19 @@ void launch_score_select_one(Ctx& c, int n, const double* d_sims, const double* 
     (void)c;
     k_score_select_one<<<1, 32, 0, st>>>(n, d_sims, d_sneg, d_dur, L, sel.temperature,
                                          sel.quality_threshold, rng_seed, d_scores, d_pick);
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_score_candidates(int n, int D, const double* d_sims, const float* d_audio,
+                             const double* d_dur, const float* d_neg, double L, double* d_scores,
+                             cudaStream_t st) {
+    k_score_candidates<<<1, 32, 0, st>>>(n, D, d_sims, d_audio, d_dur, d_neg, L, d_scores);
+    SW_CUDA(cudaGetLastError());
+}
+
+void launch_select_draw(int n, const double* d_spos, const double* d_q, double temp, double thr,
+                        double u, int32_t* d_pick, cudaStream_t st) {
+    k_select_draw<<<1, 32, 0, st>>>(n, d_spos, d_q, temp, thr, u, d_pick);
     SW_CUDA(cudaGetLastError());
 }
 

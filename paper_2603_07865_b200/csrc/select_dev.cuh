@@ -50,6 +50,9 @@ struct GateOut {
     uint32_t flags;
 };
 
+__device__ __forceinline__ GateOut select_draw(int n, const double* s_pos, const double* q,
+                                               double temp, double thr, double u);
+
 // score_candidates + select over n records; scores optionally written (n x 5).
 // Rng(seed).uniform() (core.hpp:83): (first mt19937_64 output >> 11) * 2^-53
 __device__ __forceinline__ double uniform_draw(uint64_t rng_seed) {
@@ -81,6 +84,12 @@ __device__ __forceinline__ GateOut gate_select(int n, const double* sims, const 
             scores[i * 5 + 4] = q[i];
         }
     }
+    return select_draw(n, s_pos, q, temp, thr, u);
+}
+
+// select (selector.cpp:60-85) given the gate scores and the draw u = rng.uniform()
+__device__ __forceinline__ GateOut select_draw(int n, const double* s_pos, const double* q,
+                                               double temp, double thr, double u) {
     GateOut g{-1, 0u};
     int surv[kMaxTopK], ns = 0;
     for (int i = 0; i < n; ++i)

@@ -174,6 +174,7 @@ struct Ctx {
     bool ivf = false;
     int ivf_target = 1;               // target_centroids_
     int ivf_nprobe = 8;               // nprobe_
+    int nprobe_override = 0;          // > 0: this call's search(q, k, nprobe) (index.hpp:67)
     int ivf_C = 0;                    // centroids_.size()
     uint64_t ivf_seed = 0;            // seed_
     uint64_t ivf_interval = 1024;     // rebuild_interval_
@@ -261,6 +262,12 @@ struct Ctx {
     size_t prof_used = 0;
     double prof_ms[SW_NUM_STAGES] = {};
     int64_t prof_n[SW_NUM_STAGES] = {};
+    // synchronous host entry points (sw_search_host, sw_score_select_host, sw_gater_host):
+    // persistent staging and stream, so a per-request call allocates nothing
+    std::mutex host_mu;
+    cudaStream_t host_st = nullptr;
+    void* host_stage = nullptr;
+    size_t host_stage_bytes = 0;
     // last launch info
     int last_kernels = 0, last_tc = 0, last_cand_max = 0;
     // dynamic shared-memory opt-ins already applied on this context's device (the attribute is
@@ -268,6 +275,9 @@ struct Ctx {
     std::mutex attr_mu;
     std::map<const void*, size_t> smem_attr;
 };
+
+// nprobe of the current search: a per-call override (search(q, k, nprobe)) or set_nprobe's
+inline int eff_nprobe(const Ctx& c) { return c.nprobe_override > 0 ? c.nprobe_override : c.ivf_nprobe; }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (context, kernel, size high-water).
 template <class K>
@@ -356,6 +366,11 @@ void launch_score_select_one(Ctx& c, int n, const double* d_sims, const double* 
                              const double* d_dur, double L, const sw_selector_config& sel,
                              uint64_t rng_seed, double* d_scores, int32_t* d_pick,
                              cudaStream_t st);
+void launch_score_candidates(int n, int D, const double* d_sims, const float* d_audio,
+                             const double* d_dur, const float* d_neg, double L, double* d_scores,
+                             cudaStream_t st);
+void launch_select_draw(int n, const double* d_spos, const double* d_q, double temp, double thr,
+                        double u, int32_t* d_pick, cudaStream_t st);
 void launch_gater(Ctx& c, const float* d_p, const float* d_s, const int32_t* d_T, int B,
                   int explore, double* d_phi, int32_t* d_arm, cudaStream_t st);
 
@@ -367,6 +382,8 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
 void ivf_on_remove(Ctx& c, int64_t slot);
 void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector<int32_t>& nr);
 void ivf_set_centroids(Ctx& c, const float* h, int C);
+void ivf_build_from(Ctx& c, const std::vector<int64_t>& perm);
+bool ivf_check_consistent(Ctx& c);
 bool launch_probe_rank(Ctx& c, const float* d_q, int B, cudaStream_t st);
 // grouped IVF search: returns the upper bound of work items (0 = grouped path not applicable)
 int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st);
