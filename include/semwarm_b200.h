@@ -115,7 +115,7 @@ typedef struct sw_choice {
     int32_t steps_skipped;
     int32_t n_hits;
     uint64_t entry_id;
-    sw_segment segment;
+    sw_segment segment;  /* the matched segment; segment.reserved = its pyramid row in the entry */
     double similarity;
     double skip_fraction;
     int32_t pick;    /* index of the chosen candidate in the top-k list, -1 on a miss */
@@ -460,6 +460,88 @@ int swcm_importance(const swcm_cache* cache, uint64_t entry_id, double now_h, do
 int swcm_size(const swcm_cache* cache);
 int swcm_ids(const swcm_cache* cache, uint64_t* out, int32_t cap);
 int swcm_check_consistent(const swcm_cache* cache);
+
+/* ---------------------------------------------------------------- trace replay (config 5)
+ * WorkloadConfig (simgen.hpp:87-98). */
+typedef struct swr_workload {
+    int64_t n_prompts;
+    int32_t cluster_count;
+    int32_t dim;
+    double near_duplicate_rate;
+    double cluster_perturbation;
+    double duplicate_perturbation;
+    double duration_lo_s;
+    double duration_hi_s;
+    double arrival_rate_hz;
+    int32_t total_steps;
+    int32_t reserved;
+} swr_workload;
+/* synth_workload (simgen.cpp:162-194), bit-identical for the same seed: request i (id i + 1)
+ * gets prompts[i * dim ..], durations[i], arrivals[i] (s) and total_steps[i]. */
+int swr_synth_workload(const swr_workload* cfg, uint64_t seed, float* prompts, double* durations,
+                       double* arrivals, int32_t* total_steps);
+
+/* make_negative_embedding (selector.cpp:16-20): the fixed seeded negative reference of `dim`. */
+int sw_negative_embedding(int32_t dim, float* out);
+
+/* The PipelineConfig fields a replay uses (pipeline.hpp:24-51) plus the lookup batch size. */
+typedef struct swr_config {
+    uint64_t seed;                   /* PipelineConfig::seed */
+    sw_selector_config selector;
+    sw_policy policy;
+    double q_max;                    /* QualityModel (simgen.hpp:27-31) */
+    double penalty_slope;
+    double noise_scale;
+    double skip_headroom;
+    double step_time_s_per_10s;      /* SimGenConfig */
+    double alpha;                    /* BanditModel::alpha (the reward's trade-off) */
+    int32_t latent_rate;
+    int32_t default_total_steps;
+    int32_t refinement_enabled;
+    int32_t batch;                   /* lookups per device batch; 1 = Pipeline::replay exactly */
+} swr_config;
+
+/* ServeOutcome (core.hpp:54-67); entry ids 0 = none. */
+typedef struct swr_outcome {
+    uint64_t request_id;
+    int32_t cache_hit;
+    int32_t arm_index;
+    int32_t steps_skipped;
+    int32_t fallback;
+    uint64_t entry_id;
+    uint64_t admitted_entry_id;
+    double quality;
+    double nfe_cost_s;
+    double sim_latency_s;
+    double skip_fraction;
+    double reference_similarity;
+} swr_outcome;
+
+/* RunReport's summary (pipeline.hpp:53-68) + wall-clock split of the replay. */
+typedef struct swr_stats {
+    double total_s;         /* wall time of the whole replay */
+    double lookup_s;        /* batched sw_plan + segment-row gather + D2H */
+    double mutation_s;      /* generate + record_reuse + admit (+ evictions), per request */
+    double maintenance_s;   /* refinement_candidates + refine, after every request */
+    int64_t batches, lookups, admits, evictions, refinements, reuses;
+    double total_nfe_s, baseline_nfe_s, speedup, mean_quality, mean_reward, hit_rate;
+    double mean_latency_s, median_latency_s, p95_latency_s;
+} swr_stats;
+
+/* Pipeline::replay (pipeline.cpp:299-323) over a warm-start context + Cache Manager, with the
+ * lookups of `batch` consecutive requests planned in one sw_plan against the cache as it stands
+ * when the batch starts; mutations (simulated generate, record_reuse, admit + evict)
+ * and run_maintenance (refine with the pipeline's maintenance RNG, pipeline.cpp:70,280-297) follow
+ * per request, in order. The context must hold the cache's embedding arena (IVF configured as
+ * the pipeline's index), the negative embedding and the gater; out: n outcomes. */
+int swr_replay(sw_ctx* ctx, swcm_cache* cache, const swr_config* cfg, int64_t n,
+               const float* prompts, const double* durations, const double* arrivals,
+               const int32_t* total_steps, swr_outcome* out, swr_stats* stats);
+
+/* Device gather of each chosen segment row (slot, segment.reserved) of B choices into
+ * d_rows (B x dim fp32; misses zero-filled). Stream-ordered. */
+int sw_choice_rows(sw_ctx* ctx, const sw_choice* d_choices, int32_t B, float* d_rows,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -285,9 +285,49 @@ class Ref:
         L.ref_cache_entry_rows.restype = C.c_int
         L.ref_cache_entry_rows.argtypes = [C.c_void_p, C.c_uint64, f32p, C.c_int]
 
+        L.ref_synth_workload.restype = C.c_int
+        L.ref_synth_workload.argtypes = [C.c_int64, C.c_int, C.c_uint64, f32p, f64p, f64p, i32p]
+        L.ref_replay.restype = C.c_int
+        L.ref_replay.argtypes = [C.c_int64, C.c_int, f32p, f64p, f64p, i32p, C.c_uint64, C.c_int,
+                                 C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_uint64,
+                                 C.c_int, C.c_void_p, f64p, C.POINTER(C.c_double)]
+
     # -- helpers
     def derive_seed(self, base, a, b=0, c=0):
         return self.lib.ref_derive_seed(base, a, b, c)
+
+    def synth_workload(self, n, dim, seed):
+        """the reference's synth_workload (simgen.cpp:162-194), default WorkloadConfig"""
+        p = np.zeros((n, dim), np.float32)
+        d, a = np.zeros(n), np.zeros(n)
+        t = np.zeros(n, np.int32)
+        self.lib.ref_synth_workload(n, dim, seed, p, d, a, t)
+        return p, d, a, t
+
+    def replay(self, prompts, durations, arrivals, steps, *, capacity=1024, policy="exploit",
+               theta=None, psi=None, beta=1.0, fixed_arm=0, seed=1, batch=0):
+        """batch 0: the reference's own Pipeline::replay; batch >= 1: the same flow with batched
+        lookups against per-batch snapshots (ref_harness.cpp ref_replay). Returns (outcomes in
+        OUTCOME_DTYPE layout, summary dict, wall seconds)."""
+        from paper_2603_07865_b200._lib import OUTCOME_DTYPE
+        n, dim = prompts.shape
+        out = np.zeros(n, OUTCOME_DTYPE)
+        summ = np.zeros(10)
+        wall = C.c_double()
+        th = None if theta is None else np.ascontiguousarray(theta, np.float32)
+        ps = None if psi is None else np.ascontiguousarray(psi, np.float32)
+        rc = self.lib.ref_replay(n, dim, np.ascontiguousarray(prompts, np.float32),
+                                 np.ascontiguousarray(durations, np.float64),
+                                 np.ascontiguousarray(arrivals, np.float64),
+                                 np.ascontiguousarray(steps, np.int32), capacity, POLICY[policy],
+                                 None if th is None else th.ctypes.data,
+                                 None if ps is None else ps.ctypes.data, beta, fixed_arm, seed,
+                                 batch, out.ctypes.data, summ, C.byref(wall))
+        if rc != n:
+            raise RuntimeError(f"ref_replay failed ({rc})")
+        keys = ["total_nfe_s", "baseline_nfe_s", "speedup", "mean_quality", "mean_reward",
+                "hit_rate", "mean_latency_s", "median_latency_s", "p95_latency_s", "refinements"]
+        return out, dict(zip(keys, summ.tolist())), wall.value
 
     def random_unit_vectors(self, seed, n, dim):
         out = np.zeros((n, dim), np.float32)

@@ -8,7 +8,10 @@
 // cache's segment rows looked up from the caller-owned row buffer exactly as
 // pipeline.cpp:113-131 looks them up through CacheManager::find.
 
+#include <chrono>
 #include <cmath>
+#include <string>
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -24,6 +27,7 @@
 #include "semwarm/vocoder.hpp"
 #include "semwarm/selector.hpp"
 #include "semwarm/simgen.hpp"
+#include "semwarm/pipeline.hpp"
 
 using namespace semwarm;
 
@@ -586,6 +590,283 @@ int ref_cache_entry_rows(void* p, uint64_t id, float* rows, int cap) {
 double ref_expected_quality(double skip, double sigma) {
     QualityModel m;
     return m.expected_quality(skip, sigma);
+}
+
+
+// ---------------------------------------------------------------- trace replay (config 5)
+// synth_workload (simgen.cpp:162-194) with the reference defaults, n prompts of `dim`.
+int ref_synth_workload(int64_t n, int dim, uint64_t seed, float* prompts, double* dur,
+                       double* arr, int32_t* steps) {
+    WorkloadConfig wc;
+    wc.n_prompts = (size_t)n;
+    wc.dim = (size_t)dim;
+    auto tr = synth_workload(wc, seed);
+    for (size_t i = 0; i < tr.size(); ++i) {
+        std::memcpy(prompts + i * dim, tr[i].prompt_embedding.values.data(), sizeof(float) * dim);
+        dur[i] = tr[i].duration_s;
+        arr[i] = tr[i].arrival_time_s;
+        steps[i] = tr[i].total_steps;
+    }
+    return (int)tr.size();
+}
+
+struct RefReplayOut {  // swr_outcome's layout
+    uint64_t request_id;
+    int32_t cache_hit, arm_index, steps_skipped, fallback;
+    uint64_t entry_id, admitted_entry_id;
+    double quality, nfe_cost_s, sim_latency_s, skip_fraction, reference_similarity;
+};
+
+static PipelineConfig replay_cfg(int dim, uint64_t capacity, int policy, const float* theta,
+                                 const float* psi, double beta, int fixed_arm, uint64_t seed) {
+    ConfigMap cm;
+    cm.set("dim", std::to_string(dim));
+    cm.set("seed", std::to_string(seed));
+    cm.set("cache.capacity", std::to_string(capacity));
+    const char* pol[] = {"exploit", "explore", "rule", "fixed"};
+    cm.set("gater.policy", pol[policy]);
+    cm.set("fixed.arm", std::to_string(fixed_arm));
+    PipelineConfig cfg = PipelineConfig::from_config(cm);
+    if (theta) std::memcpy(cfg.gater.theta.data(), theta, sizeof(float) * kNumArms * kFeatureDim);
+    if (psi) std::memcpy(cfg.gater.psi.data(), psi, sizeof(float) * kNumArms * kFeatureDim);
+    cfg.gater.beta = beta;
+    return cfg;
+}
+
+static void copy_out(const ServeOutcome& o, RefReplayOut* r) {
+    std::memset(r, 0, sizeof(*r));
+    r->request_id = o.request_id;
+    r->cache_hit = o.cache_hit;
+    r->arm_index = o.arm_index;
+    r->steps_skipped = o.steps_skipped;
+    r->fallback = o.fallback;
+    r->entry_id = o.entry_id ? *o.entry_id : 0;
+    r->admitted_entry_id = o.admitted_entry_id ? *o.admitted_entry_id : 0;
+    r->quality = o.quality;
+    r->nfe_cost_s = o.nfe_cost_s;
+    r->sim_latency_s = o.sim_latency_s;
+    r->skip_fraction = o.skip_fraction;
+    r->reference_similarity = o.reference_similarity;
+}
+
+static std::vector<GenerationRequest> make_trace(int64_t n, int dim, const float* prompts,
+                                                 const double* dur, const double* arr,
+                                                 const int32_t* steps) {
+    std::vector<GenerationRequest> tr((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        tr[i].id = (uint64_t)(i + 1);
+        tr[i].prompt_embedding = vec(prompts + (size_t)i * dim, dim);
+        tr[i].duration_s = dur[i];
+        tr[i].arrival_time_s = arr[i];
+        tr[i].total_steps = steps[i];
+    }
+    return tr;
+}
+
+// batch <= 0: the reference's own Pipeline::replay (pipeline.cpp:299-323), untouched.
+// batch >= 1: the same decisions with the lookups of `batch` consecutive requests planned
+// against the cache as it stands when the batch starts (plan_request, pipeline.cpp:91-178, incl.
+// slice_clip + time_stretch), then per request: pick_arm, generate, record_reuse, admit and the
+// maintenance pass (pipeline.cpp:180-297) — through the reference's public API on the
+// Pipeline's own CacheManager. batch = 1 must equal batch <= 0 (tests check it).
+int ref_replay(int64_t n, int dim, const float* prompts, const double* dur, const double* arr,
+               const int32_t* steps, uint64_t capacity, int policy, const float* theta,
+               const float* psi, double beta, int fixed_arm, uint64_t seed, int batch,
+               RefReplayOut* out, double* summary /* [total_nfe, baseline, speedup, mean_q,
+               mean_reward, hit_rate, mean_lat, median_lat, p95_lat, refinements] */,
+               double* wall_s) {
+    try {
+        PipelineConfig cfg = replay_cfg(dim, capacity, policy, theta, psi, beta, fixed_arm, seed);
+        auto trace = make_trace(n, dim, prompts, dur, arr, steps);
+        Pipeline pipe(cfg);
+        const auto t0 = std::chrono::steady_clock::now();
+        RunReport rep;
+        if (batch <= 0) {
+            rep = pipe.replay(trace);
+        } else {
+            const PipelineConfig& pc = pipe.config();
+            CacheManager& cache = pipe.cache();
+            Rng maint(derive_seed(pc.seed, 0x4d41494eULL));
+            double prev = 0.0, busy = 0.0;
+            for (int64_t b0 = 0; b0 < n; b0 += batch) {
+                const int64_t b1 = std::min<int64_t>(n, b0 + batch);
+                struct Plan {
+                    bool hit = false, fallback = false;
+                    uint64_t entry_id = 0;
+                    double similarity = 0.0;
+                    std::optional<SimClip> reference;
+                    std::vector<double> features;
+                };
+                std::vector<Plan> plans((size_t)(b1 - b0));
+                for (int64_t g = b0; g < b1; ++g) {  // lookups against the frozen snapshot
+                    const GenerationRequest& req = trace[(size_t)g];
+                    Plan& pl = plans[(size_t)(g - b0)];
+                    Rng sel_rng(derive_seed(pc.seed, req.id, 2));
+                    try {
+                        auto hits = cache.index().search(req.prompt_embedding, pc.selector.top_k);
+                        std::optional<SearchHit> chosen;
+                        std::vector<CandidateInput> inputs;
+                        for (const auto& h : hits) {
+                            const CacheEntry* e = cache.find(h.entry_id);
+                            if (!e) continue;
+                            CandidateInput in;
+                            in.entry_id = h.entry_id;
+                            in.segment = h.segment;
+                            in.prompt_similarity = h.similarity;
+                            in.duration_s = h.segment.length_s;
+                            for (const auto& v : e->segment_vectors)
+                                if (v.segment.level == h.segment.level &&
+                                    std::fabs(v.segment.start_s - h.segment.start_s) < 1e-9) {
+                                    in.audio_embedding = v.embedding;
+                                    break;
+                                }
+                            if (in.audio_embedding.dim() == 0) continue;
+                            inputs.push_back(std::move(in));
+                        }
+                        if (!inputs.empty()) {
+                            auto scored = score_candidates(inputs, req.prompt_embedding,
+                                                           req.duration_s, pc.selector);
+                            auto pick = select(scored, pc.selector, sel_rng);
+                            if (pick)
+                                chosen = SearchHit{scored[*pick].entry_id, scored[*pick].segment,
+                                                   scored[*pick].s_pos};
+                        }
+                        if (chosen) {
+                            const CacheEntry* entry = cache.find(chosen->entry_id);
+                            EmbeddingVector seg_emb = entry->full_embedding;
+                            for (const auto& v : entry->segment_vectors)
+                                if (v.segment.level == chosen->segment.level &&
+                                    std::fabs(v.segment.start_s - chosen->segment.start_s) < 1e-9) {
+                                    seg_emb = v.embedding;
+                                    break;
+                                }
+                            SimClip ref = chosen->segment.level == 0
+                                              ? entry->clip
+                                              : slice_clip(entry->clip, chosen->segment.start_s,
+                                                           chosen->segment.length_s, seg_emb);
+                            ref.embedding = seg_emb;
+                            AudioClip view;
+                            view.samples = std::move(ref.latent);
+                            view.sample_rate = ref.latent_rate;
+                            AudioClip st = time_stretch(view, req.duration_s, pc.stft);
+                            ref.latent = std::move(st.samples);
+                            ref.duration_s = req.duration_s;
+                            pl.hit = true;
+                            pl.entry_id = chosen->entry_id;
+                            pl.similarity = cosine_similarity(req.prompt_embedding, seg_emb);
+                            pl.features = context_features(
+                                BanditContext{req.prompt_embedding, seg_emb, req.total_steps});
+                            pl.reference = std::move(ref);
+                        }
+                    } catch (const std::exception&) {
+                        pl = Plan{};
+                        pl.fallback = true;
+                    }
+                }
+                for (int64_t g = b0; g < b1; ++g) {
+                    const GenerationRequest& req = trace[(size_t)g];
+                    Plan& pl = plans[(size_t)(g - b0)];
+                    if (req.arrival_time_s < prev) return -2;
+                    prev = req.arrival_time_s;
+                    ServeOutcome o;
+                    o.request_id = req.id;
+                    o.fallback = pl.fallback;
+                    int arm = 0;
+                    if (pl.hit) {
+                        switch (pc.skip_policy) {
+                            case SkipPolicy::kModelExploit:
+                                arm = choose_arm(pc.gater, pl.features, GaterMode::kExploit);
+                                break;
+                            case SkipPolicy::kModelExplore:
+                                arm = choose_arm(pc.gater, pl.features, GaterMode::kExplore);
+                                break;
+                            case SkipPolicy::kRuleBased:
+                                arm = pl.similarity >= pc.rule_similarity_threshold
+                                          ? (int)std::llround(pc.rule_skip_fraction / 0.05) : 0;
+                                break;
+                            case SkipPolicy::kFixedArm: arm = pc.fixed_arm; break;
+                        }
+                    } else if (pc.skip_policy == SkipPolicy::kFixedArm) {
+                        arm = pc.fixed_arm;
+                    }
+                    double skip = arm_skip_fraction(arm);
+                    const uint64_t gen_seed = derive_seed(pc.seed, req.id, 3);
+                    GenerationResult res = generate(req.prompt_embedding, req.duration_s,
+                                                    req.total_steps, skip,
+                                                    pl.hit ? pl.reference : std::nullopt,
+                                                    gen_seed, pc.sim);
+                    o.cache_hit = pl.hit;
+                    if (pl.hit) o.entry_id = pl.entry_id;
+                    o.arm_index = arm;
+                    o.skip_fraction = skip;
+                    o.steps_skipped = req.total_steps - res.steps_executed;
+                    o.quality = res.quality;
+                    o.nfe_cost_s = res.nfe_cost_s;
+                    o.reference_similarity = pl.similarity;
+                    const double now_h = req.arrival_time_s / 3600.0;
+                    if (pl.hit)
+                        cache.record_reuse(pl.entry_id, o.steps_skipped, req.duration_s, now_h, skip);
+                    o.admitted_entry_id = cache.admit(std::move(res.clip), req.prompt_embedding,
+                                                      res.quality, now_h);
+                    const double start = std::max(req.arrival_time_s, busy);
+                    busy = start + o.nfe_cost_s;
+                    o.sim_latency_s = busy - req.arrival_time_s;
+                    rep.total_nfe_s += o.nfe_cost_s;
+                    rep.baseline_nfe_s += pc.sim.nfe_time_s(req.total_steps, req.duration_s);
+                    rep.outcomes.push_back(o);
+                    // run_maintenance (pipeline.cpp:280-297)
+                    for (uint64_t id : cache.refinement_candidates()) {
+                        RegenerateFn regen = [&](const EmbeddingVector& prompt, double d,
+                                                 uint64_t sd) {
+                            auto r = generate(prompt, d, pc.default_total_steps, 0.0,
+                                              std::nullopt, sd, pc.sim);
+                            return std::make_pair(std::move(r.clip), r.quality);
+                        };
+                        cache.refine(id, regen, maint);
+                        rep.refinements++;
+                    }
+                }
+            }
+            std::vector<double> lat;
+            double q = 0.0, r = 0.0, h = 0.0;
+            for (const auto& o : rep.outcomes) {
+                lat.push_back(o.sim_latency_s);
+                q += o.quality;
+                r += reward(o.arm_index, o.quality, pc.gater.alpha);
+                h += o.cache_hit ? 1.0 : 0.0;
+            }
+            std::sort(lat.begin(), lat.end());
+            const double nn = (double)rep.outcomes.size();
+            if (nn > 0) {
+                auto pct = [&](double p) {
+                    size_t idx = (size_t)std::ceil(p * lat.size());
+                    return lat[std::min(lat.size() - 1, idx > 0 ? idx - 1 : 0)];
+                };
+                rep.mean_quality = q / nn;
+                rep.mean_reward = r / nn;
+                rep.hit_rate = h / nn;
+                double ls = 0.0;
+                for (double l : lat) ls += l;
+                rep.mean_latency_s = ls / nn;
+                rep.median_latency_s = pct(0.5);
+                rep.p95_latency_s = pct(0.95);
+            }
+            rep.speedup = rep.total_nfe_s > 0.0 ? rep.baseline_nfe_s / rep.total_nfe_s : 1.0;
+        }
+        if (wall_s)
+            *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (size_t i = 0; i < rep.outcomes.size(); ++i) copy_out(rep.outcomes[i], out + i);
+        if (summary) {
+            const double v[10] = {rep.total_nfe_s, rep.baseline_nfe_s, rep.speedup,
+                                  rep.mean_quality, rep.mean_reward, rep.hit_rate,
+                                  rep.mean_latency_s, rep.median_latency_s, rep.p95_latency_s,
+                                  (double)rep.refinements};
+            std::memcpy(summary, v, sizeof(v));
+        }
+        return (int)rep.outcomes.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
 }
 
 }  // extern "C"

@@ -60,6 +60,40 @@ class SwcmConfig(C.Structure):
                 ("refine_skip_threshold", C.c_double), ("latent_capacity", C.c_int64)]
 
 
+class SwrWorkload(C.Structure):
+    _fields_ = [("n_prompts", C.c_int64), ("cluster_count", C.c_int32), ("dim", C.c_int32),
+                ("near_duplicate_rate", C.c_double), ("cluster_perturbation", C.c_double),
+                ("duplicate_perturbation", C.c_double), ("duration_lo_s", C.c_double),
+                ("duration_hi_s", C.c_double), ("arrival_rate_hz", C.c_double),
+                ("total_steps", C.c_int32), ("reserved", C.c_int32)]
+
+
+class SwrConfig(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("selector", SwSelectorConfig), ("policy", SwPolicy),
+                ("q_max", C.c_double), ("penalty_slope", C.c_double), ("noise_scale", C.c_double),
+                ("skip_headroom", C.c_double), ("step_time_s_per_10s", C.c_double),
+                ("alpha", C.c_double), ("latent_rate", C.c_int32),
+                ("default_total_steps", C.c_int32), ("refinement_enabled", C.c_int32),
+                ("batch", C.c_int32)]
+
+
+class SwrStats(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("total_s", "lookup_s", "mutation_s", "maintenance_s")] + \
+               [(n, C.c_int64) for n in ("batches", "lookups", "admits", "evictions",
+                                          "refinements", "reuses")] + \
+               [(n, C.c_double) for n in ("total_nfe_s", "baseline_nfe_s", "speedup",
+                                           "mean_quality", "mean_reward", "hit_rate",
+                                           "mean_latency_s", "median_latency_s", "p95_latency_s")]
+
+
+OUTCOME_DTYPE = np.dtype([("request_id", "<u8"), ("cache_hit", "<i4"), ("arm_index", "<i4"),
+                          ("steps_skipped", "<i4"), ("fallback", "<i4"), ("entry_id", "<u8"),
+                          ("admitted_entry_id", "<u8"), ("quality", "<f8"), ("nfe_cost_s", "<f8"),
+                          ("sim_latency_s", "<f8"), ("skip_fraction", "<f8"),
+                          ("reference_similarity", "<f8")])
+assert OUTCOME_DTYPE.itemsize == 80
+
+
 REGEN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_uint64,
                        C.POINTER(C.c_float), C.POINTER(C.c_double), C.POINTER(C.c_float),
                        C.POINTER(C.c_int32))
@@ -74,7 +108,7 @@ REQUEST_DTYPE = np.dtype([("id", "<u8"), ("duration_s", "<f8"), ("total_steps", 
                           ("reserved", "<i4")])
 CHOICE_DTYPE = np.dtype([("hit", "<i4"), ("arm", "<i4"), ("steps_skipped", "<i4"),
                          ("n_hits", "<i4"), ("entry_id", "<u8"), ("level", "<i4"),
-                         ("seg_reserved", "<i4"), ("start_s", "<f8"), ("length_s", "<f8"),
+                         ("row", "<i4"), ("start_s", "<f8"), ("length_s", "<f8"),
                          ("similarity", "<f8"), ("skip_fraction", "<f8"), ("pick", "<i4"),
                          ("flags", "<u4"), ("t_out", "<i4"), ("owner", "<i4"), ("slot", "<i8")])
 assert SEGMENT_DTYPE.itemsize == 24 and HIT_DTYPE.itemsize == 40
@@ -187,6 +221,11 @@ def lib() -> C.CDLL:
         "sw_search_host_ex": ([vp, vp, i32, i32, i32, vp, vp], C.c_int),
         "sw_score_candidates_host": ([vp, i32, i32, vp, vp, vp, f64, vp, vp], C.c_int),
         "sw_select_host": ([vp, i32, vp, vp, f64, f64, f64, vp, vp], C.c_int),
+        "sw_choice_rows": ([vp, vp, i32, vp, vp], C.c_int),
+        "sw_negative_embedding": ([i32, vp], C.c_int),
+        "swr_synth_workload": ([C.POINTER(SwrWorkload), u64, vp, vp, vp, vp], C.c_int),
+        "swr_replay": ([vp, vp, C.POINTER(SwrConfig), i64, vp, vp, vp, vp, vp,
+                        C.POINTER(SwrStats)], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -209,7 +248,8 @@ EXPORTED = [
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
     "sw_overflow_stats", "sw_arena_capacity", "sw_arena_reserve", "sw_arena_row_count",
     "sw_arena_export", "sw_index_check_consistent", "sw_ivf_set_rebuild_interval", "sw_ivf_build",
-    "sw_search_host_ex", "sw_score_candidates_host", "sw_select_host",
+    "sw_search_host_ex", "sw_score_candidates_host", "sw_select_host", "sw_choice_rows",
+    "sw_negative_embedding", "swr_synth_workload", "swr_replay",
     "swcm_create", "swcm_destroy", "swcm_admit", "swcm_last_evicted", "swcm_record_reuse",
     "swcm_evict_if_full", "swcm_refinement_candidates", "swcm_refine", "swcm_importance",
     "swcm_size", "swcm_ids", "swcm_check_consistent", "sw_ivf_configure", "sw_ivf_set_nprobe",

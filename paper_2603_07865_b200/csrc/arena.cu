@@ -328,4 +328,22 @@ void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, 
     cudaFreeAsync(offs, st);
 }
 
+namespace {
+// chosen segment row of each request (slot * Rp + segment.reserved), zeros on a miss
+__global__ void k_choice_rows(const sw_choice* __restrict__ ch, int B, const float* __restrict__ rows,
+                              int Rp, int Df, int D, float* __restrict__ out) {
+    const int b = blockIdx.x;
+    if (b >= B) return;
+    const sw_choice c = ch[b];
+    const float* src = c.hit ? rows + ((int64_t)c.slot * Rp + c.segment.reserved) * Df : nullptr;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) out[(int64_t)b * D + d] = src ? src[d] : 0.0f;
+}
+}  // namespace
+
+void launch_choice_rows(Ctx& c, const sw_choice* d_ch, int B, float* d_rows, cudaStream_t st) {
+    if (B <= 0) return;
+    k_choice_rows<<<B, 128, 0, st>>>(d_ch, B, c.rows, c.Rp, c.Df, c.D, d_rows);
+    SW_CUDA(cudaGetLastError());
+}
+
 }  // namespace sw

@@ -138,6 +138,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     c.Bmax = cfg.max_batch;
     c.BmaxPad = (cfg.max_batch + 127) / 128 * 128;
     const int64_t nrow = c.S * c.Rp;
+    SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
     dalloc(&c.rows, (size_t)nrow * c.Df);
     dalloc(&c.rows_bf, (size_t)nrow * c.Dp);
     dalloc(&c.sneg, (size_t)nrow);
@@ -172,7 +173,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
         const int64_t chunks = (c.Bmax + kOvfQG - 1) / kOvfQG;
         const size_t words = (size_t)kOvfHdr + (size_t)c.Bmax + 2 * (size_t)chunks;
         dalloc(&c.ovf_state, words);
-        SW_CUDA(cudaMemset(c.ovf_state, 0, sizeof(int32_t) * words));
+        mfill(c, c.ovf_state, 0, sizeof(int32_t) * words);
         int nsm = 0;
         SW_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
         const size_t rec = 16;  // {double sim, int32 slot, int32 row}
@@ -187,8 +188,7 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     dalloc(&c.prank, (size_t)c.Bmax * kMaxCentroids);
     dalloc(&c.pmask, (size_t)c.Bmax * 4);
     c.ivf_rows.assign((size_t)c.S, 0);
-    SW_CUDA(cudaMemset(c.row_list, 0xFF, sizeof(int16_t) * (size_t)nrow));  // no list
-    SW_CUDA(cudaStreamCreateWithFlags(&c.mstream, cudaStreamNonBlocking));
+    mfill(c, c.row_list, 0xFF, sizeof(int16_t) * (size_t)nrow);  // no list
     SW_CUDA(cudaMemsetAsync(c.valid, 0, (size_t)c.S, c.mstream));
     SW_CUDA(cudaMemsetAsync(c.valid_bits, 0, sizeof(uint32_t) * (size_t)(c.S / 32 + 16), c.mstream));
     SW_CUDA(cudaMemsetAsync(c.nrows, 0, sizeof(int32_t) * (size_t)c.S, c.mstream));
@@ -222,11 +222,11 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
 // Reallocates a device array from n_old to n_new elements, keeping the first n_old and
 // filling the tail with byte `fill`.
 template <class T>
-static void regrow(T** p, size_t n_old, size_t n_new, int fill) {
+static void regrow(Ctx& c, T** p, size_t n_old, size_t n_new, int fill) {
     T* q = nullptr;
     dalloc(&q, n_new);
-    if (*p && n_old) SW_CUDA(cudaMemcpy(q, *p, sizeof(T) * n_old, cudaMemcpyDeviceToDevice));
-    SW_CUDA(cudaMemset(q + n_old, fill, sizeof(T) * (n_new - n_old)));
+    if (*p && n_old) mcopy(c, q, *p, sizeof(T) * n_old, cudaMemcpyDeviceToDevice);
+    mfill(c, q + n_old, fill, sizeof(T) * (n_new - n_old));
     if (*p) cudaFree(*p);
     *p = q;
 }
@@ -239,20 +239,20 @@ static void grow_arena(Ctx& c, int64_t entries) {
     const int64_t S2 = (entries + 1 + per_tile - 1) / per_tile * per_tile;
     if (S2 <= c.S) return;
     const int64_t S = c.S, nrow = S * c.Rp, nrow2 = S2 * c.Rp;
-    regrow(&c.rows, (size_t)nrow * c.Df, (size_t)nrow2 * c.Df, 0);
-    regrow(&c.rows_bf, (size_t)nrow * c.Dp, (size_t)nrow2 * c.Dp, 0);
-    regrow(&c.sneg, (size_t)nrow, (size_t)nrow2, 0);
-    regrow(&c.segs, (size_t)nrow, (size_t)nrow2, 0);
-    regrow(&c.row_list, (size_t)nrow, (size_t)nrow2, 0xFF);
-    regrow(&c.ids, (size_t)S, (size_t)S2, 0);
-    regrow(&c.nrows, (size_t)S, (size_t)S2, 0);
-    regrow(&c.valid, (size_t)S, (size_t)S2, 0);
-    regrow(&c.tsrc, (size_t)S, (size_t)S2, 0);
-    regrow(&c.valid_bits, (size_t)(S / 32 + 16), (size_t)(S2 / 32 + 16), 0);
+    regrow(c, &c.rows, (size_t)nrow * c.Df, (size_t)nrow2 * c.Df, 0);
+    regrow(c, &c.rows_bf, (size_t)nrow * c.Dp, (size_t)nrow2 * c.Dp, 0);
+    regrow(c, &c.sneg, (size_t)nrow, (size_t)nrow2, 0);
+    regrow(c, &c.segs, (size_t)nrow, (size_t)nrow2, 0);
+    regrow(c, &c.row_list, (size_t)nrow, (size_t)nrow2, 0xFF);
+    regrow(c, &c.ids, (size_t)S, (size_t)S2, 0);
+    regrow(c, &c.nrows, (size_t)S, (size_t)S2, 0);
+    regrow(c, &c.valid, (size_t)S, (size_t)S2, 0);
+    regrow(c, &c.tsrc, (size_t)S, (size_t)S2, 0);
+    regrow(c, &c.valid_bits, (size_t)(S / 32 + 16), (size_t)(S2 / 32 + 16), 0);
     const int64_t L2 = c.cfg.latent_slots > 0 ? std::min<int64_t>(c.cfg.latent_slots, S2) : S2;
     if (c.latent && L2 != c.Lslots) {  // slot % Lslots is unchanged for every stored slot
         const size_t per = (size_t)c.C * c.Tmax * c.F;
-        regrow(&c.latent, (size_t)c.Lslots * per, (size_t)L2 * per, 0);
+        regrow(c, &c.latent, (size_t)c.Lslots * per, (size_t)L2 * per, 0);
     }
     c.Lslots = L2;
     c.S = S2;
@@ -289,8 +289,8 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
     std::vector<uint64_t> h_ids((size_t)n);
     std::vector<int64_t> h_off((size_t)n + 1);
     if (on_device) {
-        SW_CUDA(cudaMemcpy(h_ids.data(), ids, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(h_off.data(), row_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+        mcopy(c, h_ids.data(), ids, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost);
+        mcopy(c, h_off.data(), row_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost);
     } else {
         std::memcpy(h_ids.data(), ids, sizeof(uint64_t) * n);
         std::memcpy(h_off.data(), row_off, sizeof(int64_t) * (n + 1));
@@ -528,7 +528,7 @@ int sw_set_schedule(sw_ctx* ctx, const double* abar, int32_t n) {
             dalloc(&c.abar, (size_t)n);
             c.n_abar = n;
         }
-        SW_CUDA(cudaMemcpy(c.abar, abar, sizeof(double) * n, cudaMemcpyHostToDevice));
+        mcopy(c, c.abar, abar, sizeof(double) * n, cudaMemcpyHostToDevice);
         return SW_OK;
     });
 }
@@ -661,11 +661,11 @@ int64_t sw_arena_export(sw_ctx* ctx, int64_t first, int64_t count, uint64_t* ids
         if (rows) blk.resize((size_t)(s1 - s0) * c.Rp * c.Df);
         if (segs) sblk.resize((size_t)(s1 - s0) * c.Rp);
         if (rows)
-            SW_CUDA(cudaMemcpy(blk.data(), c.rows + s0 * c.Rp * c.Df, sizeof(float) * blk.size(),
-                               cudaMemcpyDeviceToHost));
+            mcopy(c, blk.data(), c.rows + s0 * c.Rp * c.Df, sizeof(float) * blk.size(),
+                  cudaMemcpyDeviceToHost);
         if (segs)
-            SW_CUDA(cudaMemcpy(sblk.data(), c.segs + s0 * c.Rp, sizeof(sw_segment) * sblk.size(),
-                               cudaMemcpyDeviceToHost));
+            mcopy(c, sblk.data(), c.segs + s0 * c.Rp, sizeof(sw_segment) * sblk.size(),
+                  cudaMemcpyDeviceToHost);
         for (int64_t i = 0; i < n; ++i) {
             const int64_t slot = live[(size_t)(first + i)].first;
             ids[i] = live[(size_t)(first + i)].second;
@@ -699,7 +699,7 @@ int sw_index_check_consistent(sw_ctx* ctx) {
         for (const auto& kv : c.slot_of) valid += c.h_nrows[(size_t)kv.second] > 0 ? 1 : 0;
         std::vector<uint8_t> v((size_t)c.high_water);
         if (c.high_water)
-            SW_CUDA(cudaMemcpy(v.data(), c.valid, (size_t)c.high_water, cudaMemcpyDeviceToHost));
+            mcopy(c, v.data(), c.valid, (size_t)c.high_water, cudaMemcpyDeviceToHost);
         int64_t dv = 0;
         for (uint8_t x : v) dv += x ? 1 : 0;
         if (dv != valid) return 0;
@@ -886,8 +886,8 @@ int sw_ivf_entry_lists(sw_ctx* ctx, uint64_t id, int16_t* lists, int32_t cap) {
         auto it = c.slot_of.find(id);
         if (it == c.slot_of.end()) return 0;
         const int nr = std::min(cap, c.ivf_rows[(size_t)it->second]);
-        SW_CUDA(cudaMemcpy(lists, c.row_list + it->second * c.Rp, sizeof(int16_t) * nr,
-                           cudaMemcpyDeviceToHost));
+        mcopy(c, lists, c.row_list + it->second * c.Rp, sizeof(int16_t) * nr,
+              cudaMemcpyDeviceToHost);
         return nr;
     });
 }
@@ -972,8 +972,10 @@ int sw_arena_read_rows(sw_ctx* ctx, uint64_t id, float* rows, int32_t cap) {
         auto it = c.slot_of.find(id);
         if (it == c.slot_of.end()) return -1;
         const int n = std::min(cap, c.h_nrows[(size_t)it->second]);
-        SW_CUDA(cudaMemcpy2D(rows, sizeof(float) * c.D, c.rows + it->second * c.Rp * c.Df,
-                             sizeof(float) * c.Df, sizeof(float) * c.D, n, cudaMemcpyDeviceToHost));
+        SW_CUDA(cudaMemcpy2DAsync(rows, sizeof(float) * c.D, c.rows + it->second * c.Rp * c.Df,
+                                  sizeof(float) * c.Df, sizeof(float) * c.D, n,
+                                  cudaMemcpyDeviceToHost, c.mstream));
+        SW_CUDA(cudaStreamSynchronize(c.mstream));
         return n;
     });
 }
@@ -1596,6 +1598,16 @@ int sw_debug_query_stats(sw_ctx* ctx, int32_t B, int32_t* stats) {
         SW_CUDA(cudaSetDevice(ctx->c.device));
         SW_CUDA(cudaDeviceSynchronize());
         SW_CUDA(cudaMemcpy(stats, ctx->c.dbg, sizeof(int32_t) * 8 * B, cudaMemcpyDeviceToHost));
+        return SW_OK;
+    });
+}
+
+int sw_choice_rows(sw_ctx* ctx, const sw_choice* d_ch, int32_t B, float* d_rows, void* stream) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && (B == 0 || (d_ch && d_rows)), "null argument");
+        Ctx& c = ctx->c;
+        HotGuard lk(c, as_stream(stream));
+        launch_choice_rows(c, d_ch, B, d_rows, as_stream(stream));
         return SW_OK;
     });
 }

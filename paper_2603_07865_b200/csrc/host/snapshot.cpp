@@ -136,7 +136,7 @@ void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uin
         std::vector<float> pad((size_t)C * c.Df, 0.0f);
         for (uint32_t j = 0; j < C; ++j)
             std::memcpy(pad.data() + (size_t)j * c.Df, cent.data() + (size_t)j * dim, 4 * dim);
-        SW_CUDA(cudaMemcpy(c.cent, pad.data(), 4 * pad.size(), cudaMemcpyHostToDevice));
+        mcopy(c, c.cent, pad.data(), 4 * pad.size(), cudaMemcpyHostToDevice);
     }
     // stored list of every row (the snapshot's lists, not recomputed); pad rows in no list
     {
@@ -153,8 +153,8 @@ void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uin
         const int64_t slot = c.slot_of.at(id);
         const int nr = c.h_nrows[(size_t)slot];
         c.ivf_rows[(size_t)slot] = nr;
-        SW_CUDA(cudaMemcpy(c.row_list + slot * c.Rp, lists.data() + k, sizeof(int16_t) * nr,
-                           cudaMemcpyHostToDevice));
+        mcopy(c, c.row_list + slot * c.Rp, lists.data() + k, sizeof(int16_t) * nr,
+                           cudaMemcpyHostToDevice);
         k += (size_t)nr;
     }
 }
@@ -168,9 +168,9 @@ void swix_save(Ctx& c, const char* path) {
     std::vector<sw_segment> segs((size_t)nrow);
     std::vector<int16_t> lists((size_t)nrow);
     if (nrow > 0) {
-        SW_CUDA(cudaMemcpy(rows.data(), c.rows, 4 * rows.size(), cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(segs.data(), c.segs, sizeof(sw_segment) * nrow, cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(lists.data(), c.row_list, 2 * nrow, cudaMemcpyDeviceToHost));
+        mcopy(c, rows.data(), c.rows, 4 * rows.size(), cudaMemcpyDeviceToHost);
+        mcopy(c, segs.data(), c.segs, sizeof(sw_segment) * nrow, cudaMemcpyDeviceToHost);
+        mcopy(c, lists.data(), c.row_list, 2 * nrow, cudaMemcpyDeviceToHost);
     }
     const int C = c.ivf ? c.ivf_C : 1;
     std::vector<std::vector<std::pair<uint64_t, int64_t>>> per(C);

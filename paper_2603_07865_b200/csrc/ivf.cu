@@ -408,11 +408,11 @@ void upload_centroids(Ctx& c, const std::vector<float>& h, int C) {
         std::copy(h.begin() + (size_t)j * c.D, h.begin() + (size_t)(j + 1) * c.D,
                   pad.begin() + (size_t)j * c.Df);
     if (C > 0)
-        SW_CUDA(cudaMemcpy(c.cent, pad.data(), sizeof(float) * pad.size(), cudaMemcpyHostToDevice));
+        mcopy(c, c.cent, pad.data(), sizeof(float) * pad.size(), cudaMemcpyHostToDevice);
 }
 
 void fetch_row(Ctx& c, int64_t row, float* out) {
-    SW_CUDA(cudaMemcpy(out, c.rows + row * c.Df, sizeof(float) * c.D, cudaMemcpyDeviceToHost));
+    mcopy(c, out, c.rows + row * c.Df, sizeof(float) * c.D, cudaMemcpyDeviceToHost);
 }
 
 // kmeans (index.cpp:59-184) over the rows perm[0..n) (arena row indices, reference input order).
@@ -422,7 +422,7 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
     cudaStream_t st = c.mstream;
     MtRng rng(seed);
     DBuf<int64_t> d_perm((size_t)n);
-    SW_CUDA(cudaMemcpy(d_perm.p, perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice);
     std::vector<float> cent((size_t)cnum * D);
     auto crow = [&](int j) { return cent.data() + (size_t)j * D; };
 
@@ -435,7 +435,7 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
     const int TB = 256;
     const int nb = (int)((n + TB - 1) / TB);
     auto d2_pass = [&](int j, int init) {
-        SW_CUDA(cudaMemcpy(d_c.p, crow(j), sizeof(float) * D, cudaMemcpyHostToDevice));
+        mcopy(c, d_c.p, crow(j), sizeof(float) * D, cudaMemcpyHostToDevice);
         k_seed_d2<<<nb, TB, sizeof(float) * D, st>>>(c.rows, c.Df, D, d_perm.p, n, d_c.p, d_d2.p,
                                                      init);
         SW_CUDA(cudaGetLastError());
@@ -512,8 +512,8 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
                 SW_CUDA(cudaGetLastError());
                 std::vector<double> hv((size_t)fb);
                 std::vector<int64_t> hi((size_t)fb);
-                SW_CUDA(cudaMemcpy(hv.data(), bv.p, sizeof(double) * fb, cudaMemcpyDeviceToHost));
-                SW_CUDA(cudaMemcpy(hi.data(), bi.p, sizeof(int64_t) * fb, cudaMemcpyDeviceToHost));
+                mcopy(c, hv.data(), bv.p, sizeof(double) * fb, cudaMemcpyDeviceToHost);
+                mcopy(c, hi.data(), bi.p, sizeof(int64_t) * fb, cudaMemcpyDeviceToHost);
                 double worst = -2.0;
                 int64_t pick = 0;
                 for (int b = 0; b < fb; ++b)
@@ -554,8 +554,8 @@ void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector
     if (slots.empty()) return;
     DBuf<int64_t> d_s(slots.size());
     DBuf<int32_t> d_n(nr.size());
-    SW_CUDA(cudaMemcpy(d_s.p, slots.data(), sizeof(int64_t) * slots.size(), cudaMemcpyHostToDevice));
-    SW_CUDA(cudaMemcpy(d_n.p, nr.data(), sizeof(int32_t) * nr.size(), cudaMemcpyHostToDevice));
+    mcopy(c, d_s.p, slots.data(), sizeof(int64_t) * slots.size(), cudaMemcpyHostToDevice);
+    mcopy(c, d_n.p, nr.data(), sizeof(int32_t) * nr.size(), cudaMemcpyHostToDevice);
     const int64_t tot = (int64_t)slots.size() * c.Rp;
     k_list_tails<<<(unsigned)((tot + 255) / 256), 256, 0, c.mstream>>>(d_s.p, d_n.p,
                                                                     (int64_t)slots.size(), c.Rp,
@@ -576,8 +576,8 @@ static std::vector<int64_t> rebuild_order(Ctx& c) {
     std::vector<int64_t> perm;
     for (auto& [id, slot] : ents) {
         const int nr = c.ivf_rows[(size_t)slot];
-        SW_CUDA(cudaMemcpy(segs.data(), c.segs + slot * c.Rp, sizeof(sw_segment) * nr,
-                           cudaMemcpyDeviceToHost));
+        mcopy(c, segs.data(), c.segs + slot * c.Rp, sizeof(sw_segment) * nr,
+                           cudaMemcpyDeviceToHost);
         std::vector<int> o((size_t)nr);
         std::iota(o.begin(), o.end(), 0);
         std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
@@ -604,7 +604,7 @@ void ivf_rebuild(Ctx& c) {
     const int cnum = (int)std::min<int64_t>((int64_t)perm.size(), std::max(c.ivf_target, 1));
     kmeans(c, perm, cnum, dev::derive_seed(c.ivf_seed, c.ivf_rebuilds, 0, 0));
     DBuf<int64_t> d_perm(perm.size());
-    SW_CUDA(cudaMemcpy(d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice));
+    mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_perm.p, (int64_t)perm.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
 }
@@ -624,7 +624,7 @@ void ivf_build_from(Ctx& c, const std::vector<int64_t>& perm) {
     const int cnum = (int)std::min<int64_t>((int64_t)perm.size(), std::max(c.ivf_target, 1));
     kmeans(c, perm, cnum, c.ivf_seed);
     DBuf<int64_t> d_perm(perm.size());
-    SW_CUDA(cudaMemcpy(d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice));
+    mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_perm.p, (int64_t)perm.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
 }
@@ -645,8 +645,8 @@ bool ivf_check_consistent(Ctx& c) {
     std::vector<int16_t> have(rows.size());
     {
         std::vector<int16_t> all((size_t)c.high_water * c.Rp);
-        SW_CUDA(cudaMemcpy(all.data(), c.row_list, sizeof(int16_t) * all.size(),
-                           cudaMemcpyDeviceToHost));
+        mcopy(c, all.data(), c.row_list, sizeof(int16_t) * all.size(),
+                           cudaMemcpyDeviceToHost);
         for (size_t i = 0; i < rows.size(); ++i) have[i] = all[(size_t)rows[i]];
     }
     if (!c.ivf) {
@@ -657,11 +657,11 @@ bool ivf_check_consistent(Ctx& c) {
     if (c.ivf_C == 0) return false;
     DBuf<int64_t> d_rows(rows.size());
     DBuf<int32_t> d_as(rows.size());
-    SW_CUDA(cudaMemcpy(d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice));
+    mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_rows.p, (int64_t)rows.size(), c.ivf_C, nullptr, d_as.p, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
     std::vector<int32_t> as(rows.size());
-    SW_CUDA(cudaMemcpy(as.data(), d_as.p, sizeof(int32_t) * as.size(), cudaMemcpyDeviceToHost));
+    mcopy(c, as.data(), d_as.p, sizeof(int32_t) * as.size(), cudaMemcpyDeviceToHost);
     for (size_t i = 0; i < rows.size(); ++i)
         if ((int32_t)have[i] != as[i]) return false;
     return true;
@@ -700,8 +700,8 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
             for (int r = 0; r < nr[e]; ++r) rows.push_back(slot[e] * c.Rp + base[e] + r);
         if (!rows.empty()) {
             DBuf<int64_t> d_rows(rows.size());
-            SW_CUDA(cudaMemcpy(d_rows.p, rows.data(), sizeof(int64_t) * rows.size(),
-                               cudaMemcpyHostToDevice));
+            mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(),
+                               cudaMemcpyHostToDevice);
             argmax_rows(c, d_rows.p, (int64_t)rows.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
             SW_CUDA(cudaStreamSynchronize(c.mstream));
         }
@@ -729,7 +729,7 @@ void ivf_set_centroids(Ctx& c, const float* h, int C) {
         for (int r = 0; r < c.ivf_rows[(size_t)kv.second]; ++r) rows.push_back(kv.second * c.Rp + r);
     if (!rows.empty() && C > 0) {
         DBuf<int64_t> d_rows(rows.size());
-        SW_CUDA(cudaMemcpy(d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice));
+        mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice);
         argmax_rows(c, d_rows.p, (int64_t)rows.size(), C, c.row_list, nullptr, c.mstream);
         SW_CUDA(cudaStreamSynchronize(c.mstream));
     }
@@ -744,8 +744,8 @@ static void build_sorted(Ctx& c) {
     std::vector<uint8_t> valid((size_t)S);
     std::vector<int16_t> rl((size_t)S);
     if (S > 0) {
-        SW_CUDA(cudaMemcpy(valid.data(), c.valid, S, cudaMemcpyDeviceToHost));
-        SW_CUDA(cudaMemcpy(rl.data(), c.row_list, 2 * S, cudaMemcpyDeviceToHost));
+        mcopy(c, valid.data(), c.valid, S, cudaMemcpyDeviceToHost);
+        mcopy(c, rl.data(), c.row_list, 2 * S, cudaMemcpyDeviceToHost);
     }
     std::vector<int64_t> cnt((size_t)C, 0);
     for (int64_t i = 0; i < S; ++i)
@@ -803,15 +803,15 @@ static void build_sorted(Ctx& c) {
     for (int64_t r = 0; r < c.grp_rows; ++r)
         if (sorted[(size_t)r] >= 0) vb[(size_t)(r >> 5)] |= 1u << (r & 31);
     if (c.grp_rows > 0)
-        SW_CUDA(cudaMemcpy(c.d_sorted_slot, sorted.data(), sizeof(int32_t) * c.grp_rows,
-                           cudaMemcpyHostToDevice));
-    SW_CUDA(cudaMemcpy(c.d_sorted_vbits, vb.data(), sizeof(uint32_t) * vb.size(),
-                       cudaMemcpyHostToDevice));
+        mcopy(c, c.d_sorted_slot, sorted.data(), sizeof(int32_t) * c.grp_rows,
+                           cudaMemcpyHostToDevice);
+    mcopy(c, c.d_sorted_vbits, vb.data(), sizeof(uint32_t) * vb.size(),
+                       cudaMemcpyHostToDevice);
     std::vector<int32_t> t0v(kMaxCentroids, 0), ntv(kMaxCentroids, 0);
     std::copy(c.grp_tile0.begin(), c.grp_tile0.end(), t0v.begin());
     std::copy(c.grp_ntiles.begin(), c.grp_ntiles.end(), ntv.begin());
-    SW_CUDA(cudaMemcpy(c.d_list_tile0, t0v.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice));
-    SW_CUDA(cudaMemcpy(c.d_list_ntiles, ntv.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice));
+    mcopy(c, c.d_list_tile0, t0v.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice);
+    mcopy(c, c.d_list_ntiles, ntv.data(), 4 * kMaxCentroids, cudaMemcpyHostToDevice);
     if (c.grp_rows > 0) {
         k_sort_rows<<<(unsigned)((c.grp_rows + 7) / 8), 256, 0, c.mstream>>>(
             c.d_sorted_slot, c.grp_rows, c.rows_bf, c.Dp, c.d_rows_sorted);

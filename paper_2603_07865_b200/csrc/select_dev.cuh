@@ -208,6 +208,7 @@ __device__ __forceinline__ sw_choice select_one(const HitRec* __restrict__ h, in
             c.segment.level = ch.level;
             c.segment.start_s = ch.start_s;
             c.segment.length_s = ch.length_s;
+            c.segment.reserved = ch.row;  // pyramid row of the matched segment
             c.similarity = ch.sim;  // cos(prompt, seg_emb) (pipeline.cpp:173)
             c.owner = ch.owner;
             c.slot = ch.slot;
@@ -321,6 +322,7 @@ __device__ __forceinline__ sw_choice select_warp(const HitRec* __restrict__ h, i
         c.segment.level = ch.level;
         c.segment.start_s = ch.start_s;
         c.segment.length_s = ch.length_s;
+        c.segment.reserved = ch.row;  // pyramid row of the matched segment
         c.similarity = ch.sim;  // cos(prompt, seg_emb) (pipeline.cpp:173)
         c.owner = ch.owner;
         c.slot = ch.slot;

@@ -276,6 +276,22 @@ struct Ctx {
     std::map<const void*, size_t> smem_attr;
 };
 
+// Host <-> device copies and fills outside the batched hot path: stream-ordered on the context's
+// mutation stream and complete on return. A plain cudaMemcpy / cudaMemset runs on the legacy
+// default stream, which does NOT order against the non-blocking mutation / caller streams: a
+// pageable H2D may still be in flight when a kernel launched right after on mstream reads its
+// destination (this raced the IVF k-means and corrupted host state under heavy churn).
+inline void mcopy(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    if (bytes == 0) return;
+    SW_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, c.mstream));
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+}
+inline void mfill(Ctx& c, void* dst, int value, size_t bytes) {
+    if (bytes == 0) return;
+    SW_CUDA(cudaMemsetAsync(dst, value, bytes, c.mstream));
+    SW_CUDA(cudaStreamSynchronize(c.mstream));
+}
+
 // nprobe of the current search: a per-call override (search(q, k, nprobe)) or set_nprobe's
 inline int eff_nprobe(const Ctx& c) { return c.nprobe_override > 0 ? c.nprobe_override : c.ivf_nprobe; }
 
@@ -340,6 +356,7 @@ void launch_insert_rows_full(Ctx& c, int64_t n, const int64_t* d_slot, const int
 void launch_copy_latents(Ctx& c, int64_t n, const int64_t* d_slot, const float* d_lat,
                          const int64_t* d_lat_off, const int32_t* d_tsrc, cudaStream_t st);
 void launch_recompute_sneg(Ctx& c, cudaStream_t st);
+void launch_choice_rows(Ctx& c, const sw_choice* d_ch, int B, float* d_rows, cudaStream_t st);
 void launch_clear_slot(Ctx& c, int64_t slot, cudaStream_t st);
 void launch_fill_synthetic(Ctx& c, int64_t slot0, int64_t n, uint64_t first_id, uint64_t seed,
                            double delta, cudaStream_t st);

@@ -274,6 +274,9 @@ Tables tables_for(int n) {
     SW_CUDA(cudaMemcpy(tb.window, w.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
     SW_CUDA(cudaMemcpy(tb.tw_fwd, tf.data(), sizeof(double2) * tf.size(), cudaMemcpyHostToDevice));
     SW_CUDA(cudaMemcpy(tb.tw_inv, ti.data(), sizeof(double2) * ti.size(), cudaMemcpyHostToDevice));
+    // the legacy-stream copies do not order against the caller's (non-blocking) stream: make
+    // the tables complete before any kernel reads them (once per device and window)
+    SW_CUDA(cudaDeviceSynchronize());
     cache[{dev, n}] = tb;
     return tb;
 }

@@ -20,8 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import (CHOICE_DTYPE, HIT_DTYPE, POLICY, REQUEST_DTYPE, SEGMENT_DTYPE, SwConfig,
-                   SwPolicy, SwSelectorConfig, check, ptr)
+from ._lib import (CHOICE_DTYPE, HIT_DTYPE, OUTCOME_DTYPE, POLICY, REQUEST_DTYPE, SEGMENT_DTYPE,
+                   SwConfig, SwPolicy, SwSelectorConfig, check, ptr)
 
 
 def _torch():
@@ -556,3 +556,89 @@ class Batcher:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------- trace replay (config 5)
+def _splitmix64(x: int) -> int:  # core.cpp:58-63
+    M = (1 << 64) - 1
+    x = (x + 0x9e3779b97f4a7c15) & M
+    x = ((x ^ (x >> 30)) * 0xbf58476d1ce4e5b9) & M
+    x = ((x ^ (x >> 27)) * 0x94d049bb133111eb) & M
+    return x ^ (x >> 31)
+
+
+def derive_seed(base: int, a: int, b: int = 0, c: int = 0) -> int:  # core.cpp:65-71
+    s = _splitmix64(base ^ 0x53454d5741524d)
+    s = _splitmix64(s ^ a)
+    s = _splitmix64(s ^ b)
+    return _splitmix64(s ^ c)
+
+
+def negative_embedding(dim: int) -> np.ndarray:
+    """make_negative_embedding (selector.cpp:16-20)."""
+    out = np.zeros(dim, np.float32)
+    check(_lib.lib().sw_negative_embedding(dim, ptr(out)), "sw_negative_embedding")
+    return out
+
+
+def synth_workload(n: int, dim: int = 512, seed: int = 7, **kw):
+    """synth_workload (simgen.cpp:162-194), bit-identical: (prompts [n, dim], durations,
+    arrivals, total_steps). kw overrides WorkloadConfig fields (simgen.hpp:87-98)."""
+    w = _lib.SwrWorkload(n, kw.get("cluster_count", 16), dim, kw.get("near_duplicate_rate", 0.9),
+                         kw.get("cluster_perturbation", 0.5), kw.get("duplicate_perturbation", 0.16),
+                         kw.get("duration_lo_s", 4.0), kw.get("duration_hi_s", 12.0),
+                         kw.get("arrival_rate_hz", 1.2), kw.get("total_steps", 200), 0)
+    p = np.zeros((n, dim), np.float32)
+    d, a = np.zeros(n), np.zeros(n)
+    t = np.zeros(n, np.int32)
+    check(_lib.lib().swr_synth_workload(C.byref(w), seed, ptr(p), ptr(d), ptr(a), ptr(t)),
+          "swr_synth_workload")
+    return p, d, a, t
+
+
+class TraceReplay:
+    """Pipeline::replay (pipeline.cpp:299-323) on the device: a WarmStartCache configured as the
+    reference Pipeline configures its CacheManager (pipeline.cpp:66-82: IVF index with
+    derive_seed(seed, "IDX") and the rebuild interval, embedding seed derive_seed(seed, "SEGM"),
+    make_negative_embedding, the gater) plus the host Cache Manager policy, replayed by
+    swr_replay with `batch` lookups per device call."""
+
+    def __init__(self, dim: int = 512, capacity: int = 1024, seed: int = 1,
+                 policy: Policy = None, sel: SelectorConfig = None, theta=None, psi=None,
+                 beta: float = 1.0, centroids: int = 64, nprobe: int = 8,
+                 rebuild_interval: int = 1024, delta: float = 0.25, max_batch: int = 1024,
+                 device: int = 0):
+        from .synth import pyramid
+        self.dim, self.seed = dim, seed
+        self.policy = policy or Policy()
+        self.sel = sel or SelectorConfig()
+        R = len(pyramid(1.0, delta)[0])
+        self.cache = WarmStartCache(dim, rows_per_entry=R, max_entries=capacity,
+                                    latent_shape=None, max_batch=max_batch, device=device)
+        self.cache.ivf_configure(centroids, nprobe, rebuild_interval,
+                                 derive_seed(seed, 0x494458))
+        self.cache.set_negative(negative_embedding(dim))
+        th = np.zeros(14 * 11, np.float32) if theta is None else theta
+        ps = np.zeros(14 * 11, np.float32) if psi is None else psi
+        self.cache.set_gater(th, ps, beta)
+        self.cm = CacheManager(self.cache, capacity=capacity, pyramid_delta=delta,
+                               embedding_seed=derive_seed(seed, 0x5345474D))
+
+    def run(self, prompts, durations, arrivals, total_steps, batch: int = 64,
+            refinement: bool = True):
+        n = len(durations)
+        cfg = _lib.SwrConfig(self.seed, self.sel.c(), self.policy.c(), 0.95, 2.0, 0.02, 0.75,
+                             0.004, 0.47, 200, 200, int(refinement), batch)
+        out = np.zeros(n, OUTCOME_DTYPE)
+        st = _lib.SwrStats()
+        pr = np.ascontiguousarray(prompts, np.float32)
+        d = np.ascontiguousarray(durations, np.float64)
+        a = np.ascontiguousarray(arrivals, np.float64)
+        t = np.ascontiguousarray(total_steps, np.int32)
+        check(_lib.lib().swr_replay(self.cache._h, self.cm._h, C.byref(cfg), n, ptr(pr), ptr(d),
+                                    ptr(a), ptr(t), ptr(out), C.byref(st)), "swr_replay")
+        return out, {f: getattr(st, f) for f, _ in st._fields_}
+
+    def close(self):
+        self.cm = None
+        self.cache.close()

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "semwarm_b200.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = set(re.findall(r"\b(sw(?:cm|b)?_[a-z_0-9]+)\s*\(", src))
+    names = set(re.findall(r"\b(sw(?:cm|b|r)?_[a-z_0-9]+)\s*\(", src))
     return sorted(n for n in names if not n.endswith("_fn"))  # drop the callback typedef
 
 
