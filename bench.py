@@ -45,7 +45,9 @@ def parse():
     p.add_argument("--steps", type=int, default=300)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--entries", type=int, default=1_000_000, help="total cache entries")
+    p.add_argument("--entries", type=int, default=None,
+                   help="total cache entries (default: 1M at N=1 = config 3; 10M over N>1 ranks "
+                        "= config 4, entry-sharded)")
     p.add_argument("--delta", type=float, default=1.0, help="pyramid delta (1 -> 1 row/entry)")
     p.add_argument("--batch", type=int, default=1024)
     p.add_argument("--top-k", type=int, default=8)
@@ -57,6 +59,14 @@ def parse():
     p.add_argument("--no-vocoder", action="store_true",
                    help="skip the phase-vocoder (time_stretch) side measurement")
     p.add_argument("--profile-only", action="store_true", help="few steps, no extras (ncu)")
+    p.add_argument("--no-sweep", action="store_true",
+                   help="skip the cache-size sweep (1K..10M entries; 10M = config 4 at N=1)")
+    p.add_argument("--no-replay", action="store_true", help="skip the config-5 trace replay")
+    p.add_argument("--no-config1", action="store_true", help="skip the config-1 latency")
+    p.add_argument("--no-parity", action="store_true",
+                   help="skip checking a sample of the timed batch against the oracle")
+    p.add_argument("--sweep", default="1000,10000,100000,1000000,10000000",
+                   help="cache sizes of the sweep")
     p.add_argument("--no-overlap", action="store_true",
                    help="run align+noise on the planning stream (no cross-batch overlap)")
     p.add_argument("--ivf", default=None, metavar="C,NPROBE",
@@ -68,7 +78,10 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 script on ONE GPU (all ranks share cuda:0, "
                         "records all-gathered through host memory); never a bench number")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.entries is None:
+        a.entries = 10_000_000 if int(os.environ.get("WORLD_SIZE", "1")) > 1 else 1_000_000
+    return a
 
 
 def rows_per_entry(delta):
@@ -752,13 +765,56 @@ def main():
             t = sorted(a.elapsed_time(b) for a, b in ev)
             lat[f"B{bsz}"] = round(t[len(t) // 2], 4)
 
+    # ---- side measurements (one GPU): parity sample of the timed batch, cache-size sweep
+    # (10M = config 4 at N=1), config 4's per-GPU shard step, config 1 latency, config 5 replay
+    pk_burst, pk_sust, hbm, pk_src = peaks()
+    extras = {}
+    if world == 1 and rank == 0 and not args.profile_only:
+        import bench_extras as bx
+        if not args.no_parity and not ivf and R == 1:
+            try:
+                extras["parity_sample"] = bx.parity_sample(
+                    wc, qpool[last_i % n_pool].cpu().numpy(), req_np[last_i % n_pool], ch.copy(),
+                    neg, th, ps)
+            except Exception as e:  # pragma: no cover
+                extras["parity_sample"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_sweep:
+            sw = []
+            for n_s in [int(x) for x in args.sweep.split(",") if x]:
+                try:
+                    pt = bx.sweep_point(n_s, B, K, device=local, peak=pk_burst)
+                    if not args.no_cpu_baseline and n_s <= 100_000:
+                        pt["cpu_reference_requests_per_s"] = bx.cpu_reference_point(
+                            n_s, cpu_threads(), 4 if n_s <= 10_000 else 1)
+                        pt["cpu_reference_cores"] = cpu_threads()
+                    sw.append(pt)
+                except Exception as e:  # pragma: no cover
+                    sw.append({"entries": n_s, "error": f"{type(e).__name__}: {e}"})
+            extras["cache_size_sweep"] = sw
+            ten = [x for x in sw if x.get("entries") == 10_000_000 and "error" not in x]
+            try:
+                extras["config4"] = {"single_gpu_10M": ten[0] if ten else None,
+                                     "per_gpu_shard": bx.config4_shard(device=local)}
+            except Exception as e:  # pragma: no cover
+                extras["config4"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_config1:
+            try:
+                extras["config1"] = bx.config1_latency(device=local,
+                                                       cpu=not args.no_cpu_baseline)
+            except Exception as e:  # pragma: no cover
+                extras["config1"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_replay:
+            try:
+                extras["config5"] = bx.config5_replay(device=local, cpu=not args.no_cpu_baseline)
+            except Exception as e:  # pragma: no cover
+                extras["config5"] = {"error": f"{type(e).__name__}: {e}"}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
         return
 
     # ---- roofline of the dominant kernel (tcgen05 scoring), timed live on its stream
-    pk_burst, pk_sust, hbm, pk_src = peaks()
     default_workload = (args.entries == 1_000_000 and B == 1024 and K == 8 and R == 1
                         and not ivf and world == 1 and not sharded)
     sc_ms, sc_n = prof["score_tc"]
@@ -882,6 +938,7 @@ def main():
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "setup_s": round(setup_s, 1),
+        **extras,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

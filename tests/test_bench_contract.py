@@ -43,7 +43,8 @@ def test_ours_arm_json_contract():
     the pipelined e2e (H2D + D2H counted), the launch count and the clock sample."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--entries", "20000",
                           "--steps", "5", "--warmup", "3", "--no-vocoder", "--no-batcher",
-                          "--no-cpu-baseline", "--no-latency"],
+                          "--no-cpu-baseline", "--no-latency", "--no-sweep", "--no-replay",
+                          "--no-config1", "--no-parity"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [x for x in out.stdout.splitlines() if x.strip().startswith("{")]
