@@ -601,27 +601,37 @@ def main():
                              "ms_per_step": round(sync_ms, 4),
                              "path": "sw_warmstart_host (one blocking call per batch)"}}
 
-    # ---- align + noise timed alone on the same choices, both noise modes (device events)
+    # ---- align + noise timed alone, both noise modes (device events around each launch). Every
+    # rep writes a different output buffer (4 rotating, 4 x 134 MB) after a 512 MiB read that
+    # evicts L2 (clean lines, as the scoring kernel's arena stream leaves it), so the latent reads,
+    # eps reads and output writes all go to HBM.
     align_alone = {}
     if world == 1:
         eps_t = torch.randn((B, C_, T_, F_), dtype=torch.float32, device=dev)
+        outs_a = [out] + [torch.empty_like(out) for _ in range(3)]
+        flush_buf = torch.ones(1 << 27, dtype=torch.float32, device=dev)
+        sink = torch.empty((), dtype=torch.float32, device=dev)
         for mode, dptr in (("philox", None), ("eps", eps_t.data_ptr())):
-            def al():
+            def al(j):
                 _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[last_i % n_pool]
-                                             .data_ptr(), B, dptr, 1234, out.data_ptr(), T_, sp),
-                           "sw_align_noise")
-            for _ in range(3):
-                al()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 50
-            a0.record(stream)
-            for _ in range(reps):
-                al()
-            a1.record(stream)
+                                             .data_ptr(), B, dptr, 1234, outs_a[j % 4].data_ptr(),
+                                             T_, sp), "sw_align_noise")
+            for j in range(4):
+                al(j)
+            reps = 20
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps)]
+            for j in range(reps):
+                with torch.cuda.stream(stream):  # the launch stream: the flush must not overlap
+                    torch.sum(flush_buf, dim=0, out=sink)
+                evs[j][0].record(stream)
+                al(j)
+                evs[j][1].record(stream)
             torch.cuda.synchronize(dev)
-            align_alone[mode] = a0.elapsed_time(a1) / reps
-        del eps_t
+            align_alone[mode] = float(np.median([a.elapsed_time(b) for a, b in evs]))
+        del outs_a, flush_buf, eps_t
         # the reference's alignment (phase vocoder per latent channel) on the same choices
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         wc.set_align_mode("vocoder", 128, 32)
         _lib.check(L_.sw_align_noise(wc._h, choices.data_ptr(), reqs[last_i % n_pool]
                                      .data_ptr(), B, None, 1234, out.data_ptr(), T_, sp),
@@ -917,7 +927,9 @@ def main():
                            "alone_frac": {
                                "philox": round(al_bytes / (align_alone["philox"] / 1e3) / 1e9 / hbm, 4),
                                "eps": round(eps_bytes / (align_alone["eps"] / 1e3) / 1e9 / hbm, 4)}
-                           if align_alone else None},
+                           if align_alone else None,
+                           "alone_timing": "median of 20 launches, each after a 512 MiB read that "
+                                           "evicts L2, 4 rotating output buffers"},
         **({"ivf": {"centroids": ivf[0], "nprobe": ivf[1], "rebuild_s": round(rebuild_s, 3),
                     "rebuild": "GPU k-means++ + Lloyd over %d rows (fp64, bit-identical to "
                                "index.cpp:59-184)" % n_rows}} if ivf else {}),

@@ -48,6 +48,15 @@ static void dalloc(T** p, size_t n) {
     }
 }
 
+// (s0, s1) = ((float)sqrt(abar), (float)sqrt(1 - abar)) per schedule index, rounded exactly as the
+// restatement rounds them (IEEE double sqrt, then to float)
+static std::vector<float2> noise_coefficients(const std::vector<double>& abar) {
+    std::vector<float2> s(abar.size());
+    for (size_t i = 0; i < abar.size(); ++i)
+        s[i] = make_float2((float)std::sqrt(abar[i]), (float)std::sqrt(1.0 - abar[i]));
+    return s;
+}
+
 static void default_schedule(std::vector<double>& abar) {
     // scaled-linear DDPM betas 0.00085..0.012 over 1000 steps (the LDM/AudioLDM default)
     abar.assign(1001, 1.0);
@@ -83,7 +92,7 @@ static void free_ctx(Ctx& c) {
     }
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
                     c.slice_cnt, c.cta_topk, c.dbg, c.tsrc,
-                    c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.q_bf, c.q_norm, c.q_eps,
+                    c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.s01, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.ovf_state, c.ovf_ring, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
                     c.cent, c.row_list, c.prank, c.pmask, c.d_sorted_slot, c.d_rows_sorted,
@@ -203,9 +212,13 @@ static void create(Ctx& c, const sw_config& cfg, int device) {
     std::vector<double> ab;
     default_schedule(ab);
     dalloc(&c.abar, ab.size());
+    dalloc(&c.s01, ab.size());
     c.n_abar = (int)ab.size();
     SW_CUDA(cudaMemcpyAsync(c.abar, ab.data(), sizeof(double) * ab.size(), cudaMemcpyHostToDevice,
                             c.mstream));
+    c.h_s01 = noise_coefficients(ab);
+    SW_CUDA(cudaMemcpyAsync(c.s01, c.h_s01.data(), sizeof(float2) * ab.size(),
+                            cudaMemcpyHostToDevice, c.mstream));
     c.h_pinned_bytes = (size_t)c.Bmax * (sizeof(float) * c.D + sizeof(sw_request) + sizeof(sw_choice));
     SW_CUDA(cudaMallocHost(&c.h_pinned, c.h_pinned_bytes));
     SW_CUDA(cudaStreamSynchronize(c.mstream));
@@ -524,11 +537,16 @@ int sw_set_schedule(sw_ctx* ctx, const double* abar, int32_t n) {
         SW_CUDA(cudaSetDevice(c.device));
         if (n != c.n_abar) {
             cudaFree(c.abar);
+            cudaFree(c.s01);
             c.abar = nullptr;
+            c.s01 = nullptr;
             dalloc(&c.abar, (size_t)n);
+            dalloc(&c.s01, (size_t)n);
             c.n_abar = n;
         }
         mcopy(c, c.abar, abar, sizeof(double) * n, cudaMemcpyHostToDevice);
+        c.h_s01 = noise_coefficients(std::vector<double>(abar, abar + n));
+        mcopy(c, c.s01, c.h_s01.data(), sizeof(float2) * n, cudaMemcpyHostToDevice);
         return SW_OK;
     });
 }

@@ -125,6 +125,8 @@ struct Ctx {
     float* theta = nullptr;           // [14*11]
     float* psi = nullptr;
     double* abar = nullptr;
+    float2* s01 = nullptr;  // (sqrt(abar), sqrt(1 - abar)) as floats, per schedule index
+    std::vector<float2> h_s01;
     int n_abar = 0;
     double beta = 1.0;
     int fd = kFeatureDim;
