@@ -364,6 +364,39 @@ int sw_align_noise_owned(sw_ctx* ctx, const sw_choice* d_choices, const sw_reque
                          int32_t B, int32_t rank, const float* d_eps, uint64_t philox_seed,
                          float* d_out, int32_t t_out_max, void* stream);
 
+/* In-library sharding over the GPUs of one process (no torch): a group owns one context per
+ * shard and runs sw_local_topk -> all-gather -> sw_merge_select -> sw_align_noise_owned on every
+ * shard's stream. The all-gather is NCCL (ncclCommInitAll + ncclAllGather over NVLink, libnccl
+ * opened at run time) when every shard has its own device, or peer copies (cudaMemcpyPeerAsync)
+ * when shards share a device. Entries are placed by id mod n_shards (sw_group_insert) or
+ * directly through sw_group_shard. Replaces the N-way fan-out of IvfIndex::search
+ * (index.cpp:289-326) + plan_request (pipeline.cpp:91-202) of BASELINE config 4. */
+#define SW_GROUP_TRANSPORT_AUTO 0  /* NCCL if all devices differ (and N > 1), else COPY */
+#define SW_GROUP_TRANSPORT_NCCL 1
+#define SW_GROUP_TRANSPORT_COPY 2
+typedef struct sw_group sw_group;
+int sw_group_create(const sw_config* cfg, int32_t n_shards, const int32_t* devices,
+                    int32_t transport, sw_group** out);
+int sw_group_destroy(sw_group* g);
+int sw_group_info(sw_group* g, int32_t* n_shards, int32_t* transport);
+int sw_group_shard(sw_group* g, int32_t shard, sw_ctx** ctx);
+int32_t sw_group_owner(sw_group* g, uint64_t entry_id);
+int sw_group_insert(sw_group* g, uint64_t entry_id, int32_t n_rows, const float* rows,
+                    const sw_segment* segs, const float* latent, int32_t t_src);
+int sw_group_remove(sw_group* g, uint64_t entry_id);
+int sw_group_set_negative(sw_group* g, const float* neg);
+int sw_group_set_gater(sw_group* g, const float* theta, const float* psi, int32_t feature_dim,
+                       double beta);
+/* One batch from host prompts/requests: choices (identical on every shard) come back in
+ * h_choices; d_out[s] (optional, on shard s's device, B x C x t_out_max x F) receives the
+ * aligned + noised latents of the requests whose chosen entry shard s owns. Synchronous. */
+int sw_group_warmstart_host(sw_group* g, const float* h_queries, const sw_request* h_reqs,
+                            int32_t B, uint64_t seed, const sw_selector_config* sel,
+                            const sw_policy* pol, uint64_t philox_seed, sw_choice* h_choices,
+                            float* const* d_out, int32_t t_out_max);
+/* The choices shard `shard` computed in the last batch (the replicated merge, for checks). */
+int sw_group_shard_choices(sw_group* g, int32_t shard, int32_t B, sw_choice* h_choices);
+
 /* ---------------------------------------------------------------- component entry points
  * score_candidates + select (selector.cpp:24-85) on one explicit candidate set, evaluated by
  * the same device code the batched path uses. Outputs n x {s_pos,s_neg,a,b,q} and the pick. */

@@ -25,6 +25,10 @@ SW_FLAG_EXACT_ONLY = 0x1
 SW_FLAG_TC_ALWAYS = 0x2
 SW_FLAG_GROW = 0x4
 
+SW_GROUP_TRANSPORT_AUTO = 0
+SW_GROUP_TRANSPORT_NCCL = 1
+SW_GROUP_TRANSPORT_COPY = 2
+
 SW_CHOICE_AMBIGUOUS_DRAW = 0x1
 SW_CHOICE_NONFINITE_PHI = 0x2
 SW_CHOICE_INCOMPLETE = 0x4
@@ -171,6 +175,18 @@ def lib() -> C.CDLL:
         "sw_merge_select": ([vp, vp, vp, i32, vp, vp, i32, i32, u64,
                              C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy), vp, vp], C.c_int),
         "sw_align_noise_owned": ([vp, vp, vp, i32, i32, vp, u64, vp, i32, vp], C.c_int),
+        "sw_group_create": ([C.POINTER(SwConfig), i32, vp, i32, C.POINTER(vp)], C.c_int),
+        "sw_group_destroy": ([vp], C.c_int),
+        "sw_group_info": ([vp, vp, vp], C.c_int),
+        "sw_group_shard": ([vp, i32, C.POINTER(vp)], C.c_int),
+        "sw_group_owner": ([vp, u64], i32),
+        "sw_group_insert": ([vp, u64, i32, vp, vp, vp, i32], C.c_int),
+        "sw_group_remove": ([vp, u64], C.c_int),
+        "sw_group_set_negative": ([vp, vp], C.c_int),
+        "sw_group_set_gater": ([vp, vp, vp, i32, f64], C.c_int),
+        "sw_group_warmstart_host": ([vp, vp, vp, i32, u64, C.POINTER(SwSelectorConfig),
+                                     C.POINTER(SwPolicy), u64, vp, vp, i32], C.c_int),
+        "sw_group_shard_choices": ([vp, i32, i32, vp], C.c_int),
         "sw_score_select_host": ([vp, i32, vp, vp, vp, f64, C.POINTER(SwSelectorConfig), u64,
                                   vp, vp], C.c_int),
         "sw_gater_host": ([vp, vp, vp, vp, i32, i32, vp, vp], C.c_int),
@@ -243,7 +259,10 @@ EXPORTED = [
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host",
     "sw_warmstart_host_submit", "sw_warmstart_host_wait", "sw_warmstart_async", "sw_join",
     "sw_local_topk_async", "sw_async_stream",
-    "sw_local_topk", "sw_merge_select",
+    "sw_local_topk", "sw_merge_select", "sw_group_create", "sw_group_destroy", "sw_group_info",
+    "sw_group_shard", "sw_group_owner", "sw_group_insert", "sw_group_remove",
+    "sw_group_set_negative", "sw_group_set_gater", "sw_group_warmstart_host",
+    "sw_group_shard_choices",
     "sw_align_noise_owned", "sw_score_select_host", "sw_gater_host", "sw_last_launch_info",
     "sw_profile_enable", "sw_profile_reset", "sw_profile_read", "sw_debug_query_stats",
     "sw_overflow_stats", "sw_arena_capacity", "sw_arena_reserve", "sw_arena_row_count",

@@ -92,9 +92,22 @@ class WarmStartCache:
         self.latent_shape = tuple(latent_shape) if latent_shape else None
         self.max_batch = max_batch
 
+    @classmethod
+    def _borrow(cls, handle, dim: int, latent_shape, max_batch: int, device: int):
+        """A non-owning view of a context created elsewhere (a ShardGroup's shard)."""
+        self = cls.__new__(cls)
+        self._h = handle
+        self._owned = False
+        self.dim = dim
+        self.device = device
+        self.latent_shape = tuple(latent_shape) if latent_shape else None
+        self.max_batch = max_batch
+        return self
+
     def close(self):
         if getattr(self, "_h", None):
-            _lib.lib().sw_ctx_destroy(self._h)
+            if getattr(self, "_owned", True):
+                _lib.lib().sw_ctx_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -474,6 +487,111 @@ class CacheManager:
 
     def check_consistent(self):
         return bool(_lib.lib().swcm_check_consistent(self._h))
+
+
+class ShardGroup:
+    """Entry-sharded warm start inside one process (sw_group_*, csrc/host/group.cpp): one
+    context per shard, local exact top-k -> all-gather (NCCL across devices, peer copies when
+    shards share one) -> replicated merge + select -> owner-computes align + noise. The Python
+    face of the C++ caller's path; sharded.py is the multi-process (torch.distributed) one."""
+
+    def __init__(self, dim: int, n_shards: int, devices=None, transport: str = "auto",
+                 rows_per_entry: int = 7, max_entries: int = 1024, latent_shape=(8, 256, 16),
+                 max_batch: int = 1024, latent_slots: int = 0, fps: float = 25.0,
+                 exact_only: bool = False, tc_always: bool = False):
+        L = _lib.lib()
+        cfg = _lib.SwConfig()
+        cfg.dim = dim
+        cfg.rows_per_entry = rows_per_entry
+        cfg.max_entries = max_entries
+        cfg.latent_c, cfg.latent_t_max, cfg.latent_f = latent_shape if latent_shape else (0, 0, 0)
+        cfg.max_batch = max_batch
+        cfg.latent_slots = latent_slots
+        cfg.latent_fps = fps
+        cfg.flags = (_lib.SW_FLAG_EXACT_ONLY if exact_only else 0) | (
+            _lib.SW_FLAG_TC_ALWAYS if tc_always else 0)
+        devs = np.ascontiguousarray(devices if devices is not None else range(n_shards), np.int32)
+        tr = {"auto": _lib.SW_GROUP_TRANSPORT_AUTO, "nccl": _lib.SW_GROUP_TRANSPORT_NCCL,
+              "copy": _lib.SW_GROUP_TRANSPORT_COPY}[transport]
+        h = C.c_void_p()
+        check(L.sw_group_create(C.byref(cfg), n_shards, ptr(devs), tr, C.byref(h)),
+              "sw_group_create")
+        self._h = h
+        self.dim, self.n_shards, self.max_batch = dim, n_shards, max_batch
+        self.devices = [int(d) for d in devs]
+        self.latent_shape = tuple(latent_shape) if latent_shape else None
+        n, t = C.c_int32(), C.c_int32()
+        check(L.sw_group_info(h, C.byref(n), C.byref(t)), "sw_group_info")
+        self.transport = {1: "nccl", 2: "copy"}[t.value]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().sw_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard(self, s: int) -> WarmStartCache:
+        h = C.c_void_p()
+        check(_lib.lib().sw_group_shard(self._h, s, C.byref(h)), "sw_group_shard")
+        return WarmStartCache._borrow(h, self.dim, self.latent_shape, self.max_batch,
+                                      self.devices[s])
+
+    def owner(self, entry_id: int) -> int:
+        return int(_lib.lib().sw_group_owner(self._h, entry_id))
+
+    def set_negative(self, neg):
+        neg = np.ascontiguousarray(neg, np.float32)
+        check(_lib.lib().sw_group_set_negative(self._h, ptr(neg)), "sw_group_set_negative")
+
+    def set_gater(self, theta, psi, beta: float = 1.0):
+        theta = np.ascontiguousarray(theta, np.float32).reshape(-1)
+        psi = np.ascontiguousarray(psi, np.float32).reshape(-1)
+        check(_lib.lib().sw_group_set_gater(self._h, ptr(theta), ptr(psi), 11, beta),
+              "sw_group_set_gater")
+
+    def insert(self, entry_id: int, rows, levels, starts, lengths, latent=None):
+        rows = np.ascontiguousarray(rows, np.float32).reshape(-1, self.dim)
+        sg = segments(levels, starts, lengths)
+        lat = None if latent is None else np.ascontiguousarray(latent, np.float32)
+        t_src = 0 if lat is None else lat.shape[1]
+        check(_lib.lib().sw_group_insert(self._h, entry_id, rows.shape[0], ptr(rows), ptr(sg),
+                                         ptr(lat), t_src), "sw_group_insert")
+
+    def remove(self, entry_id: int) -> bool:
+        rc = _lib.lib().sw_group_remove(self._h, entry_id)
+        check(rc, "sw_group_remove")
+        return rc == _lib.SW_OK
+
+    def warmstart_host(self, queries, reqs, seed: int = 1, sel: SelectorConfig = None,
+                       policy: Policy = None, philox_seed: int = 0, outs=None,
+                       t_out_max: int = 256) -> np.ndarray:
+        """One batch from host arrays; outs: optional per-shard device tensors
+        (B x C x t_out_max x F on that shard's device) for the owned latents."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        r = np.ascontiguousarray(reqs)
+        B = q.shape[0]
+        sel = sel or SelectorConfig()
+        policy = policy or Policy()
+        ch = np.zeros(B, _lib.CHOICE_DTYPE)
+        arr = None
+        if outs is not None:
+            arr = (C.c_void_p * self.n_shards)(*[o.data_ptr() if o is not None else None
+                                                 for o in outs])
+        check(_lib.lib().sw_group_warmstart_host(self._h, ptr(q), ptr(r), B, seed,
+                                                 C.byref(sel.c()), C.byref(policy.c()),
+                                                 philox_seed, ptr(ch), arr, t_out_max),
+              "sw_group_warmstart_host")
+        return ch
+
+    def shard_choices(self, s: int, B: int) -> np.ndarray:
+        ch = np.zeros(B, _lib.CHOICE_DTYPE)
+        check(_lib.lib().sw_group_shard_choices(self._h, s, B, ptr(ch)), "sw_group_shard_choices")
+        return ch
 
 
 def read_swem(path: str) -> np.ndarray:
