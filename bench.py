@@ -63,6 +63,9 @@ def parse():
                    help="skip the cache-size sweep (1K..10M entries; 10M = config 4 at N=1)")
     p.add_argument("--no-replay", action="store_true", help="skip the config-5 trace replay")
     p.add_argument("--no-config1", action="store_true", help="skip the config-1 latency")
+    p.add_argument("--parity-max-entries", type=int, default=2_000_000,
+                   help="sharded runs: largest cache whose shards are gathered for the parity "
+                        "sample")
     p.add_argument("--no-parity", action="store_true",
                    help="skip checking a sample of the timed batch against the oracle")
     p.add_argument("--sweep", default="1000,10000,100000,1000000,10000000",
@@ -779,6 +782,26 @@ def main():
     # (10M = config 4 at N=1), config 4's per-GPU shard step, config 1 latency, config 5 replay
     pk_burst, pk_sust, hbm, pk_src = peaks()
     extras = {}
+    if world > 1 and not args.profile_only and not args.no_parity and not ivf and R == 1:
+        # sharded run: every rank exports its shard, rank 0 checks the merged choices of the
+        # timed batch against the oracle over the union (bounded: host copies of the shards)
+        import bench_extras as bx
+        if n_local * world <= args.parity_max_entries:
+            part = bx.export_arena(wc)
+            parts = [None] * world if rank == 0 else None
+            dist.gather_object(part, parts, dst=0)
+            if rank == 0:
+                arena = tuple(np.concatenate([p_[i] for p_ in parts]) for i in range(3))
+                try:
+                    extras["parity_sample"] = bx.parity_sample(
+                        wc, qpool[last_i % n_pool].cpu().numpy(), req_np[last_i % n_pool],
+                        ch.copy(), neg, th, ps, arena=arena)
+                    extras["parity_sample"]["shards"] = world
+                except Exception as e:  # pragma: no cover
+                    extras["parity_sample"] = {"error": f"{type(e).__name__}: {e}"}
+        elif rank == 0:
+            extras["parity_sample"] = {"skipped": f"{n_local * world} entries > "
+                                                  f"--parity-max-entries {args.parity_max_entries}"}
     if world == 1 and rank == 0 and not args.profile_only:
         import bench_extras as bx
         if not args.no_parity and not ivf and R == 1:

@@ -327,14 +327,12 @@ def config5_replay(n=2000, batch=64, device=0, cpu=True):
     return res
 
 
-def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=64, nthreads=None):
-    """Checks n_check requests of a timed batch against the C restatement (oracle) over the
-    arena exported from the device (sw_arena_export)."""
-    import oracle
+def export_arena(wc):
+    """The context's whole arena (ids, rows, segments) read back from the device
+    (sw_arena_export), one row per entry (delta = 1)."""
     from paper_2603_07865_b200 import _lib
     L_ = _lib.lib()
     n = wc.entry_count()
-    R = 1
     ids = np.zeros(n, np.uint64)
     nr = np.zeros(n, np.int32)
     rows = np.zeros((n, D), np.float32)
@@ -345,6 +343,18 @@ def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=64, nthreads=
         got = L_.sw_arena_export(wc._h, s0, m, ids[s0:].ctypes.data, nr[s0:].ctypes.data,
                                  rows[s0:].ctypes.data, segs[s0:].ctypes.data)
         assert got == m, got
+    return ids, rows, segs
+
+
+def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=64, nthreads=None,
+                  arena=None):
+    """Checks n_check requests of a timed batch against the C restatement (oracle) over the
+    arena exported from the device (sw_arena_export) — or over `arena` = (ids, rows, segs), the
+    union of every rank's exported shard in the sharded run."""
+    import oracle
+    R = 1
+    ids, rows, segs = arena if arena is not None else export_arena(wc)
+    n = len(ids)
     ar = oracle.Arena(ids, np.arange(n + 1, dtype=np.int64) * R, rows, segs["level"],
                       segs["start_s"], segs["length_s"])
     B = q.shape[0]

@@ -67,7 +67,8 @@ def test_ours_arm_json_contract():
 @pytest.mark.gpu
 def test_two_rank_sharded_bench_gloo_validation():
     """bench.py under torchrun with two ranks on one device (gloo host-staged gather — the
-    validation mode of the entry-sharded step): rank 0 prints one line for the sharded run."""
+    validation mode of the entry-sharded step): rank 0 prints one line for the sharded run, and
+    its parity sample checks the merged choices against the oracle over both shards."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29541",
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
@@ -80,3 +81,6 @@ def test_two_rank_sharded_bench_gloo_validation():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["parallelism"] == "entry-sharded x2"
+    # the merged choices of the timed batch equal the oracle over the union of both shards
+    ps = d["parity_sample"]
+    assert ps["shards"] == 2 and ps["match"], ps
