@@ -105,12 +105,12 @@ def sweep_point(n, B=1024, K=8, steps=20, warm=3, device=0, peak=None):
     wc.profile(False)
     ms = e0.elapsed_time(e1) / steps
     sc_ms, sc_n = wc.profile_read()["score_tc"]
-    tc = sc_n > 0  # caches under 4096 rows take the exact fp64 path (no tcgen05 pre-filter)
+    tc = sc_n > 0
     score_ms = sc_ms / sc_n if tc else None
     flops = 2.0 * B * n * D
     ch = wc.choices(ring[(steps - 1) % 2])
     res = {"entries": n, "requests_per_s": round(B / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
-           "scoring": "tcgen05 pre-filter + fp64 rescoring" if tc else "exact fp64 only (< 4096 rows)",
+           "scoring": "tcgen05 pre-filter + fp64 rescoring" if tc else "exact fp64 only",
            "score_ms": round(score_ms, 4) if tc else None,
            "score_tflops": round(flops / (score_ms / 1e3) / 1e12, 1) if tc else None,
            "score_frac_of_peak": round(flops / (score_ms / 1e3) / 1e12 / peak, 4) if tc and peak else None,

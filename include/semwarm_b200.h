@@ -35,7 +35,8 @@ extern "C" {
 
 /* sw_config.flags */
 #define SW_FLAG_EXACT_ONLY 0x1u   /* never use the tcgen05 pre-filter: fp64 brute force only */
-#define SW_FLAG_TC_ALWAYS 0x2u    /* use the tcgen05 pre-filter even for tiny caches (tests) */
+#define SW_FLAG_TC_ALWAYS 0x2u    /* tcgen05 pre-filter at any size (now the default; kept so
+                                     callers that set it keep compiling) */
 #define SW_FLAG_GROW 0x4u         /* inserts grow a full arena (capacity doubles) instead of
                                      failing — the unbounded IvfIndex the C++ adapter mirrors */
 
@@ -201,6 +202,10 @@ int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t re
                      uint64_t seed);
 /* IvfIndex::set_rebuild_interval (index.hpp:76; pipeline.cpp:81). */
 int sw_ivf_set_rebuild_interval(sw_ctx* ctx, uint64_t rebuild_interval);
+/* The configuration sw_ivf_configure installed (target centroids, nprobe, interval, seed);
+ * enabled = 0 for the exhaustive (parity) mode. */
+int sw_ivf_config(sw_ctx* ctx, int32_t* enabled, int32_t* centroids, int32_t* nprobe,
+                  uint64_t* rebuild_interval, uint64_t* seed);
 /* IvfIndex::build(vecs, C, seed, nprobe) with non-empty vecs (index.cpp:186-208) on a configured,
  * empty arena: bulk-inserts the entries (no mutation counting), then k-means over the rows in
  * the given order with the configured seed itself; C is reduced to the row count. */
@@ -269,6 +274,10 @@ int sw_swix_load(sw_ctx* ctx, const char* path);
 /* IvfIndex::save (index.cpp:347-369) of the context's index; rows inside a list in rebuild
  * order (id, level, start). */
 int sw_swix_save(sw_ctx* ctx, const char* path);
+/* BanditModel::load / save (gater.cpp:277-306, "SWMB"): the Skip Gater's theta / psi straight
+ * into (out of) the context's device-resident gater; beta is GaterConfig's (not in the file). */
+int sw_gater_load_swmb(sw_ctx* ctx, const char* path, double beta);
+int sw_gater_save_swmb(sw_ctx* ctx, const char* path);
 /* load_embeddings (core.cpp:201-220): reads a SWEM file into `out` (up to cap floats); returns
  * count * dim and the shape, or a negative status. */
 int64_t sw_swem_read(const char* path, float* out, int64_t cap_floats, int32_t* count,
@@ -493,6 +502,13 @@ int swcm_importance(const swcm_cache* cache, uint64_t entry_id, double now_h, do
 int swcm_size(const swcm_cache* cache);
 int swcm_ids(const swcm_cache* cache, uint64_t* out, int32_t cap);
 int swcm_check_consistent(const swcm_cache* cache);
+/* CacheManager::save_snapshot / load_snapshot (cache.cpp:211-295): manifest.jsonl + <id>.emb
+ * (SWEM) + <id>.clip (SWSC). Load replaces the ledger, re-creates the index with the context's
+ * IVF configuration and inserts every entry's stored segment rows in ascending id order straight
+ * into the device arena (the SimClip latent into its slot when slots are [1][T][1]); save reads
+ * the rows back from the arena. Files are interchangeable with the reference's. */
+int swcm_save_snapshot(const swcm_cache* cache, const char* dir);
+int swcm_load_snapshot(swcm_cache* cache, const char* dir);
 
 /* ---------------------------------------------------------------- trace replay (config 5)
  * WorkloadConfig (simgen.hpp:87-98). */

@@ -284,6 +284,26 @@ class Ref:
                                        f64p, f64p]
         L.ref_cache_entry_rows.restype = C.c_int
         L.ref_cache_entry_rows.argtypes = [C.c_void_p, C.c_uint64, f32p, C.c_int]
+        L.ref_cache_save_snapshot.restype = C.c_int
+        L.ref_cache_save_snapshot.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_cache_load_snapshot.restype = C.c_int
+        L.ref_cache_load_snapshot.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_cache_check_consistent.restype = C.c_int
+        L.ref_cache_check_consistent.argtypes = [C.c_void_p]
+        L.ref_cache_admit_clip.restype = C.c_int64
+        L.ref_cache_admit_clip.argtypes = [C.c_void_p, f32p, f32p, C.c_int, C.c_double,
+                                           C.c_double, C.c_double, f32p, C.c_int, C.c_int,
+                                           C.c_uint64, C.c_double]
+        L.ref_cache_entry_state.restype = C.c_int
+        L.ref_cache_entry_state.argtypes = [C.c_void_p, C.c_uint64, f64p, f64p, C.c_int]
+        L.ref_cache_clip.restype = C.c_int
+        L.ref_cache_clip.argtypes = [C.c_void_p, C.c_uint64, f32p, C.c_int,
+                                     C.POINTER(C.c_int), C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_double), f32p]
+        L.ref_bandit_save.restype = C.c_int
+        L.ref_bandit_save.argtypes = [C.c_char_p, f32p, f32p, C.c_int]
+        L.ref_bandit_load.restype = C.c_int
+        L.ref_bandit_load.argtypes = [C.c_char_p, f32p, f32p, C.c_int]
 
         L.ref_synth_workload.restype = C.c_int
         L.ref_synth_workload.argtypes = [C.c_int64, C.c_int, C.c_uint64, f32p, f64p, f64p, i32p]

@@ -586,6 +586,97 @@ int ref_cache_entry_rows(void* p, uint64_t id, float* rows, int cap) {
     return n;
 }
 
+// ---------------------------------------------------------------- snapshots (cache.cpp:211-295,
+// gater.cpp:277-306): the reference's own directory snapshot and model file, for the
+// interchange tests of the device-arena loaders
+int ref_cache_save_snapshot(void* p, const char* dir) {
+    try {
+        static_cast<RefCache*>(p)->cm->save_snapshot(dir);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return 0;
+}
+int ref_cache_load_snapshot(void* p, const char* dir) {
+    try {
+        static_cast<RefCache*>(p)->cm->load_snapshot(dir);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return 0;
+}
+int ref_cache_check_consistent(void* p) {
+    return static_cast<RefCache*>(p)->cm->check_consistent() ? 1 : 0;
+}
+// admit with a full SimClip payload (latent series, rate, seed, skip fraction)
+int64_t ref_cache_admit_clip(void* p, const float* emb, const float* prompt, int dim,
+                             double duration, double quality, double now_h, const float* latent,
+                             int n_latent, int rate, uint64_t seed, double skip) {
+    auto* r = static_cast<RefCache*>(p);
+    SimClip clip;
+    clip.duration_s = duration;
+    clip.embedding = vec(emb, dim);
+    clip.latent.assign(latent, latent + n_latent);
+    clip.latent_rate = rate;
+    clip.seed = seed;
+    clip.skip_fraction_used = skip;
+    auto id = r->cm->admit(std::move(clip), vec(prompt, dim), quality, now_h);
+    return id ? (int64_t)*id : -1;
+}
+// ledger state of one entry: importance, last_update_h, admitted_h, quality, duration_s,
+// attempts, reuse_count, then the recent skips (returns their count)
+int ref_cache_entry_state(void* p, uint64_t id, double* out, double* skips, int cap) {
+    const CacheEntry* e = static_cast<RefCache*>(p)->cm->find(id);
+    if (!e) return -1;
+    out[0] = e->importance;
+    out[1] = e->last_update_h;
+    out[2] = e->admitted_h;
+    out[3] = e->quality;
+    out[4] = e->duration_s;
+    out[5] = e->refinement_attempts;
+    out[6] = (double)e->reuse_count;
+    int n = 0;
+    for (double s : e->recent_skips) {
+        if (n < cap) skips[n] = s;
+        ++n;
+    }
+    return n;
+}
+int ref_cache_clip(void* p, uint64_t id, float* latent, int cap, int* rate, uint64_t* seed,
+                   double* skip, float* emb) {
+    const CacheEntry* e = static_cast<RefCache*>(p)->cm->find(id);
+    if (!e) return -1;
+    const int n = (int)e->clip.latent.size();
+    for (int i = 0; i < n && i < cap; ++i) latent[i] = e->clip.latent[i];
+    *rate = e->clip.latent_rate;
+    *seed = e->clip.seed;
+    *skip = e->clip.skip_fraction_used;
+    std::memcpy(emb, e->full_embedding.values.data(), sizeof(float) * e->full_embedding.values.size());
+    return n;
+}
+int ref_bandit_save(const char* path, const float* theta, const float* psi, int fd) {
+    BanditModel m = BanditModel::zeros((size_t)fd);
+    std::memcpy(m.theta.data(), theta, sizeof(float) * m.theta.size());
+    std::memcpy(m.psi.data(), psi, sizeof(float) * m.psi.size());
+    try {
+        m.save(path);
+    } catch (const std::exception&) {
+        return -1;
+    }
+    return 0;
+}
+int ref_bandit_load(const char* path, float* theta, float* psi, int cap) {
+    try {
+        BanditModel m = BanditModel::load(path);
+        if ((int)m.theta.size() > cap) return -2;
+        std::memcpy(theta, m.theta.data(), sizeof(float) * m.theta.size());
+        std::memcpy(psi, m.psi.data(), sizeof(float) * m.psi.size());
+        return (int)m.feature_dim;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // ---------------------------------------------------------------- simgen quality (simgen.cpp:12-17)
 double ref_expected_quality(double skip, double sigma) {
     QualityModel m;

@@ -175,6 +175,11 @@ def lib() -> C.CDLL:
         "sw_merge_select": ([vp, vp, vp, i32, vp, vp, i32, i32, u64,
                              C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy), vp, vp], C.c_int),
         "sw_align_noise_owned": ([vp, vp, vp, i32, i32, vp, u64, vp, i32, vp], C.c_int),
+        "sw_ivf_config": ([vp, vp, vp, vp, vp, vp], C.c_int),
+        "sw_gater_load_swmb": ([vp, C.c_char_p, f64], C.c_int),
+        "sw_gater_save_swmb": ([vp, C.c_char_p], C.c_int),
+        "swcm_save_snapshot": ([vp, C.c_char_p], C.c_int),
+        "swcm_load_snapshot": ([vp, C.c_char_p], C.c_int),
         "sw_group_create": ([C.POINTER(SwConfig), i32, vp, i32, C.POINTER(vp)], C.c_int),
         "sw_group_destroy": ([vp], C.c_int),
         "sw_group_info": ([vp, vp, vp], C.c_int),
@@ -259,6 +264,8 @@ EXPORTED = [
     "sw_align_noise", "sw_warmstart", "sw_warmstart_host",
     "sw_warmstart_host_submit", "sw_warmstart_host_wait", "sw_warmstart_async", "sw_join",
     "sw_local_topk_async", "sw_async_stream",
+    "sw_ivf_config", "sw_gater_load_swmb", "sw_gater_save_swmb", "swcm_save_snapshot",
+    "swcm_load_snapshot",
     "sw_local_topk", "sw_merge_select", "sw_group_create", "sw_group_destroy", "sw_group_info",
     "sw_group_shard", "sw_group_owner", "sw_group_insert", "sw_group_remove",
     "sw_group_set_negative", "sw_group_set_gater", "sw_group_warmstart_host",

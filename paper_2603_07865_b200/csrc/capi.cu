@@ -792,6 +792,21 @@ int sw_ivf_configure(sw_ctx* ctx, int32_t centroids, int32_t nprobe, uint64_t re
     });
 }
 
+int sw_ivf_config(sw_ctx* ctx, int32_t* enabled, int32_t* centroids, int32_t* nprobe,
+                  uint64_t* rebuild_interval, uint64_t* seed) {
+    return guarded([&] {
+        SW_REQUIRE(ctx, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        if (enabled) *enabled = c.ivf ? 1 : 0;
+        if (centroids) *centroids = c.ivf_target;
+        if (nprobe) *nprobe = c.ivf_nprobe;
+        if (rebuild_interval) *rebuild_interval = c.ivf_interval;
+        if (seed) *seed = c.ivf_seed;
+        return SW_OK;
+    });
+}
+
 int sw_ivf_set_rebuild_interval(sw_ctx* ctx, uint64_t interval) {
     return guarded([&] {  // IvfIndex::set_rebuild_interval (index.hpp:76)
         SW_REQUIRE(ctx && interval >= 1, "rebuild interval must be >= 1");
@@ -963,6 +978,31 @@ int sw_swix_save(sw_ctx* ctx, const char* path) {
         wait_readers(c);
         SW_CUDA(cudaSetDevice(c.device));
         swix_save(c, path);
+        return SW_OK;
+    });
+}
+
+int sw_gater_load_swmb(sw_ctx* ctx, const char* path, double beta) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && path, "null argument");
+        std::vector<float> theta, psi;
+        int fd = 0;
+        swmb_read(path, theta, psi, fd);
+        SW_REQUIRE(fd == kFeatureDim, "feature dim mismatch");  // gater.cpp:62
+        return sw_set_gater(ctx, theta.data(), psi.data(), fd, beta);
+    });
+}
+
+int sw_gater_save_swmb(sw_ctx* ctx, const char* path) {
+    return guarded([&] {
+        SW_REQUIRE(ctx && path, "null argument");
+        Ctx& c = ctx->c;
+        std::shared_lock lk(c.mu);
+        SW_CUDA(cudaSetDevice(c.device));
+        std::vector<float> theta((size_t)kNumArms * c.fd), psi((size_t)kNumArms * c.fd);
+        mcopy(c, theta.data(), c.theta, sizeof(float) * theta.size(), cudaMemcpyDeviceToHost);
+        mcopy(c, psi.data(), c.psi, sizeof(float) * psi.size(), cudaMemcpyDeviceToHost);
+        swmb_write(path, theta.data(), psi.data(), c.fd);
         return SW_OK;
     });
 }

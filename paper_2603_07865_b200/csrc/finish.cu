@@ -1018,8 +1018,11 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     int kernels = 0;
     const int64_t rows_hw = c.high_water * c.Rp;
     const bool exact_only = (c.cfg.flags & SW_FLAG_EXACT_ONLY) != 0;
-    const bool tc = c.tc_ok && !exact_only && c.high_water > 0 &&
-                    (rows_hw >= 4096 || (c.cfg.flags & SW_FLAG_TC_ALWAYS));
+    // the tcgen05 pre-filter wins at every cache size and batch measured (tools/exact_vs_tc.py:
+    // 256 rows B = 1 0.046 vs 0.052 ms; 1000 rows B = 1024 0.074 vs 0.652 ms), so the exact
+    // brute force only runs when asked for (SW_FLAG_EXACT_ONLY)
+    const bool tc = c.tc_ok && !exact_only && c.high_water > 0;
+    (void)rows_hw;
     if (!tc)
         SW_REQUIRE(c.high_water <= kCandCap,
                    "exact-only search is limited to 16384 slots; enable the tcgen05 path");

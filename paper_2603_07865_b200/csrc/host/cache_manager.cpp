@@ -45,9 +45,13 @@ int swcm_cache::refine(uint64_t id, HostRng& rng, swcm_regenerate_fn regen, void
         }
     }
     if (best_q <= e.quality) return SW_OK;
+    std::vector<swh::Seg> segs;
     const int rc = h->write_rows(true, e.id, best_emb, e.duration_s,
-                                 lat_cap && best_t > 0 ? best_lat.data() : nullptr, best_t);
+                                 lat_cap && best_t > 0 ? best_lat.data() : nullptr, best_t, &segs);
     if (rc < 0) return rc;  // the ledger keeps the quality the arena still holds
+    e.segs = std::move(segs);
+    e.clip_embedding = best_emb;  // e.clip = best_clip; full_embedding = clip.embedding
+    h->keep_clip_latent(e, lat_cap && best_t > 0 ? best_lat.data() : nullptr, best_t);
     e.quality = best_q;
     e.recent_skips.clear();
     *replaced = 1;
@@ -91,8 +95,10 @@ int swcm_admit(swcm_cache* h, const float* clip_embedding, double duration_s,
     e.last_update_h = now_h;
     e.admitted_h = now_h;
     const std::vector<float> full(clip_embedding, clip_embedding + h->dim);
-    int rc = h->write_rows(false, e.id, full, duration_s, latent, t_src);
+    int rc = h->write_rows(false, e.id, full, duration_s, latent, t_src, &e.segs);
     if (rc < 0) return rc;  // nothing stored: the id is not consumed
+    e.clip_embedding = full;
+    h->keep_clip_latent(e, latent, t_src);
     ++h->next_id;
     const uint64_t id = e.id;
     h->entries.emplace(id, std::move(e));

@@ -141,6 +141,15 @@ struct Entry {
     int refinement_attempts = 0;
     size_t reuse_count = 0;
     std::deque<double> recent_skips;
+    // what the directory snapshot (cache.cpp:211-295) carries beyond the policy ledger: the
+    // segments of the stored rows (the rows themselves live in the device arena), and the
+    // SimClip payload (simgen.hpp:13-20) — its embedding is the entry's full embedding
+    std::vector<Seg> segs;
+    std::vector<float> clip_embedding;
+    std::vector<float> clip_latent;
+    int latent_rate = 200;
+    uint64_t clip_seed = 0;
+    double clip_skip = 0.0;
 };
 
 }  // namespace swh
@@ -162,8 +171,9 @@ struct swcm_cache {
     }
 
     int write_rows(bool replace, uint64_t id, const std::vector<float>& full, double duration,
-                   const float* latent, int t_src) {
+                   const float* latent, int t_src, std::vector<Seg>* segs_out = nullptr) {
         const std::vector<Seg> segs = swh::pyramid_segments(duration, cfg.pyramid_delta);
+        if (segs_out) *segs_out = segs;
         std::vector<float> rows;
         std::vector<sw_segment> ss;
         for (const Seg& s : segs) {
@@ -175,6 +185,17 @@ struct swcm_cache {
                                           latent, t_src)
                        : sw_arena_insert(ctx, id, (int32_t)segs.size(), rows.data(), ss.data(),
                                          latent, t_src);
+    }
+
+    // A context whose latent slots are [1][T][1] stores the reference's 1-D SimClip latent
+    // (simgen.hpp:14) as is; the host copy is what a directory snapshot writes back.
+    bool latent_1d() const {
+        int32_t d = 0, lc = 0, lt = 0, lf = 0, mb = 0, dev = 0;
+        return sw_ctx_info(ctx, &d, &lc, &lt, &lf, &mb, &dev) == SW_OK && lc == 1 && lf == 1;
+    }
+    void keep_clip_latent(Entry& e, const float* latent, int t_src) const {
+        if (latent && t_src > 0 && latent_1d()) e.clip_latent.assign(latent, latent + t_src);
+        else e.clip_latent.clear();
     }
 
     int evict_if_full(double now_h, std::vector<uint64_t>& evicted) {  // cache.cpp:70-105

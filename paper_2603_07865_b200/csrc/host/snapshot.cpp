@@ -5,6 +5,9 @@
 //         f32 start_s, f32 length_s, D x f32 embedding}. Little endian (binio, core.cpp:287-330).
 //   SWEM  save_embeddings / load_embeddings (core.cpp:183-220): "SWEM", u32 count, u32 dim,
 //         count x dim f32.
+//   SWMB  BanditModel::save / load (gater.cpp:277-306): "SWMB", u32 feature_dim, u32 arms (14),
+//         arms x fd f32 theta, arms x fd f32 psi — read into / written from the context's
+//         device-resident Skip Gater parameters.
 //
 // A warm restart of a large cache is then one file read + one bulk arena insert, without the
 // host-side re-insert (and re-clustering) the reference's load path implies.
@@ -12,6 +15,8 @@
 #include <cstring>
 #include <fstream>
 #include <map>
+#include <string>
+#include <vector>
 
 #include "../sw_internal.cuh"
 
@@ -235,6 +240,38 @@ int64_t swem_read(const char* path, float* out, int64_t cap_floats, int32_t* cou
     const int64_t nf = (int64_t)n * d;
     if (out) std::memcpy(out, r.p, 4 * (size_t)std::min(nf, cap_floats));
     return nf;
+}
+
+// ---------------------------------------------------------------- SWMB
+void swmb_read(const char* path, std::vector<float>& theta, std::vector<float>& psi, int& fd) {
+    const std::string bytes = read_file(path);
+    Reader r{reinterpret_cast<const uint8_t*>(bytes.data()),
+             reinterpret_cast<const uint8_t*>(bytes.data()) + bytes.size()};
+    r.need(4);
+    if (std::memcmp(r.p, "SWMB", 4) != 0)
+        throw Error(SW_ERUNTIME, std::string("not a bandit model snapshot (bad magic): ") + path);
+    r.p += 4;
+    fd = (int)r.get<uint32_t>();
+    const uint32_t arms = r.get<uint32_t>();
+    if (arms != (uint32_t)kNumArms)  // gater.cpp:295-298
+        throw Error(SW_ERUNTIME, "model snapshot arm count " + std::to_string(arms) +
+                                     " does not match build (14)");
+    theta.resize((size_t)kNumArms * fd);
+    psi.resize((size_t)kNumArms * fd);
+    for (auto& v : theta) v = r.get<float>();
+    for (auto& v : psi) v = r.get<float>();
+}
+
+void swmb_write(const char* path, const float* theta, const float* psi, int fd) {
+    std::string out("SWMB");
+    put<uint32_t>(out, (uint32_t)fd);
+    put<uint32_t>(out, (uint32_t)kNumArms);
+    for (int i = 0; i < kNumArms * fd; ++i) put<float>(out, theta[i]);
+    for (int i = 0; i < kNumArms * fd; ++i) put<float>(out, psi[i]);
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) throw Error(SW_ERUNTIME, std::string("cannot write ") + path);
+    f.write(out.data(), (std::streamsize)out.size());
+    if (!f) throw Error(SW_ERUNTIME, std::string("short write to ") + path);
 }
 
 }  // namespace sw

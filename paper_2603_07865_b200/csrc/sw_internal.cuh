@@ -422,5 +422,7 @@ void swix_load(Ctx& c, const char* path, void (*insert)(Ctx&, int64_t, const uin
                                                         const sw_segment*));
 void swix_save(Ctx& c, const char* path);
 int64_t swem_read(const char* path, float* out, int64_t cap_floats, int32_t* count, int32_t* dim);
+void swmb_read(const char* path, std::vector<float>& theta, std::vector<float>& psi, int& fd);
+void swmb_write(const char* path, const float* theta, const float* psi, int fd);
 
 }  // namespace sw

@@ -226,6 +226,21 @@ class WarmStartCache:
         check(_lib.lib().sw_set_align_mode(self._h, m, window, hop), "sw_set_align_mode")
 
     # ------------------------------------------------------------------ snapshots
+    def load_swmb(self, path: str, beta: float = 1.0):
+        """BanditModel::load (gater.cpp:287-306) into the device-resident Skip Gater."""
+        check(_lib.lib().sw_gater_load_swmb(self._h, path.encode(), beta), "sw_gater_load_swmb")
+
+    def save_swmb(self, path: str):
+        check(_lib.lib().sw_gater_save_swmb(self._h, path.encode()), "sw_gater_save_swmb")
+
+    def ivf_config(self) -> dict:
+        en, c, npb = C.c_int32(), C.c_int32(), C.c_int32()
+        iv, sd = C.c_uint64(), C.c_uint64()
+        check(_lib.lib().sw_ivf_config(self._h, C.byref(en), C.byref(c), C.byref(npb),
+                                       C.byref(iv), C.byref(sd)), "sw_ivf_config")
+        return {"enabled": bool(en.value), "centroids": c.value, "nprobe": npb.value,
+                "rebuild_interval": iv.value, "seed": sd.value}
+
     def load_swix(self, path: str):
         """IvfIndex::load (index.cpp:371-406) into this (empty) cache's device arena."""
         check(_lib.lib().sw_swix_load(self._h, path.encode()), "sw_swix_load")
@@ -484,6 +499,14 @@ class CacheManager:
         buf = np.zeros(max(1, self.size()), np.uint64)
         n = _lib.lib().swcm_ids(self._h, ptr(buf), buf.shape[0])
         return buf[:n].tolist()
+
+    def save_snapshot(self, directory: str):
+        """CacheManager::save_snapshot (cache.cpp:211-243)."""
+        check(_lib.lib().swcm_save_snapshot(self._h, directory.encode()), "swcm_save_snapshot")
+
+    def load_snapshot(self, directory: str):
+        """CacheManager::load_snapshot (cache.cpp:245-295) straight into the device arena."""
+        check(_lib.lib().swcm_load_snapshot(self._h, directory.encode()), "swcm_load_snapshot")
 
     def check_consistent(self):
         return bool(_lib.lib().swcm_check_consistent(self._h))
