@@ -265,6 +265,12 @@ int swb_destroy(swb_batcher* b);
 int swb_submit(swb_batcher* b, const float* prompt, const sw_request* req, sw_choice* choice,
                float* latent);
 int swb_stats(swb_batcher* b, int64_t* batches, int64_t* requests);
+/* Native load generator (measurement): `clients` threads each submit `per_client` blocking
+ * requests drawn round-robin from the n prompts / requests (ids first_id, first_id + 1, ...);
+ * reports wall-clock requests/s, p50 / p99 latency and the mean device batch. */
+int swb_load_test(swb_batcher* b, const float* prompts, const sw_request* reqs, int32_t n,
+                  int32_t clients, int32_t per_client, uint64_t first_id, double* req_per_s,
+                  double* p50_ms, double* p99_ms, double* mean_batch);
 
 /* ---------------------------------------------------------------- snapshots
  * IvfIndex::load (index.cpp:371-406) straight into an EMPTY context's device arena: entries,

@@ -224,6 +224,7 @@ def lib() -> C.CDLL:
         "swb_create": ([vp, i32, i32, u64, C.POINTER(SwSelectorConfig), C.POINTER(SwPolicy), u64,
                         i32, i32, C.POINTER(vp)], C.c_int),
         "swb_destroy": ([vp], C.c_int),
+        "swb_load_test": ([vp, vp, vp, i32, i32, i32, u64, vp, vp, vp, vp], C.c_int),
         "swb_submit": ([vp, vp, vp, vp, vp], C.c_int),
         "swb_stats": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "sw_time_stretch": ([vp, vp, vp, i32, i32, vp, i32, i32, vp, i64, vp, vp, vp, vp],
@@ -282,6 +283,7 @@ EXPORTED = [
     "sw_ivf_rebuild", "sw_ivf_info", "sw_ivf_centroids", "sw_ivf_set_centroids",
     "sw_ivf_entry_lists", "sw_swix_load", "sw_swix_save", "sw_swem_read", "sw_time_stretch",
     "sw_ctx_info", "sw_set_align_mode", "swb_create", "swb_destroy", "swb_submit", "swb_stats",
+    "swb_load_test",
 ]
 STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
 

@@ -91,7 +91,7 @@ static void free_ctx(Ctx& c) {
         cudaStreamDestroy(c.async_st);
     }
     void* ptrs[] = {c.rows, c.rows_bf, c.sneg, c.segs, c.ids, c.nrows, c.valid, c.valid_bits,
-                    c.slice_cnt, c.cta_topk, c.dbg, c.tsrc,
+                    c.slice_cnt, c.cta_topk, c.dbg, c.tsrc, c.mscratch,
                     c.latent, c.norms, c.neg, c.theta, c.psi, c.abar, c.s01, c.q_bf, c.q_norm, c.q_eps,
                     c.thr, c.top1, c.cand_n, c.cand_slot, c.cand_score, c.cand_exact, c.cand_row,
                     c.cand_list, c.ovf_state, c.ovf_ring, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
@@ -346,13 +346,19 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
     }
     cudaStream_t st = c.mstream;
     const int64_t total_rows = h_off[n] - h_off[0];
-    int64_t *d_slot = nullptr, *d_off = nullptr, *d_latoff = nullptr;
-    int32_t *d_base = nullptr, *d_tsrc = nullptr;
+    // temporaries on the mutation scratch stack (no cudaMalloc / cudaFree per admit)
+    MScratch<int64_t> s_slot(c, (size_t)n);
+    MScratch<int32_t> s_base(c, (size_t)n);
+    int64_t *d_slot = s_slot.p, *d_off = nullptr, *d_latoff = nullptr;
+    int32_t *d_base = s_base.p, *d_tsrc = nullptr;
     uint64_t* d_ids = nullptr;
     float *d_rows = nullptr, *d_lat = nullptr;
     sw_segment* d_segs = nullptr;
-    dalloc(&d_slot, (size_t)n);
-    dalloc(&d_base, (size_t)n);
+    const bool host_src = !on_device;
+    MScratch<uint64_t> s_ids(c, host_src ? (size_t)n : 0);
+    MScratch<int64_t> s_off(c, host_src ? (size_t)n + 1 : 0);
+    MScratch<float> s_rows(c, host_src ? (size_t)std::max<int64_t>(1, h_off[n]) * c.D : 0);
+    MScratch<sw_segment> s_segs(c, host_src ? (size_t)std::max<int64_t>(1, h_off[n]) : 0);
     SW_CUDA(cudaMemcpyAsync(d_slot, pl.slot.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
     SW_CUDA(cudaMemcpyAsync(d_base, pl.base.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
     if (on_device) {
@@ -361,10 +367,10 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
         d_rows = const_cast<float*>(rows);
         d_segs = const_cast<sw_segment*>(segs);
     } else {
-        dalloc(&d_ids, (size_t)n);
-        dalloc(&d_off, (size_t)n + 1);
-        dalloc(&d_rows, (size_t)std::max<int64_t>(1, h_off[n]) * c.D);
-        dalloc(&d_segs, (size_t)std::max<int64_t>(1, h_off[n]));
+        d_ids = s_ids.p;
+        d_off = s_off.p;
+        d_rows = s_rows.p;
+        d_segs = s_segs.p;
         SW_CUDA(cudaMemcpyAsync(d_ids, ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
         SW_CUDA(cudaMemcpyAsync(d_off, row_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
         if (total_rows > 0) {
@@ -375,18 +381,24 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
         }
     }
     launch_insert_rows_full(c, n, d_slot, d_base, d_off, d_ids, d_rows, d_segs, st);
+    int64_t lat_tot = 0;
+    if (latents && c.latent && !on_device)
+        for (int64_t e = 0; e < n; ++e)
+            lat_tot = std::max<int64_t>(lat_tot, lat_off[e] + (int64_t)c.C * t_src[e] * c.F);
+    const bool host_lat = latents && c.latent && !on_device;
+    MScratch<float> s_lat(c, host_lat ? (size_t)std::max<int64_t>(lat_tot, 1) : 0);
+    MScratch<int64_t> s_latoff(c, host_lat ? (size_t)n : 0);
+    MScratch<int32_t> s_tsrc(c, host_lat ? (size_t)n : 0);
     if (latents && c.latent) {
         if (on_device) {
             d_lat = const_cast<float*>(latents);
             d_latoff = const_cast<int64_t*>(lat_off);
             d_tsrc = const_cast<int32_t*>(t_src);
         } else {
-            int64_t tot = 0;
-            for (int64_t e = 0; e < n; ++e)
-                tot = std::max<int64_t>(tot, lat_off[e] + (int64_t)c.C * t_src[e] * c.F);
-            dalloc(&d_lat, (size_t)std::max<int64_t>(tot, 1));
-            dalloc(&d_latoff, (size_t)n);
-            dalloc(&d_tsrc, (size_t)n);
+            const int64_t tot = lat_tot;
+            d_lat = s_lat.p;
+            d_latoff = s_latoff.p;
+            d_tsrc = s_tsrc.p;
             SW_CUDA(cudaMemcpyAsync(d_lat, latents, sizeof(float) * tot, cudaMemcpyHostToDevice, st));
             SW_CUDA(cudaMemcpyAsync(d_latoff, lat_off, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
             SW_CUDA(cudaMemcpyAsync(d_tsrc, t_src, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
@@ -398,19 +410,6 @@ static void do_insert(Ctx& c, int64_t n, const uint64_t* ids, const int64_t* row
         std::vector<int32_t> nr((size_t)n);
         for (int64_t e = 0; e < n; ++e) nr[(size_t)e] = (int32_t)(h_off[e + 1] - h_off[e]);
         ivf_on_insert(c, pl.slot, pl.base, nr);
-    }
-    cudaFree(d_slot);
-    cudaFree(d_base);
-    if (!on_device) {
-        cudaFree(d_ids);
-        cudaFree(d_off);
-        cudaFree(d_rows);
-        cudaFree(d_segs);
-        if (latents && c.latent) {
-            cudaFree(d_lat);
-            cudaFree(d_latoff);
-            cudaFree(d_tsrc);
-        }
     }
 }
 

@@ -17,6 +17,7 @@
 // SURVEY H5). tests/test_gpu_batcher.py checks concurrent submitters against one sw_plan.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
@@ -220,6 +221,56 @@ int swb_stats(swb_batcher* b, int64_t* batches, int64_t* requests) {
     std::lock_guard<std::mutex> lk(b->mu);
     if (batches) *batches = b->n_batches;
     if (requests) *requests = b->n_requests;
+    return SW_OK;
+}
+
+// Native load generator: `clients` threads (the reference's thread per connection) each submit
+// `per_client` blocking requests, prompt/request (t * per_client + j) mod n of the given pools,
+// with fresh request ids. Wall-clock throughput and per-request latency percentiles; the Python
+// driver's GIL is not in the loop.
+int swb_load_test(swb_batcher* b, const float* prompts, const sw_request* reqs, int32_t n,
+                  int32_t clients, int32_t per_client, uint64_t first_id, double* req_per_s,
+                  double* p50_ms, double* p99_ms, double* mean_batch) {
+    if (!b || !prompts || !reqs || n < 1 || clients < 1 || per_client < 1) return SW_EINVAL;
+    std::vector<std::vector<double>> lat((size_t)clients);
+    std::vector<int> rc((size_t)clients, SW_OK);
+    int64_t b0 = 0, r0 = 0, b1 = 0, r1 = 0;
+    swb_stats(b, &b0, &r0);
+    const auto t0 = std::chrono::steady_clock::now();
+    {
+        std::vector<std::thread> th;
+        th.reserve((size_t)clients);
+        for (int t = 0; t < clients; ++t)
+            th.emplace_back([&, t] {
+                sw_choice ch;
+                lat[t].reserve((size_t)per_client);
+                for (int j = 0; j < per_client; ++j) {
+                    const int64_t k = (int64_t)t * per_client + j;
+                    sw_request rq = reqs[k % n];
+                    rq.id = first_id + (uint64_t)k;
+                    const auto a = std::chrono::steady_clock::now();
+                    const int r = swb_submit(b, prompts + (k % n) * b->D, &rq, &ch, nullptr);
+                    const auto z = std::chrono::steady_clock::now();
+                    if (r != SW_OK) {
+                        rc[t] = r;
+                        return;
+                    }
+                    lat[t].push_back(std::chrono::duration<double, std::milli>(z - a).count());
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int r : rc)
+        if (r != SW_OK) return r;
+    swb_stats(b, &b1, &r1);
+    std::vector<double> all;
+    for (auto& v : lat) all.insert(all.end(), v.begin(), v.end());
+    std::sort(all.begin(), all.end());
+    if (req_per_s) *req_per_s = (double)all.size() / wall;
+    if (p50_ms) *p50_ms = all[all.size() / 2];
+    if (p99_ms) *p99_ms = all[std::min(all.size() - 1, (size_t)(all.size() * 0.99))];
+    if (mean_batch) *mean_batch = b1 > b0 ? (double)(r1 - r0) / (double)(b1 - b0) : 0.0;
     return SW_OK;
 }
 

@@ -421,7 +421,7 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
     const int D = c.D;
     cudaStream_t st = c.mstream;
     MtRng rng(seed);
-    DBuf<int64_t> d_perm((size_t)n);
+    MScratch<int64_t> d_perm(c, (size_t)n);
     mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice);
     std::vector<float> cent((size_t)cnum * D);
     auto crow = [&](int j) { return cent.data() + (size_t)j * D; };
@@ -429,8 +429,8 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
     // ---- k-means++ seeding with a running minimum distance (index.cpp:79-107)
     const uint64_t first = rng.uniform_int((uint64_t)n);
     fetch_row(c, perm[first], crow(0));
-    DBuf<double> d_d2((size_t)n);
-    DBuf<float> d_c((size_t)D);
+    MScratch<double> d_d2(c, (size_t)n);
+    MScratch<float> d_c(c, (size_t)D);
     std::vector<double> d2((size_t)n);
     const int TB = 256;
     const int nb = (int)((n + TB - 1) / TB);
@@ -466,10 +466,10 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
     }
 
     // ---- Lloyd iterations on the sphere (index.cpp:109-176)
-    DBuf<int32_t> d_assign((size_t)n);
-    DBuf<int32_t> d_mem((size_t)n);
-    DBuf<int64_t> d_moff((size_t)cnum + 1);
-    DBuf<double> d_sums((size_t)cnum * D);
+    MScratch<int32_t> d_assign(c, (size_t)n);
+    MScratch<int32_t> d_mem(c, (size_t)n);
+    MScratch<int64_t> d_moff(c, (size_t)cnum + 1);
+    MScratch<double> d_sums(c, (size_t)cnum * D);
     std::vector<int32_t> assign((size_t)n), mem((size_t)n);
     std::vector<int64_t> moff((size_t)cnum + 1);
     std::vector<double> sums((size_t)cnum * D);
@@ -505,8 +505,8 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
                 // re-seed with the point farthest from its (current) centroid (index.cpp:142-151)
                 upload_centroids(c, cent, cnum);
                 const int fb = (int)((n + 255) / 256);
-                DBuf<double> bv((size_t)fb);
-                DBuf<int64_t> bi((size_t)fb);
+                MScratch<double> bv(c, (size_t)fb);
+                MScratch<int64_t> bi(c, (size_t)fb);
                 k_farthest<<<fb, 256, 0, st>>>(c.rows, c.Df, D, d_perm.p, n, d_assign.p, c.cent,
                                                bv.p, bi.p);
                 SW_CUDA(cudaGetLastError());
@@ -552,8 +552,8 @@ void kmeans(Ctx& c, const std::vector<int64_t>& perm, int cnum, uint64_t seed) {
 
 void ivf_mark_tails(Ctx& c, const std::vector<int64_t>& slots, const std::vector<int32_t>& nr) {
     if (slots.empty()) return;
-    DBuf<int64_t> d_s(slots.size());
-    DBuf<int32_t> d_n(nr.size());
+    MScratch<int64_t> d_s(c, slots.size());
+    MScratch<int32_t> d_n(c, nr.size());
     mcopy(c, d_s.p, slots.data(), sizeof(int64_t) * slots.size(), cudaMemcpyHostToDevice);
     mcopy(c, d_n.p, nr.data(), sizeof(int32_t) * nr.size(), cudaMemcpyHostToDevice);
     const int64_t tot = (int64_t)slots.size() * c.Rp;
@@ -603,7 +603,7 @@ void ivf_rebuild(Ctx& c) {
     }
     const int cnum = (int)std::min<int64_t>((int64_t)perm.size(), std::max(c.ivf_target, 1));
     kmeans(c, perm, cnum, dev::derive_seed(c.ivf_seed, c.ivf_rebuilds, 0, 0));
-    DBuf<int64_t> d_perm(perm.size());
+    MScratch<int64_t> d_perm(c, perm.size());
     mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_perm.p, (int64_t)perm.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
@@ -623,7 +623,7 @@ void ivf_build_from(Ctx& c, const std::vector<int64_t>& perm) {
     }
     const int cnum = (int)std::min<int64_t>((int64_t)perm.size(), std::max(c.ivf_target, 1));
     kmeans(c, perm, cnum, c.ivf_seed);
-    DBuf<int64_t> d_perm(perm.size());
+    MScratch<int64_t> d_perm(c, perm.size());
     mcopy(c, d_perm.p, perm.data(), sizeof(int64_t) * perm.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_perm.p, (int64_t)perm.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
@@ -655,8 +655,8 @@ bool ivf_check_consistent(Ctx& c) {
         return true;
     }
     if (c.ivf_C == 0) return false;
-    DBuf<int64_t> d_rows(rows.size());
-    DBuf<int32_t> d_as(rows.size());
+    MScratch<int64_t> d_rows(c, rows.size());
+    MScratch<int32_t> d_as(c, rows.size());
     mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice);
     argmax_rows(c, d_rows.p, (int64_t)rows.size(), c.ivf_C, nullptr, d_as.p, c.mstream);
     SW_CUDA(cudaStreamSynchronize(c.mstream));
@@ -699,7 +699,7 @@ void ivf_on_insert(Ctx& c, const std::vector<int64_t>& slot, const std::vector<i
         for (size_t e = e0; e <= e1; ++e)
             for (int r = 0; r < nr[e]; ++r) rows.push_back(slot[e] * c.Rp + base[e] + r);
         if (!rows.empty()) {
-            DBuf<int64_t> d_rows(rows.size());
+            MScratch<int64_t> d_rows(c, rows.size());
             mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(),
                                cudaMemcpyHostToDevice);
             argmax_rows(c, d_rows.p, (int64_t)rows.size(), c.ivf_C, c.row_list, nullptr, c.mstream);
@@ -728,7 +728,7 @@ void ivf_set_centroids(Ctx& c, const float* h, int C) {
     for (auto& kv : c.slot_of)
         for (int r = 0; r < c.ivf_rows[(size_t)kv.second]; ++r) rows.push_back(kv.second * c.Rp + r);
     if (!rows.empty() && C > 0) {
-        DBuf<int64_t> d_rows(rows.size());
+        MScratch<int64_t> d_rows(c, rows.size());
         mcopy(c, d_rows.p, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice);
         argmax_rows(c, d_rows.p, (int64_t)rows.size(), C, c.row_list, nullptr, c.mstream);
         SW_CUDA(cudaStreamSynchronize(c.mstream));

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -162,6 +163,11 @@ struct Ctx {
     sw_choice* d_choice_stage = nullptr;
     void* h_pinned = nullptr;       // pinned host staging
     size_t h_pinned_bytes = 0;
+    // device temporaries of arena mutations (MScratch): a grow-once stack, stream-ordered on
+    // mstream, so a single-entry admit / evict allocates and frees nothing (cudaFree
+    // synchronises the whole device)
+    char* mscratch = nullptr;
+    size_t mscratch_cap = 0, mscratch_top = 0;
 
     // TMA descriptors (encoded once at creation; cover the full capacity)
     CUtensorMap tm_rows{};
@@ -288,6 +294,37 @@ inline void mcopy(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcpyKi
     SW_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, c.mstream));
     SW_CUDA(cudaStreamSynchronize(c.mstream));
 }
+// A typed device temporary for mutation code: carved from the context's scratch stack (LIFO
+// with the scoped objects), falling back to cudaMalloc when the stack is exhausted. All users
+// touch it on mstream only, so stream order makes the reuse of a popped region safe.
+template <typename T>
+struct MScratch {
+    Ctx& c;
+    T* p = nullptr;
+    size_t bytes = 0;
+    bool owned = false;
+    MScratch(Ctx& cc, size_t n) : c(cc) {
+        bytes = (sizeof(T) * std::max<size_t>(n, 1) + 255) & ~(size_t)255;
+        if (!c.mscratch) {
+            c.mscratch_cap = (size_t)32 << 20;
+            SW_CUDA(cudaMalloc((void**)&c.mscratch, c.mscratch_cap));
+        }
+        if (c.mscratch_top + bytes <= c.mscratch_cap) {
+            p = reinterpret_cast<T*>(c.mscratch + c.mscratch_top);
+            c.mscratch_top += bytes;
+        } else {
+            SW_CUDA(cudaMalloc((void**)&p, bytes));
+            owned = true;
+        }
+    }
+    ~MScratch() {
+        if (owned) cudaFree(p);
+        else c.mscratch_top -= bytes;
+    }
+    MScratch(const MScratch&) = delete;
+    MScratch& operator=(const MScratch&) = delete;
+};
+
 inline void mfill(Ctx& c, void* dst, int value, size_t bytes) {
     if (bytes == 0) return;
     SW_CUDA(cudaMemsetAsync(dst, value, bytes, c.mstream));

@@ -682,6 +682,17 @@ class Batcher:
               "swb_submit")
         return (ch[0], lat) if want_latent else ch[0]
 
+    def load_test(self, prompts, reqs, clients: int = 256, per_client: int = 64,
+                  first_id: int = 1 << 40) -> dict:
+        """swb_load_test: native client threads (no GIL), blocking submits, wall clock."""
+        q = np.ascontiguousarray(prompts, np.float32).reshape(-1, self.cache.dim)
+        r = np.ascontiguousarray(reqs)
+        out = [C.c_double() for _ in range(4)]
+        check(_lib.lib().swb_load_test(self._h, ptr(q), ptr(r), q.shape[0], clients, per_client,
+                                       first_id, *[C.byref(x) for x in out]), "swb_load_test")
+        return {"requests_per_s": out[0].value, "p50_ms": out[1].value, "p99_ms": out[2].value,
+                "mean_batch": out[3].value}
+
     def stats(self):
         b, r = C.c_int64(), C.c_int64()
         check(_lib.lib().swb_stats(self._h, C.byref(b), C.byref(r)), "swb_stats")
