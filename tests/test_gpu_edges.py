@@ -108,3 +108,32 @@ def test_cache_emptied_by_removals(orc, mode):
     wc.remove(int(c.ids[last]))
     hits, n = wc.search(q, 8)
     assert (n == 0).all()
+
+
+def test_ambiguous_draw_is_flagged(ref):
+    """A softmax draw whose cumulative weight lands on the target within the exp() ulp slack is
+    flagged SW_CHOICE_AMBIGUOUS_DRAW (H3): two candidates whose weight ratio is
+    constructed from the request's own draw u so that the first boundary equals u * total;
+    moving the second similarity by 1e-6 clears the flag, and the pick then equals the
+    reference's select."""
+    import math
+
+    from paper_2603_07865_b200 import _lib
+    from paper_2603_07865_b200.warmstart import SelectorConfig
+    wc = _wc(64, 1, 64)
+    sel = SelectorConfig(top_k=2, temperature=0.05, quality_threshold=0.0)
+    seed = next(s for s in range(1, 1000) if 0.55 < ref.lib.ref_rng_first_uniform(s) < 0.9)
+    u = ref.lib.ref_rng_first_uniform(seed)
+    s0 = 0.9
+    s1 = s0 + sel.temperature * math.log(1.0 / u - 1.0)  # w1 / w0 = (1 - u) / u
+    dur = np.array([5.0, 5.0])
+    neg = np.array([0.1, 0.1])
+    _, pick, flags = wc.score_select(np.array([s0, s1]), neg, dur, 5.0, sel, seed)
+    assert flags & _lib.SW_CHOICE_AMBIGUOUS_DRAW
+    assert pick in (0, 1)
+    for d in (1e-6, -1e-6):
+        _, pick, flags = wc.score_select(np.array([s0, s1 + d]), neg, dur, 5.0, sel, seed)
+        assert not flags & _lib.SW_CHOICE_AMBIGUOUS_DRAW
+        # the unambiguous draw agrees with the reference's select on the same inputs
+        exp_pick = 0 if u * (1.0 + math.exp((s1 + d - s0) / sel.temperature)) <= 1.0 else 1
+        assert pick == exp_pick
