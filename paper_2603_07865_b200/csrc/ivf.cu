@@ -280,19 +280,25 @@ __global__ void k_group_count(const uint8_t* __restrict__ prank, int C, int np,
     }
 }
 
-// work items: list j, query block b of its queries, tile chunk jj of its tiles
+// work items: list j, query block b of its queries, tile chunk jj of its tiles. pair: a list's
+// blocks come in pairs (the odd one padded with an empty block) and one item covers two blocks —
+// a CTA pair (cta_group::2, M = 256) — so the list's tiles stream from HBM once per 256 queries
+// instead of once per 128.
 __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
                              const int32_t* __restrict__ tile0, const int32_t* __restrict__ ntl,
-                             int tpc, int32_t* __restrict__ qbase, int4* __restrict__ items) {
+                             int tpc, int pair, int32_t* __restrict__ qbase,
+                             int4* __restrict__ items) {
     __shared__ int s_nb[kMaxCentroids], s_ni[kMaxCentroids];
     const int j = threadIdx.x;
     int nb = 0, ch = 0;
     if (j < C && qcnt[j] > 0 && ntl[j] > 0) {
         nb = (qcnt[j] + 127) / 128;
+        if (pair) nb += nb & 1;
         ch = (ntl[j] + tpc - 1) / tpc;
     }
+    const int bstep = pair ? 2 : 1;
     s_nb[j] = nb;
-    s_ni[j] = nb * ch;
+    s_ni[j] = nb / bstep * ch;
     __syncthreads();
     if (j == 0) {  // exclusive scans over <= 256 lists
         int a = 0, b = 0;
@@ -308,9 +314,9 @@ __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
     }
     __syncthreads();
     if (j < kMaxCentroids) qbase[j] = s_nb[j];
-    for (int b = 0; b < nb; ++b)
+    for (int b = 0; b < nb; b += bstep)
         for (int jj = 0; jj < ch; ++jj)
-            items[s_ni[j] + b * ch + jj] =
+            items[s_ni[j] + b / bstep * ch + jj] =
                 make_int4((s_nb[j] + b) * 128, tile0[j] + jj * tpc, min(tpc, ntl[j] - jj * tpc),
                           j | (jj << 8));
 }
@@ -789,7 +795,9 @@ static void build_sorted(Ctx& c) {
         SW_CUDA(cudaMalloc(&c.d_rows_sorted, sizeof(__nv_bfloat16) * c.grp_cap_rows * c.Dp));
         SW_CUDA(cudaMalloc(&c.d_sorted_vbits, sizeof(uint32_t) * (c.grp_cap_rows / 32 + 16)));
         SW_REQUIRE(encode_2d_map(&c.tm_sorted, c.d_rows_sorted, (uint64_t)c.Dp,
-                                 (uint64_t)c.grp_cap_rows, 256),
+                                 (uint64_t)c.grp_cap_rows, 256) &&
+                       encode_2d_map(&c.tm_sorted_half, c.d_rows_sorted, (uint64_t)c.Dp,
+                                     (uint64_t)c.grp_cap_rows, 128),
                    "grouped IVF: tensor map encode failed");
     }
     if (!c.d_list_tile0) {
@@ -833,7 +841,17 @@ int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st) {
     if (np >= c.ivf_C) return 0;
     if (c.grp_dirty || c.grp_C != c.ivf_C) build_sorted(c);
     if (c.grp_rows == 0) return 0;
-    const int64_t blocks = ((int64_t)B * np + 127) / 128 + c.ivf_C;
+    // SW_IVF_PAIR=1: items of two query blocks on CTA pairs. Measured (1M x 512, 64/8, B = 1024):
+    // DRAM per launch 1.35 -> 1.07 GB (each tile once per 256 queries) but slower, 0.285 ->
+    // 0.329 ms: the kernel is not HBM-bound at this size (tensor 39%, 4.6 TB/s), and a list with
+    // one query block occupies two SMs for one block's work. Off by default.
+    static const bool pair_ok = [] {
+        const char* e = getenv("SW_IVF_PAIR");
+        return e && e[0] == '1';
+    }();
+    c.grp_pair = pair_ok && c.num_sms >= 2;
+    // blocks of 128 gathered queries: every list rounds up (and to an even count with pairs)
+    const int64_t blocks = ((int64_t)B * np + 127) / 128 + (c.grp_pair ? 2 : 1) * c.ivf_C;
     const int64_t max_items = blocks * c.grp_ch;
     if (np * c.grp_ch > kMaxSlices) return 0;
     if (blocks * 128 > c.qg_cap) {
@@ -854,7 +872,8 @@ int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st) {
     SW_CUDA(cudaMemsetAsync(c.d_items, 0, sizeof(int4) * max_items, st));
     k_group_count<<<B, kMaxCentroids, 0, st>>>(c.prank, c.ivf_C, np, c.d_qcnt, c.d_qlist, c.Bmax);
     k_group_plan<<<1, kMaxCentroids, 0, st>>>(c.d_qcnt, c.ivf_C, c.d_list_tile0, c.d_list_ntiles,
-                                              c.grp_tpc, c.d_qbase, c.d_items);
+                                              c.grp_tpc, c.grp_pair ? 1 : 0, c.d_qbase,
+                                              c.d_items);
     k_group_gather<<<(unsigned)((blocks * 128 + 7) / 8), 256, 0, st>>>(
         c.d_qcnt, c.d_qlist, c.d_qbase, c.ivf_C, c.Bmax, c.q_bf, c.Dp, c.d_qg, c.d_qmap,
         blocks * 128);

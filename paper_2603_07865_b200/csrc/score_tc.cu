@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         Item r;
         if (p.items) {
             const int4 it = p.items[i];
-            r.qrow = it.x;
+            r.qrow = it.x + (PAIR ? (int)(blockIdx.x & 1) * BM : 0);  // pair: block b, b + 1
             r.t0 = it.y;
             r.ntiles = it.z;
             r.list = it.w & 255;
@@ -218,14 +218,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         return r;
     };
-    const int istep = p.items ? (int)gridDim.x : bal ? (PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x) : 1;
+    const int istep = (p.items || bal) ? (PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x) : 1;
     // does item i load A? (balanced mode: only when its query block differs from the unit's
     // previous item's)
     auto loads_a = [&](int i, int first) {
         return !bal || i == first || item_at(i).qrow != item_at(i - istep).qrow;
     };
     const int n_items = p.items ? *p.n_items : bal ? p.n_items_bal : 1;
-    const int item0 = p.items ? (int)blockIdx.x : bal ? unit : 0;
+    const int item0 = (p.items || bal) ? unit : 0;
     if (item0 >= n_items || item_at(item0).ntiles == 0) return;  // uniform for the CTA / pair
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
@@ -777,7 +777,9 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.kch = c.Dp / 64;
     const int budget = c.smem_optin - 1024 - 512;
     p.k = k;
-    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / B_STAGE);
+    const bool pair = c.grp_pair;
+    const int bstg = pair ? B_HALF : B_STAGE;
+    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / bstg);
     SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
     p.n_tiles = c.grp_rows / BN;
     p.tiles_per_cta = 1;
@@ -804,12 +806,33 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     SW_REQUIRE(p.n_chunks <= kMaxSlices, "grouped IVF: too many slices per query");
     p.cap_local = (kCandCap / p.n_chunks) & ~3;
     c.last_chunks = p.n_chunks;
-    c.last_score_pair = false;
+    c.last_score_pair = pair;
     c.last_score_ts = false;
     p.experiment = 0;
-    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * B_STAGE + 512;
+    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * bstg + 512;
     auto kern = [&](auto rp_tag, auto kl_tag) {
         constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
+        if (pair) {
+            // persistent CTA pairs (the two SMs of a TPC): each walks the items of two query
+            // blocks, staging half of every tile, so a tile streams once per 256 queries
+            auto kf = k_score_tc<RPv, KLv, true, false>;
+            ensure_smem_attr(c, kf, (size_t)c.smem_optin);
+            const int64_t units = std::min<int64_t>(max_items, c.num_sms / 2);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(2 * units), 1);
+            cfg.blockDim = dim3(THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            SW_CUDA(cudaLaunchKernelEx(&cfg, kf, c.tm_qg, c.tm_sorted_half, p));
+            return;
+        }
         auto kf = k_score_tc<RPv, KLv, false, false>;
         ensure_smem_attr(c, kf, (size_t)c.smem_optin);
         // persistent: one CTA per SM walks the items (max_items only bounds the grid)

@@ -219,6 +219,8 @@ struct Ctx {
     int4* d_items = nullptr;                 // [items_cap]
     int64_t items_cap = 0;
     CUtensorMap tm_sorted{};
+    CUtensorMap tm_sorted_half{};  // 128-row boxes: each CTA of a pair stages half a tile
+    bool grp_pair = false;         // grouped IVF items cover two query blocks (CTA pairs)
     CUtensorMap tm_qg{};
 
     // host bookkeeping (mirrors the reference's entry_vector_counts_, index.hpp:92)
