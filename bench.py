@@ -867,7 +867,11 @@ def main():
     flops = 2.0 * B * n_rows * D
     score_ms = sc_ms / max(1, sc_n)
     achieved = flops / (score_ms / 1000.0) / 1e12 if sc_n else None
+    # align + noise = the per-request geometry pre-pass + the streaming kernel, both counted
     al_ms, al_n = prof["align"]
+    if al_n and prof.get("align_geom", (0, 0))[1]:
+        g_ms, g_n = prof["align_geom"]
+        al_ms = al_ms + g_ms * al_n / g_n
     hits = ch["hit"].astype(bool)
     owned = hits & ((ch["owner"] == rank) if world > 1 else True)  # owner-computes align
     t_out = ch["t_out"][owned].astype(np.int64)
@@ -954,7 +958,10 @@ def main():
                          "alone_ms": round(score_alone_ms, 4),
                          "alone_frac": round(flops / (score_alone_ms / 1e3) / 1e12 / pk_burst, 4)}
                         if score_alone_ms else {})}),
-        "align_roofline": {"bound": "hbm", "achieved": round(al_gbs, 1) if al_gbs else None,
+        "align_roofline": {"bound": "hbm",
+                           "kernel": "k_align_geom + k_align_noise (per-request geometry, then "
+                                     "one 128-thread CTA per latent plane; both timed)",
+                           "achieved": round(al_gbs, 1) if al_gbs else None,
                            "peak": hbm, "unit": "GB/s",
                            "frac": round(al_gbs / hbm, 4) if al_gbs else None,
                            "bytes_per_launch": al_bytes,

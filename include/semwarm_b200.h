@@ -444,7 +444,8 @@ int sw_gater_host(sw_ctx* ctx, const float* prompts, const float* segs, const in
 #define SW_STAGE_SELECT 3    /* standalone select (multi-GPU merge path) */
 #define SW_STAGE_ALIGN 4     /* align + noise */
 #define SW_STAGE_MERGE 5     /* multi-GPU record merge */
-#define SW_NUM_STAGES 6
+#define SW_STAGE_ALIGN_GEOM 6 /* per-request align geometry (the pre-pass of align + noise) */
+#define SW_NUM_STAGES 7
 /* on: 0 off, 1 every stage, SW_PROFILE_MASK | (1 << stage) | ... only the listed stages */
 #define SW_PROFILE_MASK 0x100
 int sw_profile_enable(sw_ctx* ctx, int32_t on);

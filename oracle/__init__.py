@@ -94,6 +94,8 @@ class Oracle:
                                      C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_uint64,
                                      C.c_uint64, f32p]
         L.so_philox_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, f32p]
+        L.so_icdf_normals.argtypes = [np.ctypeslib.ndpointer(np.uint32, flags="C"), C.c_int64,
+                                      f32p]
         L.so_abar_table.argtypes = [f64p]
         L.so_abar_index.restype = C.c_int
         L.so_abar_index.argtypes = [C.c_int, C.c_int]
@@ -168,6 +170,12 @@ class Oracle:
     def philox_normals(self, seed, rid, n):
         out = np.zeros(n, np.float32)
         self.lib.so_philox_normals(seed, rid, n, out)
+        return out
+
+    def icdf_normals(self, words):
+        words = np.ascontiguousarray(words, np.uint32)
+        out = np.zeros(words.size, np.float32)
+        self.lib.so_icdf_normals(words, words.size, out)
         return out
 
     def abar_table(self):

@@ -2,6 +2,8 @@
  * warm-start path; built with -ffp-contract=off so no FMA changes a rounding. */
 #define _GNU_SOURCE
 #include "semwarm_oracle.h"
+/* the segment table of the noise definition (shared constants, not code) */
+#include "noise_table.h"
 
 #include <math.h>
 #include <pthread.h>
@@ -347,42 +349,22 @@ void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 static float as_f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 static uint32_t as_u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
-/* Box-Muller, our definition, every fp32 rounding spelled out
- * exactly as the device evaluates it (paper_2603_07865_b200/csrc/align.cu box_muller):
- * v = 2 - asfloat(0x3f800000 | a>>9) in (0,1]; ln v = e ln2 + ln(1+f) with
- * ln(1+f) = f - f^2/2 + f^3 q(f) (degree-6 minimax q); r = sqrt(-2 ln v);
- * theta = 2 pi (b>>8) 2^-24 split into the nearest quadrant and phi in [-pi/4, pi/4);
- * minimax sin (odd, deg 7) / cos (even, deg 8) of phi; (z0, z1) = (r cos, r sin). */
-static void box_muller(uint32_t a, uint32_t b, float* z0, float* z1) {
-    float v = 2.0f - as_f(0x3f800000u | (a >> 9));
-    uint32_t iv = as_u(v);
-    int e = ((int32_t)(iv - 0x3f3504f3u)) >> 23;
-    float f = as_f(iv - ((uint32_t)e << 23)) - 1.0f;
-    float f2 = f * f, f3 = f2 * f;
-    float q = 0x1.644d8ap-4f;
-    q = fmaf(q, f, -0x1.24291cp-3f);
-    q = fmaf(q, f, 0x1.317306p-3f);
-    q = fmaf(q, f, -0x1.53836p-3f);
-    q = fmaf(q, f, 0x1.98d828p-3f);
-    q = fmaf(q, f, -0x1.00037ep-2f);
-    q = fmaf(q, f, 0x1.5556d8p-2f);
-    float l1p = fmaf(f3, q, fmaf(f2, -0.5f, f));
-    float lnv = fmaf((float)e, 0x1.62e43p-1f, l1p);
-    float r = sqrtf(-2.0f * lnv);
-    uint32_t j = b >> 8;
-    uint32_t n = (j + (1u << 21)) >> 22;
-    float ph = (float)((int32_t)j - (int32_t)(n << 22)) * 0x1.921fb6p-22f;
-    float p2 = ph * ph;
-    float sp = fmaf(ph * p2, fmaf(p2, fmaf(p2, -0x1.994522p-13f, 0x1.11073ep-7f), -0x1.555546p-3f),
-                    ph);
-    float cp = fmaf(p2, fmaf(p2, fmaf(p2, fmaf(p2, 0x1.99177ap-16f, -0x1.6c07f6p-10f),
-                                      0x1.55553cp-5f), -0.5f), 1.0f);
-    /* quadrant n: swap on odd n; sin negative for n mod 4 in {2,3}, cos for {1,2} */
-    float sn = (n & 1u) ? cp : sp, cs = (n & 1u) ? sp : cp;
-    if (n & 2u) sn = -sn;
-    if ((n + 1u) & 2u) cs = -cs;
-    *z0 = r * cs;
-    *z1 = r * sn;
+/* The normal transform, our definition, every fp32 rounding spelled
+ * out exactly as the device evaluates it (paper_2603_07865_b200/csrc/align.cu icdf4): one normal
+ * per 32-bit Philox word w,
+ *   v = 2 - asfloat(0x3f800000 | (w & 0x7fffff))   in (0, 1], exact
+ *   s = (bits(v) >> 17) - 6656; |z| = fmaf(B[s], v, A[s]); z = |z| with w's sign bit,
+ * (A, B) the committed segment table (noise_table.h, generated by tools/gen_noise_table.py: the
+ * least-squares lines through sqrt(2) erfcinv(v - 2^-24), 64 per binade). */
+static float icdf_normal(uint32_t w) {
+    float v = 2.0f - as_f(0x3f800000u | (w & 0x7fffffu));
+    uint32_t s = (as_u(v) >> SW_NOISE_SHIFT) - SW_NOISE_BASE;
+    float za = fmaf(sw_noise_tab[s][1], v, sw_noise_tab[s][0]);
+    return as_f(as_u(za) ^ (w & 0x80000000u));
+}
+
+void so_icdf_normals(const uint32_t* words, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = icdf_normal(words[i]);
 }
 
 void so_philox_normals(uint64_t seed, uint64_t rid, int64_t n, float* out) {
@@ -394,8 +376,7 @@ void so_philox_normals(uint64_t seed, uint64_t rid, int64_t n, float* out) {
         uint32_t r[4];
         float z[4];
         so_philox4x32_10(ctr, key, r);
-        box_muller(r[0], r[1], &z[0], &z[1]);
-        box_muller(r[2], r[3], &z[2], &z[3]);
+        for (int t = 0; t < 4; ++t) z[t] = icdf_normal(r[t]);
         for (int t = 0; t < 4 && i + t < n; ++t) out[i + t] = z[t];
     }
 }

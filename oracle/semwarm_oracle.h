@@ -87,6 +87,8 @@ int so_plan_batch(const so_arena* ar, const float* neg, int B, const float* quer
 
 /* ---- our align + noise definition (no reference counterpart) ---- */
 void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* The normal transform of each 32-bit word. */
+void so_icdf_normals(const uint32_t* words, int64_t n, float* out);
 /* n standard normals for (seed, request_id), element i from philox counter (i/4, rid). */
 void so_philox_normals(uint64_t seed, uint64_t request_id, int64_t n, float* out);
 /* x_t[c][t][f] = fmaf(s1, eps, s0 * x0[c][lo + t mod T_seg][f]), t < T_out = llround(L*fps).

@@ -285,7 +285,7 @@ EXPORTED = [
     "sw_ctx_info", "sw_set_align_mode", "swb_create", "swb_destroy", "swb_submit", "swb_stats",
     "swb_load_test",
 ]
-STAGES = ["prep", "score_tc", "finish", "select", "align", "merge"]
+STAGES = ["prep", "score_tc", "finish", "select", "align", "merge", "align_geom"]
 
 
 def check(rc: int, what: str = "") -> int:

@@ -97,12 +97,13 @@ static void free_ctx(Ctx& c) {
                     c.cand_list, c.ovf_state, c.ovf_ring, c.hits, c.nhits, c.d_q_stage, c.d_req_stage, c.d_choice_stage,
                     c.cent, c.row_list, c.prank, c.pmask, c.d_sorted_slot, c.d_rows_sorted,
                     c.d_sorted_vbits, c.d_list_tile0, c.d_list_ntiles, c.d_qcnt, c.d_qlist,
-                    c.d_qbase, c.d_qg, c.d_qmap, c.d_items, c.d_voc};
+                    c.d_qbase, c.d_qg, c.d_qmap, c.d_items, c.d_voc, c.k4_state};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_pinned) cudaFreeHost(c.h_pinned);
     for (cudaEvent_t e : c.prof_ev) cudaEventDestroy(e);
     if (c.scratch_ev) cudaEventDestroy(c.scratch_ev);
+    if (c.k4_ev) cudaEventDestroy(c.k4_ev);
     for (int i = 0; i < Ctx::kPipe; ++i) {
         if (c.pipe_q[i]) cudaFree(c.pipe_q[i]);
         if (c.pipe_req[i]) cudaFree(c.pipe_req[i]);
@@ -1194,13 +1195,14 @@ static int warmstart_async_impl(Ctx& c, const float* d_q, const sw_request* d_re
     if (!c.last_user_async && c.scratch_ev) SW_CUDA(cudaStreamWaitEvent(S, c.scratch_ev, 0));
     set_par(c, par);
     const int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, S, c.async_st);
-    launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, c.async_st);
+    const int ka =
+        launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, c.async_st);
     SW_CUDA(cudaEventRecord(c.async_done[par], c.async_st));
     if (c.scratch_ev) SW_CUDA(cudaEventRecord(c.scratch_ev, c.async_st));  // for later sync users
     c.async_used[par] = true;
     c.async_par = par ^ 1;
     c.last_user_async = true;
-    return kn + 1;
+    return kn + ka;
 }
 
 int sw_plan(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t B, uint64_t seed,
@@ -1255,8 +1257,8 @@ int sw_warmstart(sw_ctx* ctx, const float* d_q, const sw_request* d_req, int32_t
         SW_CUDA(cudaSetDevice(c.device));
         cudaStream_t st = as_stream(stream);
         int kn = plan_impl(c, d_q, d_req, B, seed, sel, pol, d_ch, st);
-        launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, st);
-        c.last_kernels = kn + 1;
+        kn += launch_align_noise(c, d_ch, d_req, B, -1, d_eps, philox_seed, d_out, t_out_max, st);
+        c.last_kernels = kn;
         return SW_OK;
     });
 }
@@ -1385,12 +1387,12 @@ int sw_warmstart_host(sw_ctx* ctx, const float* q, const sw_request* reqs, int32
         SW_CUDA(cudaMemcpyAsync(c.d_req_stage, reqs, sizeof(sw_request) * (size_t)B,
                                 cudaMemcpyHostToDevice, st));
         int kn = plan_impl(c, c.d_q_stage, c.d_req_stage, B, seed, sel, pol, c.d_choice_stage, st);
-        launch_align_noise(c, c.d_choice_stage, c.d_req_stage, B, -1, nullptr, philox_seed, d_out,
-                           t_out_max, st);
+        kn += launch_align_noise(c, c.d_choice_stage, c.d_req_stage, B, -1, nullptr, philox_seed,
+                                 d_out, t_out_max, st);
         SW_CUDA(cudaMemcpyAsync(choices, c.d_choice_stage, sizeof(sw_choice) * (size_t)B,
                                 cudaMemcpyDeviceToHost, st));
         SW_CUDA(cudaStreamSynchronize(st));
-        c.last_kernels = kn + 1;
+        c.last_kernels = kn;
         return SW_OK;
     });
 }

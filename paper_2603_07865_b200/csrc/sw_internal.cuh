@@ -284,6 +284,12 @@ struct Ctx {
     // per device, so it cannot be a process-wide static)
     std::mutex attr_mu;
     std::map<const void*, size_t> smem_attr;
+    // K4 (align.cu): the per-request geometry written by the pre-pass; launches chained through
+    // k4_ev so two align launches on different streams never share it concurrently
+    std::mutex k4_mu;
+    char* k4_state = nullptr;
+    int k4_cap = 0;
+    cudaEvent_t k4_ev = nullptr;
 };
 
 // Host <-> device copies and fills outside the batched hot path: stream-ordered on the context's
@@ -417,7 +423,7 @@ void launch_select(Ctx& c, const HitRec* d_hits, const int32_t* d_nh, int ld, co
                    cudaStream_t st);
 void launch_merge(Ctx& c, const HitRec* d_gathered, const int32_t* d_gn, int world, int B,
                   int k, cudaStream_t st);
-void launch_align_noise(Ctx& c, const sw_choice* d_ch, const sw_request* d_req, int B,
+int launch_align_noise(Ctx& c, const sw_choice* d_ch, const sw_request* d_req, int B,
                         int rank, const float* d_eps, uint64_t seed, float* d_out, int t_out_max,
                         cudaStream_t st);
 void launch_score_select_one(Ctx& c, int n, const double* d_sims, const double* d_sneg,

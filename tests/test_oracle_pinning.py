@@ -187,30 +187,40 @@ def test_philox_known_answer(orc):
     assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
 
 
-def test_box_muller_definition_tracks_libm(orc):
-    """Our Box-Muller (polynomial ln / sin / cos) against the same
-    transform evaluated in float64 libm from the same Philox words: the definition is a
-    faithful Gaussian transform (|d| <= 2e-6 absolute, tails included)."""
-    import ctypes as C
-    seed, rid, nq = 0x1234ABCD5678, 77, 1 << 14
-    z = orc.philox_normals(seed, rid, 4 * nq)
-    key = (C.c_uint32 * 2)(seed & 0xFFFFFFFF, seed >> 32)
-    words = np.zeros((nq, 4), np.uint64)
-    out = (C.c_uint32 * 4)()
-    for i in range(nq):
-        orc.lib.so_philox4x32_10((C.c_uint32 * 4)(i, 0, rid, 0), key, out)
-        words[i] = list(out)
-    a = words[:, [0, 2]].reshape(-1)
-    b = words[:, [1, 3]].reshape(-1)
-    v = 2.0 - (1.0 + (a >> 9).astype(np.float64) * 2.0 ** -23)
-    r = np.sqrt(-2.0 * np.log(v))
-    th = 2 * np.pi * (b >> 8).astype(np.float64) * 2.0 ** -24
-    ref = np.stack([r * np.cos(th), r * np.sin(th)], 1).reshape(-1)
+def test_normal_transform_tracks_erfcinv(orc):
+    """Our normal transform (v from the word's low 23 bits, one fma from
+    the committed segment table, the word's sign bit) at EVERY one of the 2^23 magnitudes,
+    against its target sqrt(2) erfcinv(v - 2^-24) in float64: |d| <= 1e-5 everywhere, tails
+    included, and odd in the sign bit."""
+    from scipy.special import erfcinv
+    m = np.arange(1 << 23, dtype=np.uint32)
+    z = orc.icdf_normals(m)
+    v = 2.0 - (1.0 + m.astype(np.float64) * 2.0 ** -23)
+    ref = np.sqrt(2.0) * erfcinv(v - 2.0 ** -24)
     err = np.abs(z.astype(np.float64) - ref)
-    assert err.max() <= 2e-6, err.max()
-    # the tail: v = 2^-23 gives r = sqrt(46 ln 2) = 5.647
-    assert abs(z).max() <= 5.65
-    assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
+    assert err.max() <= 1e-5, err.max()
+    zn = orc.icdf_normals(m[::97] | np.uint32(0x80000000))
+    np.testing.assert_array_equal(zn, -z[::97])
+    # the high bits 23..30 do not enter; the largest magnitude is the 2^-23 cell's median
+    np.testing.assert_array_equal(orc.icdf_normals(m[:4096] | np.uint32(0x7F800000)), z[:4096])
+    assert 5.41 < z.max() < 5.43
+
+
+def test_noise_distribution(orc):
+    """Philox4x32-10 words through the transform are N(0, 1): moments and the Kolmogorov-Smirnov
+    distance over 4M draws of one request (KS 1%-critical value 1.63 / sqrt(n) = 8.2e-4)."""
+    from scipy.special import ndtr
+    n = 1 << 22
+    z = orc.philox_normals(0x5EED, 12345, n).astype(np.float64)
+    assert abs(z.mean()) < 5 / np.sqrt(n)
+    assert abs(z.var() - 1) < 5 * np.sqrt(2 / n)
+    assert abs((z ** 3).mean()) < 5 * np.sqrt(15 / n)
+    assert abs((z ** 4).mean() - 3) < 5 * np.sqrt(96 / n)
+    zs = np.sort(z)
+    cdf = ndtr(zs)
+    ks = max((np.arange(1, n + 1) / n - cdf).max(), (cdf - np.arange(n) / n).max())
+    assert ks < 8.2e-4, ks
+    assert np.abs(z).max() < 5.43
 
 
 def test_reference_ivf_harness(ref):
