@@ -299,9 +299,20 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
             // meanwhile: exclusive prefix of the slices' emission counts (capped at the slice
             // capacity; an overflowing slice flags the query) into shared memory
             int carry = 0;
-            for (int j0 = 0; j0 < p.n_chunks; j0 += 32) {
+            constexpr int kPre = (kMaxSlices + 31) / 32;
+            int raws[kPre];  // every count's load in flight at once (one L2 round trip)
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+                const int j = 32 * u + lane;
+                const int v = p.slice_cnt[(int64_t)b * p.n_chunks + min(j, p.n_chunks - 1)];
+                raws[u] = j < p.n_chunks ? v : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+                const int j0 = 32 * u;
+                if (j0 >= p.n_chunks) break;
                 const int j = j0 + lane;
-                const int raw = j < p.n_chunks ? p.slice_cnt[(int64_t)b * p.n_chunks + j] : 0;
+                const int raw = raws[u];
                 if (__any_sync(full, raw > p.cap_local) && lane == 0) S.ovf = 1;
                 const int c = min(raw, p.cap_local);
                 int incl = c;

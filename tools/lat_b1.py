@@ -70,7 +70,11 @@ def main():
     torch.cuda.synchronize(dev)
     wc.profile(False)
     prof = {k: round(v[0] / v[1] * 1e3, 2) for k, v in wc.profile_read().items() if v[1]}
-    print(json.dumps({"entries": args.entries, "B": B, "p50_ms": round(t[len(t) // 2], 4),
+    qs = wc.query_stats(B)
+    stats = {"emitted_mean": float(qs[:, 0].mean()), "kept_mean": float(qs[:, 1].mean()),
+             "finish_phase_kcycles_mean": [round(float(x) / 1e3, 2) for x in qs[:, 2:6].mean(0)],
+             "dbg6_7_kcycles": [round(float(x) / 1e3, 2) for x in qs[:, 6:8].mean(0)]}
+    print(json.dumps({"stats": stats, "entries": args.entries, "B": B, "p50_ms": round(t[len(t) // 2], 4),
                       "p99_ms": round(t[int(len(t) * 0.99)], 4), "stage_us": prof,
                       "launch": wc.launch_info()}))
 
