@@ -333,6 +333,6 @@ def test_align_noise_matches_restatement(orc, eps_mode):
                               float(L[b]), 25.0, ab, eps=ep, seed=777, rid=int(ids[b]))
         assert ref.shape[1] == t_out
         got = out[b, :, :t_out]
-        # bit-exact in both modes: eps input, and Philox + the fully specified fp32 Box-Muller
+        # bit-exact in both modes: eps input, and Philox + the fully specified table transform
         np.testing.assert_array_equal(got, ref)
         assert not out[b, :, t_out:].any()
