@@ -41,7 +41,8 @@ extern "C" {
                                      failing — the unbounded IvfIndex the C++ adapter mirrors */
 
 /* sw_choice.flags */
-#define SW_CHOICE_AMBIGUOUS_DRAW 0x1u  /* |acc - target| within exp() ulp slack (H3) */
+#define SW_CHOICE_AMBIGUOUS_DRAW 0x1u  /* never set: the device exp is glibc's, bit for bit, so
+                                          every softmax draw is the reference's */
 #define SW_CHOICE_NONFINITE_PHI 0x2u   /* non-finite features -> arm 0 (gater.cpp:71-76) */
 #define SW_CHOICE_INCOMPLETE 0x4u      /* search not certified (never set: overflowing queries
                                           are re-searched exactly, see sw_overflow_stats) */

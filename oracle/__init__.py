@@ -94,6 +94,9 @@ class Oracle:
                                      C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_uint64,
                                      C.c_uint64, f32p]
         L.so_philox_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, f32p]
+        L.so_ref_exp.restype = C.c_double
+        L.so_ref_exp.argtypes = [C.c_double]
+        L.so_exp_pair.argtypes = [f64p, C.c_int64, f64p, f64p]
         L.so_icdf_normals.argtypes = [np.ctypeslib.ndpointer(np.uint32, flags="C"), C.c_int64,
                                       f32p]
         L.so_abar_table.argtypes = [f64p]
@@ -171,6 +174,12 @@ class Oracle:
         out = np.zeros(n, np.float32)
         self.lib.so_philox_normals(seed, rid, n, out)
         return out
+
+    def exp_pair(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        ours, lib = np.zeros_like(x), np.zeros_like(x)
+        self.lib.so_exp_pair(x, x.size, ours, lib)
+        return ours, lib
 
     def icdf_normals(self, words):
         words = np.ascontiguousarray(words, np.uint32)

@@ -2,8 +2,10 @@
  * warm-start path; built with -ffp-contract=off so no FMA changes a rounding. */
 #define _GNU_SOURCE
 #include "semwarm_oracle.h"
-/* the segment table of the noise definition (shared constants, not code) */
+/* the segment table of the noise definition and glibc exp's 2^(k/128) table (shared
+ * constants, not code) */
 #include "noise_table.h"
+#include "exp_table.h"
 
 #include <math.h>
 #include <pthread.h>
@@ -325,6 +327,76 @@ int so_plan_batch(const so_arena* ar, const float* neg, int B, const float* quer
     if (nthreads > 1)
         for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
     return 0;
+}
+
+/* ------------------------------------------------------------ glibc exp, restated */
+/* The reference's std::exp is glibc 2.39's exp; on an x86-64 CPU with FMA + AVX2 its ifunc picks
+ * the FMA build of sysdeps/ieee754/dbl-64/e_exp.c (ARM optimized-routines, 128-entry table).
+ * This is that object code's operation sequence (objdump of libm.so.6, __exp_fma), every fma
+ * where the binary has one, so it is bit-identical to the library on every input; the device
+ * copy (csrc/select_dev.cuh ref_exp) repeats it with __fma_rn / __dmul_rn / __dadd_rn.
+ * tests/test_oracle_pinning.py checks this function against the libm exp. */
+static double u2d(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
+static uint64_t d2u(double d) { uint64_t u; memcpy(&u, &d, 8); return u; }
+
+double so_ref_exp(double x) {
+    const double InvLn2N = 0x1.71547652b82fep7, Shift = 0x1.8p52;
+    const double NegLn2hiN = -0x1.62e42fefa0000p-8, NegLn2loN = -0x1.cf79abc9e3b3ap-47;
+    const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+    const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    const uint64_t ix = d2u(x);
+    const uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ff;
+    int special = 0;
+    if (abstop - 0x3c9u > 0x3eu) {
+        if ((int32_t)(abstop - 0x3c9u) < 0) return x + 1.0;  /* |x| < 2^-54 */
+        if (abstop > 0x408u) {                                /* |x| >= 1024 */
+            if (ix == 0xfff0000000000000ull) return 0.0;
+            if (abstop == 0x7ffu) return x + 1.0;             /* inf or nan */
+            if (ix >> 63) return 0x1p-767 * 0x1p-767;        /* underflow: +0 */
+            return 0x1p769 * 0x1p769;                         /* overflow: inf */
+        }
+        special = 1;                                          /* large |x|: scale may overflow */
+    }
+    double kd = fma(x, InvLn2N, Shift);
+    const uint64_t ki = d2u(kd);
+    kd = kd - Shift;
+    double r = fma(kd, NegLn2hiN, x);
+    r = fma(kd, NegLn2loN, r);
+    const uint64_t idx = 2 * (ki & 127), top = ki << 45;
+    const double tail = u2d(sw_exp_tab[idx]);
+    uint64_t sbits = sw_exp_tab[idx + 1] + top;
+    const double r2 = r * r;
+    const double p1 = fma(r, C3, C2), p2 = fma(r, C5, C4);
+    double tmp = fma(p1, r2, r + tail);
+    tmp = fma(r2 * r2, p2, tmp);
+    if (special) {  /* specialcase() */
+        if ((ki & 0x80000000u) == 0) {
+            sbits -= 1009ull << 52;
+            const double scale = u2d(sbits);
+            return fma(scale, tmp, scale) * 0x1p1009;
+        }
+        sbits += 1022ull << 52;
+        const double scale = u2d(sbits);
+        const double st = tmp * scale;
+        double y = scale + st;
+        if (1.0 > y) {
+            const double hi = y + 1.0;
+            const double lo = (scale - y) + st;
+            y = (((1.0 - hi) + y) + lo + hi) - 1.0;
+            if (y == 0.0) y = 0.0;
+        }
+        return y * 0x1p-1022;
+    }
+    const double scale = u2d(sbits);
+    return fma(scale, tmp, scale);
+}
+
+/* ours and the library's exp over the same arguments (pinning test only) */
+void so_exp_pair(const double* x, int64_t n, double* ours, double* lib) {
+    for (int64_t i = 0; i < n; ++i) {
+        ours[i] = so_ref_exp(x[i]);
+        lib[i] = exp(x[i]);
+    }
 }
 
 /* ------------------------------------------------------------------ align + noise (ours) */

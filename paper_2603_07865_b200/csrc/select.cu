@@ -5,9 +5,11 @@
 // core.hpp:83), context_features (gater.cpp:13-30), choose_arm (gater.cpp:52-92, double x double
 // products WITHOUT fma), the rule / fixed policies (pipeline.cpp:180-202) and
 // t* = llround(0.05 * arm * T) (gater.hpp:16-19, simgen.cpp:70).
-// The only non-IEEE-exact step is exp() in the softmax (and log1p/exp in explore mode): CUDA's
-// double exp is within 1 ulp of glibc's, so a draw whose cumulative sum lands within that slack
-// of the target is flagged SW_CHOICE_AMBIGUOUS_DRAW instead of being silently trusted (H3).
+// The softmax's exp() is glibc's exp restated operation for operation (select_dev.cuh ref_exp),
+// so the weights and the cumulative draw are bit-identical to the reference's: no draw is ever
+// ambiguous (SW_CHOICE_AMBIGUOUS_DRAW is no longer set). The one remaining libm difference is
+// log1p in explore mode's softplus (CUDA's is within 1 ulp of glibc's): an explore-mode arm
+// tie within that slack is flagged SW_CHOICE_AMBIGUOUS_ARM.
 #include "select_dev.cuh"
 
 namespace sw {

@@ -1,8 +1,11 @@
 // Device-side restatement of score_candidates + select + context_features + choose_arm + t*,
 // shared by the per-request select kernel and the fused per-query finish kernel.
-// See select.cu for the parity notes (fp64 operation order, unfused products, exp() slack).
+// See select.cu for the parity notes (fp64 operation order, unfused products, glibc's exp).
 #pragma once
 #include "sw_internal.cuh"
+
+#define SW_EXP_QUAL static __device__ const
+#include "exp_table.h"
 
 namespace sw {
 namespace dev {
@@ -39,10 +42,66 @@ __device__ __forceinline__ uint64_t mt64_first(uint64_t seed) {
 }
 __device__ __forceinline__ double clamp01(double v) { return fmin(1.0, fmax(0.0, v)); }
 
+// The reference's std::exp = glibc 2.39's exp, whose ifunc picks the FMA build of
+// sysdeps/ieee754/dbl-64/e_exp.c on an FMA + AVX2 host: this is that object code's operation
+// sequence (every fma where the binary has one; table: exp_table.h, tools/gen_exp_table.py),
+// so the softmax weights — and with them the cumulative draw — are bit-identical to the
+// reference's. Restated in C as so_ref_exp (oracle), pinned there to the library bit for bit.
+__device__ __forceinline__ double ref_exp(double x) {
+    constexpr double InvLn2N = 0x1.71547652b82fep7, Shift = 0x1.8p52;
+    constexpr double NegLn2hiN = -0x1.62e42fefa0000p-8, NegLn2loN = -0x1.cf79abc9e3b3ap-47;
+    constexpr double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+    constexpr double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    const uint64_t ix = (uint64_t)__double_as_longlong(x);
+    const uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ffu;
+    bool special = false;
+    if (abstop - 0x3c9u > 0x3eu) {
+        if ((int32_t)(abstop - 0x3c9u) < 0) return __dadd_rn(x, 1.0);  // |x| < 2^-54
+        if (abstop > 0x408u) {                                          // |x| >= 1024
+            if (ix == 0xfff0000000000000ull) return 0.0;
+            if (abstop == 0x7ffu) return __dadd_rn(x, 1.0);             // inf or nan
+            return (ix >> 63) ? 0.0 : __longlong_as_double(0x7ff0000000000000ll);
+        }
+        special = true;  // large |x|: the scale may over/underflow
+    }
+    double kd = __fma_rn(x, InvLn2N, Shift);
+    const uint64_t ki = (uint64_t)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, Shift);
+    double r = __fma_rn(kd, NegLn2hiN, x);
+    r = __fma_rn(kd, NegLn2loN, r);
+    const uint64_t idx = 2 * (ki & 127), top = ki << 45;
+    const double tail = __longlong_as_double((long long)sw_exp_tab[idx]);
+    uint64_t sbits = sw_exp_tab[idx + 1] + top;
+    const double r2 = __dmul_rn(r, r);
+    const double p1 = __fma_rn(r, C3, C2), p2 = __fma_rn(r, C5, C4);
+    double tmp = __fma_rn(p1, r2, __dadd_rn(r, tail));
+    tmp = __fma_rn(__dmul_rn(r2, r2), p2, tmp);
+    if (special) {  // glibc's specialcase()
+        if ((ki & 0x80000000u) == 0) {
+            sbits -= 1009ull << 52;
+            const double scale = __longlong_as_double((long long)sbits);
+            return __dmul_rn(__fma_rn(scale, tmp, scale), 0x1p1009);
+        }
+        sbits += 1022ull << 52;
+        const double scale = __longlong_as_double((long long)sbits);
+        const double st = __dmul_rn(tmp, scale);
+        double y = __dadd_rn(scale, st);
+        if (1.0 > y) {
+            const double hi = __dadd_rn(y, 1.0);
+            const double lo = __dadd_rn(__dsub_rn(scale, y), st);
+            y = __dsub_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(1.0, hi), y), lo), hi), 1.0);
+            if (y == 0.0) y = 0.0;
+        }
+        return __dmul_rn(y, 0x1p-1022);
+    }
+    const double scale = __longlong_as_double((long long)sbits);
+    return __fma_rn(scale, tmp, scale);
+}
+
 __device__ __forceinline__ double softplus(double x) {  // gater.cpp:32-36
     if (x > 30.0) return x;
-    if (x < -30.0) return exp(x);
-    return log1p(exp(x));
+    if (x < -30.0) return ref_exp(x);
+    return log1p(ref_exp(x));  // CUDA log1p: within 1 ulp of glibc's (see choose_arm's flag)
 }
 
 struct GateOut {
@@ -99,16 +158,14 @@ __device__ __forceinline__ GateOut select_draw(int n, const double* s_pos, const
     for (int j = 0; j < ns; ++j) max_s = fmax(max_s, s_pos[surv[j]]);
     double w[kMaxTopK], total = 0.0;
     for (int j = 0; j < ns; ++j) {
-        w[j] = exp(__ddiv_rn(s_pos[surv[j]] - max_s, temp));
+        w[j] = ref_exp(__ddiv_rn(s_pos[surv[j]] - max_s, temp));
         total = __dadd_rn(total, w[j]);
     }
     const double target = __dmul_rn(u, total);
-    const double slack = 1e-13 * total;
     double acc = 0.0;
     g.pick = surv[ns - 1];
     for (int j = 0; j < ns; ++j) {
         acc = __dadd_rn(acc, w[j]);
-        if (fabs(acc - target) <= slack) g.flags |= SW_CHOICE_AMBIGUOUS_DRAW;
         if (acc >= target) {
             g.pick = surv[j];
             break;
@@ -265,21 +322,19 @@ __device__ __forceinline__ GateOut gate_select_warp(int n, double sim, double sn
     if (!surv) return g;  // no survivor: miss, and no RNG draw (selector.cpp:67)
     const bool me = (surv >> lane) & 1u;
     const double max_s = warp_max_d(me ? s_pos : -INFINITY);
-    const double w = me ? exp(__ddiv_rn(s_pos - max_s, temp)) : 0.0;
+    const double w = me ? ref_exp(__ddiv_rn(s_pos - max_s, temp)) : 0.0;
     double total = 0.0;
     for (int j = 0; j < 32; ++j) {
         const double wj = __shfl_sync(full, w, j);
         if ((surv >> j) & 1u) total = __dadd_rn(total, wj);
     }
     const double target = __dmul_rn(u, total);
-    const double slack = 1e-13 * total;
     double acc = 0.0;
     g.pick = 31 - __clz(surv);  // last survivor (selector.cpp:84)
     for (int j = 0; j < 32; ++j) {
         const double wj = __shfl_sync(full, w, j);
         if (!((surv >> j) & 1u)) continue;
         acc = __dadd_rn(acc, wj);
-        if (fabs(acc - target) <= slack) g.flags |= SW_CHOICE_AMBIGUOUS_DRAW;
         if (acc >= target) {
             g.pick = j;
             break;

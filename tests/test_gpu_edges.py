@@ -110,30 +110,48 @@ def test_cache_emptied_by_removals(orc, mode):
     assert (n == 0).all()
 
 
-def test_ambiguous_draw_is_flagged(ref):
-    """A softmax draw whose cumulative weight lands on the target within the exp() ulp slack is
-    flagged SW_CHOICE_AMBIGUOUS_DRAW (H3): two candidates whose weight ratio is
-    constructed from the request's own draw u so that the first boundary equals u * total;
-    moving the second similarity by 1e-6 clears the flag, and the pick then equals the
-    reference's select."""
+def test_boundary_draw_matches_reference(ref):
+    """A softmax draw whose cumulative weight lands ON the target: two
+    candidates whose weight ratio is constructed from the request's own draw u so that the
+    first boundary equals u * total, then moved by a few ulps / 1e-12 / 1e-6 either way. The
+    device's exp is glibc's restated bit for bit, so every pick equals the reference's select —
+    replayed here in Python (IEEE doubles; math.exp is the same glibc exp the compiled reference
+    calls) — and no draw is flagged SW_CHOICE_AMBIGUOUS_DRAW any more."""
     import math
 
     from paper_2603_07865_b200 import _lib
     from paper_2603_07865_b200.warmstart import SelectorConfig
     wc = _wc(64, 1, 64)
     sel = SelectorConfig(top_k=2, temperature=0.05, quality_threshold=0.0)
-    seed = next(s for s in range(1, 1000) if 0.55 < ref.lib.ref_rng_first_uniform(s) < 0.9)
-    u = ref.lib.ref_rng_first_uniform(seed)
-    s0 = 0.9
-    s1 = s0 + sel.temperature * math.log(1.0 / u - 1.0)  # w1 / w0 = (1 - u) / u
     dur = np.array([5.0, 5.0])
     neg = np.array([0.1, 0.1])
-    _, pick, flags = wc.score_select(np.array([s0, s1]), neg, dur, 5.0, sel, seed)
-    assert flags & _lib.SW_CHOICE_AMBIGUOUS_DRAW
-    assert pick in (0, 1)
-    for d in (1e-6, -1e-6):
-        _, pick, flags = wc.score_select(np.array([s0, s1 + d]), neg, dur, 5.0, sel, seed)
-        assert not flags & _lib.SW_CHOICE_AMBIGUOUS_DRAW
-        # the unambiguous draw agrees with the reference's select on the same inputs
-        exp_pick = 0 if u * (1.0 + math.exp((s1 + d - s0) / sel.temperature)) <= 1.0 else 1
-        assert pick == exp_pick
+
+    def ref_pick(s, u):  # score_candidates + select (selector.cpp:24-85), both survive
+        sp = [min(1.0, max(0.0, x)) for x in s]
+        mx = max(sp)
+        w = [math.exp((x - mx) / sel.temperature) for x in sp]
+        total = 0.0
+        for x in w:
+            total += x
+        target = u * total
+        acc = 0.0
+        for j, x in enumerate(w):
+            acc += x
+            if acc >= target:
+                return j
+        return len(w) - 1
+
+    n_boundary = 0
+    seeds = [s for s in range(1, 4000) if 0.3 < ref.lib.ref_rng_first_uniform(s) < 0.9][:40]
+    for seed in seeds:
+        u = ref.lib.ref_rng_first_uniform(seed)
+        s0 = 0.9
+        s1 = s0 + sel.temperature * math.log(1.0 / u - 1.0)  # w1 / w0 = (1 - u) / u
+        for d in (0.0, 1e-16, -1e-16, 2e-16, -2e-16, 1e-12, -1e-12, 1e-6, -1e-6):
+            sims = np.array([s0, s1 + d])
+            _, pick, flags = wc.score_select(sims, neg, dur, 5.0, sel, seed)
+            assert not flags & _lib.SW_CHOICE_AMBIGUOUS_DRAW
+            assert pick == ref_pick(list(sims), u), (seed, d)
+            w = [math.exp((x - max(sims)) / sel.temperature) for x in sims]
+            n_boundary += abs(w[0] - u * (w[0] + w[1])) <= 1e-13 * (w[0] + w[1])
+    assert n_boundary >= 40  # the constructed draws really sit on the boundary

@@ -1,6 +1,8 @@
 """CPU: pin the C restatement (oracle/semwarm_oracle.c) to the compiled reference and to the
 committed golden vectors, and check the reference's own known answers (SPEC examples).
 These tests are the reason the GPU parity tests may trust the restatement as their checker."""
+import os
+
 import numpy as np
 import pytest
 
@@ -242,3 +244,26 @@ def test_reference_ivf_harness(ref):
         a, b = ri.search(q, 8), ex.search(q, 8)
         np.testing.assert_array_equal(a[0], b[0])
         np.testing.assert_array_equal(a[4], b[4])
+
+
+def test_glibc_exp_restatement_is_bit_exact(orc):
+    """so_ref_exp (the oracle's restatement of glibc 2.39's FMA-build exp, which the device's
+    ref_exp repeats op for op) against the library's exp on 5M arguments: the softmax range,
+    the whole finite range, tiny arguments and the special cases (underflow to subnormals,
+    overflow, +-inf, nan). Needs the FMA + AVX2 ifunc the reference gets on the GPU box."""
+    import re
+    flags = open("/proc/cpuinfo").read() if os.path.exists("/proc/cpuinfo") else ""
+    if not (re.search(r"\bfma\b", flags) and re.search(r"\bavx2\b", flags)):
+        pytest.skip("libm's exp ifunc is not the FMA build on this CPU")
+    rng = np.random.default_rng(0)
+    s = rng.uniform(0, 1, (200000, 2))
+    t = rng.uniform(0.005, 1, 200000)
+    x = np.concatenate([
+        rng.uniform(-50, 0, 2_000_000), rng.uniform(-745.2, 709.8, 2_000_000),
+        rng.standard_normal(800_000) * 1e-3, (s[:, 0] - s.max(1)) / t,
+        np.array([0.0, -0.0, 1e-300, -1e-300, 2.0 ** -54, -2.0 ** -54, 2.0 ** -55, 709.78,
+                  709.79, 710, -708.39, -708.4, -745.13, -745.14, -746, 1024, -1024, np.inf,
+                  -np.inf, np.nan, 1.0, -1.0, 0.5])])
+    ours, lib = orc.exp_pair(x)
+    same = (ours.view(np.uint64) == lib.view(np.uint64)) | (np.isnan(ours) & np.isnan(lib))
+    assert same.all(), x[~same][:8]
