@@ -46,7 +46,8 @@ extern "C" {
 #define SW_CHOICE_NONFINITE_PHI 0x2u   /* non-finite features -> arm 0 (gater.cpp:71-76) */
 #define SW_CHOICE_INCOMPLETE 0x4u      /* search not certified (never set: overflowing queries
                                           are re-searched exactly, see sw_overflow_stats) */
-#define SW_CHOICE_AMBIGUOUS_ARM 0x8u   /* explore-mode softplus within ulp slack of a tie */
+#define SW_CHOICE_AMBIGUOUS_ARM 0x8u   /* never set: explore-mode softplus uses glibc's exp and
+                                          log1p restated bit for bit */
 
 typedef struct sw_ctx sw_ctx;
 

@@ -97,6 +97,7 @@ class Oracle:
         L.so_ref_exp.restype = C.c_double
         L.so_ref_exp.argtypes = [C.c_double]
         L.so_exp_pair.argtypes = [f64p, C.c_int64, f64p, f64p]
+        L.so_log1p_pair.argtypes = [f64p, C.c_int64, f64p, f64p]
         L.so_icdf_normals.argtypes = [np.ctypeslib.ndpointer(np.uint32, flags="C"), C.c_int64,
                                       f32p]
         L.so_abar_table.argtypes = [f64p]
@@ -179,6 +180,12 @@ class Oracle:
         x = np.ascontiguousarray(x, np.float64)
         ours, lib = np.zeros_like(x), np.zeros_like(x)
         self.lib.so_exp_pair(x, x.size, ours, lib)
+        return ours, lib
+
+    def log1p_pair(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        ours, lib = np.zeros_like(x), np.zeros_like(x)
+        self.lib.so_log1p_pair(x, x.size, ours, lib)
         return ours, lib
 
     def icdf_normals(self, words):

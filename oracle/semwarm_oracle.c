@@ -391,6 +391,97 @@ double so_ref_exp(double x) {
     return fma(scale, tmp, scale);
 }
 
+/* glibc 2.39 log1p, FMA build (x86-64 ifunc; fdlibm's s_log1p.c as compiled with FMA): the op
+ * sequence of its object code, like so_ref_exp. Used by explore-mode softplus (gater.cpp:32-36);
+ * the device copy is select_dev.cuh ref_log1p. */
+static double set_high(double u, uint32_t hi) {
+    return u2d(((uint64_t)hi << 32) | (d2u(u) & 0xffffffffull));
+}
+
+double so_ref_log1p(double x) {
+    const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2;
+    const double Lp3 = 0x1.2492494229359p-2, Lp4 = 0x1.c71c51d8e78afp-3;
+    const double Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3;
+    const double Lp7 = 0x1.2f112df3e5244p-3;
+    const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+    const int32_t hx = (int32_t)(d2u(x) >> 32);
+    int32_t k = 0;
+    uint32_t hu = 0;
+    double f, c = 0.0, u, hfsq;
+    if (hx <= 0x3fda8279) {                        /* x < 0.41422 */
+        const uint32_t ax = (uint32_t)hx & 0x7fffffffu;
+        if (ax > 0x3fefffffu) {                    /* x <= -1 */
+            if (x == -1.0) return -0x1p54 / 0.0;
+            return (x - x) / (x - x);
+        }
+        if (ax <= 0x3e1fffffu) {                   /* |x| < 2^-29 */
+            if (ax <= 0x3c8fffffu) return x;
+            return fma(x * x, -0.5, x);
+        }
+        if ((uint32_t)hx + 0x402d413cu > 0x402d413cu) {  /* k = 0: f = x */
+            f = x;
+            hfsq = (x * 0.5) * x;
+            goto poly;
+        }
+        goto upath;                                /* -1 < x <= -0.2929 */
+    }
+    if (hx > 0x7fefffff) return x + x;             /* inf, nan */
+    if (hx > 0x433fffff) {                         /* x >= 2^53: u = x, c = 0 */
+        k = (hx >> 20) - 0x3ff;
+        u = x;
+        hu = (uint32_t)hx;
+        goto norm;
+    }
+upath:
+    u = x + 1.0;
+    hu = (uint32_t)(d2u(u) >> 32);
+    k = (int32_t)(hu >> 20) - 0x3ff;
+    c = k > 0 ? (1.0 - (u - x)) / u : (x - (u - 1.0)) / u;  /* correction term */
+norm:
+    hu &= 0xfffffu;
+    if (hu > 0x6a09du) {
+        k += 1;
+        u = set_high(u, hu | 0x3fe00000u);
+        hu = (0x100000u - hu) >> 2;
+    } else {
+        u = set_high(u, hu | 0x3ff00000u);
+    }
+    f = u - 1.0;
+    hfsq = (f * 0.5) * f;
+    if (hu == 0) {                                 /* |f| < 2^-20 */
+        if (f == 0.0) {
+            if (k == 0) return 0.0;
+            const double dk = (double)k;
+            return fma(dk, ln2_hi, fma(dk, ln2_lo, c));
+        }
+        const double R = fma(-f, 0x1.5555555555555p-1, 1.0) * hfsq;
+        if (k == 0) return f - R;
+        const double dk = (double)k;
+        return fma(dk, ln2_hi, -((R - fma(dk, ln2_lo, c)) - f));
+    }
+poly:
+    {
+        const double s = f / (f + 2.0), z = s * s;
+        const double R2 = fma(z, Lp3, Lp2), R3 = fma(z, Lp5, Lp4), R4 = fma(z, Lp7, Lp6);
+        const double z2 = z * z, z4 = z2 * z2, z6 = z2 * z4;
+        double R = fma(z, Lp1, z2 * R2);
+        R = fma(z4, R3, R);
+        R = fma(z6, R4, R);
+        const double w = (R + hfsq) * s;
+        if (k == 0) return f - (hfsq - w);
+        const double dk = (double)k;
+        return fma(dk, ln2_hi, -((hfsq - (fma(dk, ln2_lo, c) + w)) - f));
+    }
+}
+
+/* ours and the library's log1p over the same arguments (pinning test only) */
+void so_log1p_pair(const double* x, int64_t n, double* ours, double* lib) {
+    for (int64_t i = 0; i < n; ++i) {
+        ours[i] = so_ref_log1p(x[i]);
+        lib[i] = log1p(x[i]);
+    }
+}
+
 /* ours and the library's exp over the same arguments (pinning test only) */
 void so_exp_pair(const double* x, int64_t n, double* ours, double* lib) {
     for (int64_t i = 0; i < n; ++i) {

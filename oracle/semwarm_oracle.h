@@ -90,6 +90,9 @@ void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 /* glibc 2.39 exp (FMA build), restated op for op (the reference's std::exp). */
 double so_ref_exp(double x);
 void so_exp_pair(const double* x, int64_t n, double* ours, double* lib);
+/* glibc 2.39 log1p (FMA build), restated op for op (explore-mode softplus). */
+double so_ref_log1p(double x);
+void so_log1p_pair(const double* x, int64_t n, double* ours, double* lib);
 /* The normal transform of each 32-bit word. */
 void so_icdf_normals(const uint32_t* words, int64_t n, float* out);
 /* n standard normals for (seed, request_id), element i from philox counter (i/4, rid). */

@@ -5,11 +5,10 @@
 // core.hpp:83), context_features (gater.cpp:13-30), choose_arm (gater.cpp:52-92, double x double
 // products WITHOUT fma), the rule / fixed policies (pipeline.cpp:180-202) and
 // t* = llround(0.05 * arm * T) (gater.hpp:16-19, simgen.cpp:70).
-// The softmax's exp() is glibc's exp restated operation for operation (select_dev.cuh ref_exp),
-// so the weights and the cumulative draw are bit-identical to the reference's: no draw is ever
-// ambiguous (SW_CHOICE_AMBIGUOUS_DRAW is no longer set). The one remaining libm difference is
-// log1p in explore mode's softplus (CUDA's is within 1 ulp of glibc's): an explore-mode arm
-// tie within that slack is flagged SW_CHOICE_AMBIGUOUS_ARM.
+// The libm calls on the path — exp in the softmax, exp / log1p in explore-mode softplus — are
+// glibc's, restated operation for operation (select_dev.cuh ref_exp / ref_log1p), so weights,
+// draws and arm scores are bit-identical to the reference's: SW_CHOICE_AMBIGUOUS_DRAW and
+// SW_CHOICE_AMBIGUOUS_ARM are no longer set.
 #include "select_dev.cuh"
 
 namespace sw {

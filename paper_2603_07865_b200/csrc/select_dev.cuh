@@ -98,10 +98,97 @@ __device__ __forceinline__ double ref_exp(double x) {
     return __fma_rn(scale, tmp, scale);
 }
 
+__device__ __forceinline__ double set_high(double u, uint32_t hi) {
+    return __longlong_as_double(
+        (long long)(((uint64_t)hi << 32) | ((uint64_t)__double_as_longlong(u) & 0xffffffffull)));
+}
+
+// glibc 2.39's log1p, FMA build (fdlibm's s_log1p.c as compiled with FMA; x86-64 ifunc): its
+// object code's operation sequence, like ref_exp (restated in C as so_ref_log1p, pinned to the
+// library bit for bit). Explore-mode softplus (gater.cpp:32-36) is therefore exact too.
+__device__ __forceinline__ double ref_log1p(double x) {
+    constexpr double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2;
+    constexpr double Lp3 = 0x1.2492494229359p-2, Lp4 = 0x1.c71c51d8e78afp-3;
+    constexpr double Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3;
+    constexpr double Lp7 = 0x1.2f112df3e5244p-3;
+    constexpr double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+    const int32_t hx = (int32_t)((uint64_t)__double_as_longlong(x) >> 32);
+    int32_t k = 0;
+    uint32_t hu = 0;
+    double f, c = 0.0, u = 0.0, hfsq;
+    bool upath = false;
+    if (hx <= 0x3fda8279) {  // x < 0.41422
+        const uint32_t ax = (uint32_t)hx & 0x7fffffffu;
+        if (ax > 0x3fefffffu) {  // x <= -1
+            if (x == -1.0) return -__longlong_as_double(0x7ff0000000000000ll);
+            return __longlong_as_double(0x7ff8000000000000ll);
+        }
+        if (ax <= 0x3e1fffffu) {  // |x| < 2^-29
+            if (ax <= 0x3c8fffffu) return x;
+            return __fma_rn(__dmul_rn(x, x), -0.5, x);
+        }
+        if ((uint32_t)hx + 0x402d413cu > 0x402d413cu) {  // k = 0: f = x
+            f = x;
+            hfsq = __dmul_rn(__dmul_rn(x, 0.5), x);
+        } else {
+            upath = true;  // -1 < x <= -0.2929
+        }
+    } else {
+        if (hx > 0x7fefffff) return __dadd_rn(x, x);  // inf, nan
+        if (hx > 0x433fffff) {                          // x >= 2^53: u = x, c = 0
+            k = (hx >> 20) - 0x3ff;
+            u = x;
+            hu = (uint32_t)hx;
+        } else {
+            upath = true;
+        }
+    }
+    if (k != 0 || upath) {
+        if (upath) {
+            u = __dadd_rn(x, 1.0);
+            hu = (uint32_t)((uint64_t)__double_as_longlong(u) >> 32);
+            k = (int32_t)(hu >> 20) - 0x3ff;
+            c = k > 0 ? __ddiv_rn(__dsub_rn(1.0, __dsub_rn(u, x)), u)
+                      : __ddiv_rn(__dsub_rn(x, __dsub_rn(u, 1.0)), u);  // correction term
+        }
+        hu &= 0xfffffu;
+        if (hu > 0x6a09du) {
+            k += 1;
+            u = set_high(u, hu | 0x3fe00000u);
+            hu = (0x100000u - hu) >> 2;
+        } else {
+            u = set_high(u, hu | 0x3ff00000u);
+        }
+        f = __dsub_rn(u, 1.0);
+        hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+        if (hu == 0) {  // |f| < 2^-20
+            const double dk = (double)k;
+            if (f == 0.0) {
+                if (k == 0) return 0.0;
+                return __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+            }
+            const double R = __dmul_rn(__fma_rn(-f, 0x1.5555555555555p-1, 1.0), hfsq);
+            if (k == 0) return __dsub_rn(f, R);
+            return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+        }
+    }
+    const double s = __ddiv_rn(f, __dadd_rn(f, 2.0)), z = __dmul_rn(s, s);
+    const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+    const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+    double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+    R = __fma_rn(z4, R3, R);
+    R = __fma_rn(z6, R4, R);
+    const double w = __dmul_rn(__dadd_rn(R, hfsq), s);
+    if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, w));
+    const double dk = (double)k;
+    return __fma_rn(dk, ln2_hi,
+                    -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(dk, ln2_lo, c), w)), f));
+}
+
 __device__ __forceinline__ double softplus(double x) {  // gater.cpp:32-36
     if (x > 30.0) return x;
     if (x < -30.0) return ref_exp(x);
-    return log1p(ref_exp(x));  // CUDA log1p: within 1 ulp of glibc's (see choose_arm's flag)
+    return ref_log1p(ref_exp(x));
 }
 
 struct GateOut {
@@ -201,20 +288,17 @@ __device__ __forceinline__ int choose_arm(const float* __restrict__ theta, const
             *flags |= SW_CHOICE_NONFINITE_PHI;
             return 0;
         }
+    // every score is the reference's bit for bit (exploit: IEEE products / sums; explore: plus
+    // glibc's exp / log1p restated), so the ">=" scan picks exactly the reference's arm
     int best = 0;
-    double best_score = -INFINITY, second = -INFINITY;
+    double best_score = -INFINITY;
     for (int a = 0; a < kNumArms; ++a) {
         const double s = arm_score(theta, psi, fd, beta, phi, a, explore);
         if (s >= best_score) {  // ties to the larger skip fraction
-            second = best_score;
             best_score = s;
             best = a;
-        } else if (s > second) {
-            second = s;
         }
     }
-    if (explore && fabs(best_score - second) <= 1e-13 * fmax(1.0, fabs(best_score)))
-        *flags |= SW_CHOICE_AMBIGUOUS_ARM;
     return best;
 }
 
@@ -410,11 +494,6 @@ __device__ __forceinline__ sw_choice select_warp(const HitRec* __restrict__ h, i
                     }
                 }
                 arm = ba;
-                if (explore) {
-                    double sec = lane == arm ? -INFINITY : s;
-                    for (int o = 16; o; o >>= 1) sec = fmax(sec, __shfl_xor_sync(0xffffffffu, sec, o));
-                    if (fabs(bs - sec) <= 1e-13 * fmax(1.0, fabs(bs))) flags |= SW_CHOICE_AMBIGUOUS_ARM;
-                }
             }
         } else if (p.policy == SW_POLICY_RULE) {
             arm = c.similarity >= p.rule_thr ? p.rule_arm : 0;

@@ -267,3 +267,25 @@ def test_glibc_exp_restatement_is_bit_exact(orc):
     ours, lib = orc.exp_pair(x)
     same = (ours.view(np.uint64) == lib.view(np.uint64)) | (np.isnan(ours) & np.isnan(lib))
     assert same.all(), x[~same][:8]
+
+
+def test_glibc_log1p_restatement_is_bit_exact(orc):
+    """so_ref_log1p (glibc 2.39's FMA-build log1p restated op for op; the device's ref_log1p
+    repeats it) against the library's log1p on 5M arguments: exp(u) for the softplus range
+    u in [-31, 31], all of (-1, 1), the finite range, and the branch boundaries."""
+    import re
+    flags = open("/proc/cpuinfo").read() if os.path.exists("/proc/cpuinfo") else ""
+    if not (re.search(r"\bfma\b", flags) and re.search(r"\bavx2\b", flags)):
+        pytest.skip("libm's log1p ifunc is not the FMA build on this CPU")
+    rng = np.random.default_rng(1)
+    x = np.concatenate([
+        np.exp(rng.uniform(-31, 31, 2_000_000)), rng.uniform(-1, 1, 1_000_000),
+        rng.uniform(-1, 0.5, 500_000), np.exp(rng.uniform(-745, 709, 1_000_000)),
+        -np.exp(rng.uniform(-745, 0, 500_000)),
+        np.array([0.0, -0.0, -1.0, -1.5, np.inf, -np.inf, np.nan, 2.0 ** -29, 2.0 ** -30,
+                  2.0 ** -54, 2.0 ** -55, 1e-300, 5e-324, -0.2928932188134524,
+                  -0.29289321881345254, 0.41421356237309503, 0.414213562373095, 2.0 ** 53,
+                  2.0 ** 53 * 1.5, 1e308])])
+    ours, lib = orc.log1p_pair(x)
+    same = (ours.view(np.uint64) == lib.view(np.uint64)) | (np.isnan(ours) & np.isnan(lib))
+    assert same.all(), x[~same][:8]
