@@ -146,6 +146,28 @@ __device__ __forceinline__ void emit_chunk(const uint32_t (&r)[32], uint32_t mas
     }
 }
 
+// Emission of one entry whose clamped best-row score m reaches theta (packed tiles), as
+// emit_chunk does it.
+template <int KL>
+__device__ __forceinline__ void emit_one(float m, int64_t slot, float& theta, float (&list)[KL],
+                                         float& kth, float eps2, int& cnt, int64_t slice,
+                                         const TcParams& p) {
+    if (cnt < p.cap_local) {
+        p.cand_slot[slice + cnt] = (int32_t)slot;
+        p.cand_score[slice + cnt] = m;
+    }
+    ++cnt;
+    float x = m;  // sorted insertion (descending)
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+        const float hi = fmaxf(list[i], x);
+        x = fminf(list[i], x);
+        list[i] = hi;
+    }
+    kth = list[KL - 1];
+    theta = fmaxf(theta, kth - eps2);
+}
+
 // PAIR: a 2-CTA cluster (the two CTAs of one TPC) runs the MMA as cta_group::2 with M = 256:
 // each CTA keeps its own 128 queries resident and stages HALF of every 256-row cache tile
 // (128 rows), so the per-SM L2 -> SM operand feed halves; the leader CTA issues the MMA for
@@ -162,12 +184,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_score_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmE,
                const TcParams p) {
     static_assert(!TS || PAIR, "TMEM-resident A is implemented for CTA pairs");
-    constexpr int TBN = TS ? BN_TS : BN;
+    // PACK (RP = R in {3, 7}, not a power of two): a tile is 32 entries x R rows with the arena's
+    // pad row skipped by a 3-D TMA box, so N = 32 R (224 at R = 7) carries no padding
+    constexpr bool PACK = (RP & (RP - 1)) != 0;
+    static_assert(!PACK || (!TS && RP <= 7), "packed tiles: R <= 7, no TS mode");
+    constexpr int TBN = TS ? BN_TS : (PACK ? 32 * RP : BN);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     constexpr int KPS = TS ? 2 : 1;  // 64-wide K chunks per ring stage (TS: 2 x 8 KB boxes)
-    constexpr int BSTG = TS ? KPS * B_QUARTER : (PAIR ? B_HALF : B_STAGE);
+    constexpr int BSTG = TS ? KPS * B_QUARTER : (PAIR ? (TBN / 2) * 128 : TBN * 128);
+    constexpr uint32_t ID_PAIR = ptx::idesc_bf16_f32(2 * BM, TBN);
+    constexpr uint32_t ID_ONE = ptx::idesc_bf16_f32(BM, TBN);
     uint8_t* sA = smem;
     uint8_t* sB = smem + (TS ? 0 : p.kch * A_CHUNK);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * BSTG);
@@ -307,14 +335,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (PAIR) {
                             if (leader) ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)(2 * BSTG));
     #pragma unroll
-                            for (int u = 0; u < KPS; ++u)
-                                ptx::tma_load_2d_pair(
-                                    ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
-                                    (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
+                            for (int u = 0; u < KPS; ++u) {
+                                if (PACK)  // 16 entries x R rows per CTA
+                                    ptx::tma_load_3d_pair(ptx::smem_u32(sB + s * BSTG), &tmE,
+                                                          bar(FULL + s), (kc + u) * 64, 0,
+                                                          (int32_t)(tile * 32 + rank * 16));
+                                else
+                                    ptx::tma_load_2d_pair(
+                                        ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
+                                        (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
+                            }
                         } else {
-                            ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)B_STAGE);
-                            ptx::tma_load_2d(ptx::smem_u32(sB + s * B_STAGE), &tmE, bar(FULL + s),
-                                             kc * 64, (int32_t)(tile * BN));
+                            ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)BSTG);
+                            if (PACK)
+                                ptx::tma_load_3d(ptx::smem_u32(sB + s * BSTG), &tmE, bar(FULL + s),
+                                                 kc * 64, 0, (int32_t)(tile * 32));
+                            else
+                                ptx::tma_load_2d(ptx::smem_u32(sB + s * BSTG), &tmE, bar(FULL + s),
+                                                 kc * 64, (int32_t)(tile * BN));
                         }
                     }
                 }
@@ -366,9 +404,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                                         d_tmem, tmem_base + 2 * TBN + (kc + u) * 32 + k * 8, bk,
                                         IDESC_TS, acc_in);
                                 else if (PAIR)
-                                    ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bk, IDESC_PAIR, acc_in);
+                                    ptx::mma_bf16_pair(d_tmem, ad + 2 * k, bk, ID_PAIR, acc_in);
                                 else
-                                    ptx::mma_bf16(d_tmem, ad + 2 * k, bk, IDESC, acc_in);
+                                    ptx::mma_bf16(d_tmem, ad + 2 * k, bk, ID_ONE, acc_in);
                             }
                             // frees the smem stage (both CTAs' halves) when the MMAs finish
                             if (PAIR)
@@ -401,8 +439,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
     } else {
         // ---------------- epilogue: TMEM lane == query
-        constexpr int E = 32 / RP;          // entries per 32-column chunk
-        constexpr int SPT = TBN / RP;       // slots per tile
+        constexpr int E = PACK ? 1 : 32 / RP;  // entries per 32-column chunk (unpacked tiles)
+        constexpr int SPT = TBN / RP;          // slots per tile (32 when packed)
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
         int gt = 0;  // tiles across items (accumulator index / phase, as the MMA counts them)
@@ -473,7 +511,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_wait_sleep(bar(TFULL + acc), aph);  // no spinning on the MMA's SMSPs
             ptx::tc_fence_after();
             constexpr int NSUB = (TS && E >= 2) ? 2 : 1;  // TS tiles have only 4 chunks
-            if (done == 0 && p.k <= NSUB * TBN / 32 && p.experiment == 0 && !p.ivf) {
+            if (!PACK && done == 0 && p.k <= NSUB * TBN / 32 && p.experiment == 0 && !p.ivf) {
                 // First tile of this slice: the threshold is still -inf, so a one-pass scan
                 // would emit the whole record sequence of the tile (~k + k ln(256/k)). A
                 // pre-pass takes each fully valid (sub-)chunk's best entry; the k-th largest of
@@ -569,13 +607,37 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // path before the next one (a partially valid warp, B % 32 != 0, hangs otherwise)
                 __syncwarp();
             };
-            if (p.experiment != 1 && p.experiment != 2) {
+            if (PACK && p.experiment != 1 && p.experiment != 2) {
+                // packed tile: entry e's R rows are columns [R e, R e + R); one x8 load per entry
+                // (8 in flight), its max over R columns, one compare
+                const uint32_t tb = lane_base + acc * TBN;
+                const uint32_t vb = __ldg(p.valid_bits + tile);  // 32 entries = one word
+#pragma unroll 1
+                for (int g = 0; g < 32; g += 8) {
+                    uint32_t r[8][8];
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) ptx::tmem_ld8(tb + RP * (g + u), r[u]);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        float m = __uint_as_float(r[u][0]);
+#pragma unroll
+                        for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[u][j]));
+                        m = fminf(1.0f, fmaxf(-1.0f, m));
+                        if (qvalid && ((vb >> (g + u)) & 1u) && m >= theta)
+                            emit_one<KL>(m, slot0 + g + u, theta, list, kth, eps2, cnt, slice, p);
+                    }
+                }
+                __syncwarp();
+            }
+            if (!PACK && p.experiment != 1 && p.experiment != 2) {
                 constexpr int NCH = TBN / 32;
                 const uint32_t tb = lane_base + acc * TBN;
 #if SW_EPI_PAIRS
                 // two 32-column chunks per stage, two stages: 64 columns in flight while 64
                 // are examined, so a tile costs NCH / 2 TMEM round trips instead of NCH
-                static_assert(NCH % 4 == 0, "pairs of stages");
+                static_assert(PACK || NCH % 4 == 0, "pairs of stages");
                 uint32_t ra[32], ra2[32], rb[32], rb2[32];
                 __syncwarp();
                 ptx::tmem_ld32(tb, ra);
@@ -597,7 +659,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     ptx::tmem_ld_wait();
                 }
 #else
-                static_assert(NCH % 2 == 0, "even");
+                static_assert(PACK || NCH % 2 == 0, "even");
                 uint32_t ra[32], rb[32];
                 __syncwarp();
                 ptx::tmem_ld32(tb, ra);
@@ -719,6 +781,21 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32
     return r == CUDA_SUCCESS;
 }
 
+// the arena viewed as [S][Rp][Dp] bf16, boxes (64, R, entries): packed pyramid tiles
+bool encode_3d(CUtensorMap* m, void* base, uint64_t inner, uint64_t rp, uint64_t slots,
+               uint32_t r, uint32_t box_entries) {
+    PFN_encodeTiled enc = get_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {inner, rp, slots};
+    cuuint64_t strides[2] = {inner * sizeof(__nv_bfloat16), rp * inner * sizeof(__nv_bfloat16)};
+    cuuint32_t box[3] = {64, r, box_entries};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult res = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return res == CUDA_SUCCESS;
+}
+
 template <int RP, int KL, bool PAIR, bool TS>
 void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
     auto kern = k_score_tc<RP, KL, PAIR, TS>;
@@ -736,9 +813,12 @@ void launch_tc_kl(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        SW_CUDA(cudaLaunchKernelEx(&cfg, kern, c.tm_q, TS ? c.tm_rows_q64 : c.tm_rows_half, p));
+        constexpr bool PACK = (RP & (RP - 1)) != 0;
+        SW_CUDA(cudaLaunchKernelEx(&cfg, kern, c.tm_q,
+                                   TS ? c.tm_rows_q64 : (PACK ? c.tm_pack_half : c.tm_rows_half), p));
     } else {
-        kern<<<grid, THREADS, smem, st>>>(c.tm_q, c.tm_rows, p);
+        constexpr bool PACK = (RP & (RP - 1)) != 0;
+        kern<<<grid, THREADS, smem, st>>>(c.tm_q, PACK ? c.tm_pack : c.tm_rows, p);
     }
 }
 
@@ -751,7 +831,12 @@ void launch_tc_rp(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_
 }
 
 template <bool PAIR, bool TS>
-void launch_tc(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+void launch_tc(Ctx& c, const TcParams& p, dim3 grid, size_t smem, cudaStream_t st, bool pack) {
+    if (pack && !TS) {  // packed pyramid tiles (no pad rows in the MMA)
+        if (c.R == 7) launch_tc_rp<7, PAIR, false>(c, p, grid, smem, st);
+        else launch_tc_rp<3, PAIR, false>(c, p, grid, smem, st);
+        return;
+    }
     switch (c.Rp) {
         case 1: launch_tc_rp<1, PAIR, TS>(c, p, grid, smem, st); break;
         case 2: launch_tc_rp<2, PAIR, TS>(c, p, grid, smem, st); break;
@@ -854,6 +939,14 @@ bool encode_tensor_maps(Ctx& c) {
     ok = ok && encode_2d(&c.tm_rows_half, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN / 2);
     ok = ok && encode_2d(&c.tm_rows_q64, c.rows_bf, (uint64_t)c.Dp, (uint64_t)(c.S * c.Rp), BN_TS / 2);
     ok = ok && encode_2d(&c.tm_q, c.q_bf, (uint64_t)c.Dp, (uint64_t)c.BmaxPad, BM);
+    // packed pyramid tiles when R is 3 or 7 (the padded power of two wastes 1/4 or 1/8)
+    c.pack_ok = false;
+    if (ok && (c.R == 7 || c.R == 3) && c.Rp == c.R + 1) {
+        c.pack_ok = encode_3d(&c.tm_pack, c.rows_bf, (uint64_t)c.Dp, (uint64_t)c.Rp, (uint64_t)c.S,
+                              (uint32_t)c.R, 32) &&
+                    encode_3d(&c.tm_pack_half, c.rows_bf, (uint64_t)c.Dp, (uint64_t)c.Rp,
+                              (uint64_t)c.S, (uint32_t)c.R, 16);
+    }
     return ok;
 }
 
@@ -880,13 +973,20 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     }();
     const bool pair = pair_ok && qb >= 2 && qb % 2 == 0;
     const bool ts = pair && ts_ok && p.kch * 32 <= 256 && p.kch % 2 == 0;
-    int stage_bytes = B_STAGE, a_bytes = p.kch * A_CHUNK, max_stages = 8;
+    // packed pyramid tiles (SW_SCORE_PACK=0 keeps the padded 256-row tiles, for A/B timing)
+    static const bool pack_env = [] {
+        const char* e = getenv("SW_SCORE_PACK");
+        return !(e && e[0] == '0');
+    }();
+    const bool pack = pack_env && c.pack_ok && !ivf && !ts;
+    const int tile_rows = pack ? 32 * c.R : BN;
+    int stage_bytes = tile_rows * 128, a_bytes = p.kch * A_CHUNK, max_stages = 8;
     if (ts) {
         stage_bytes = 2 * B_QUARTER;  // two 64-wide K chunks per stage
         a_bytes = 0;
         max_stages = 12;
     } else if (pair) {
-        stage_bytes = B_HALF;
+        stage_bytes = tile_rows / 2 * 128;
     }
     // CTA pairs keep 4 B stages: measured as fast as 6 (0.711 vs 0.708-0.729 ms; 3 stages lose
     // 12%), and the ~35 KB of shared memory it frees per SM lets one k_finish CTA of the
@@ -900,7 +1000,7 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
     SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
     const int tbn = ts ? BN_TS : BN;
     const int64_t rows_hw = c.high_water * c.Rp;
-    p.n_tiles = (rows_hw + tbn - 1) / tbn;
+    p.n_tiles = pack ? (c.high_water + 31) / 32 : (rows_hw + tbn - 1) / tbn;  // packed: 32 entries
     const int qblocks = qb;
     int64_t chunks = std::max<int64_t>(1, c.num_sms / qblocks);
     chunks = std::min<int64_t>(chunks, p.n_tiles);
@@ -957,12 +1057,13 @@ int launch_score_tc(Ctx& c, int B, int k, bool ivf, cudaStream_t st) {
         return e ? atoi(e) : 0;
     }();
     p.experiment = experiment;
+    c.last_score_pack = pack;
     if (ts)
-        launch_tc<true, true>(c, p, grid, smem, st);
+        launch_tc<true, true>(c, p, grid, smem, st, false);
     else if (pair)
-        launch_tc<true, false>(c, p, grid, smem, st);
+        launch_tc<true, false>(c, p, grid, smem, st, pack);
     else
-        launch_tc<false, false>(c, p, grid, smem, st);
+        launch_tc<false, false>(c, p, grid, smem, st, pack);
     SW_CUDA(cudaGetLastError());
     return 1;
 }

@@ -147,6 +147,7 @@ struct Ctx {
     bool last_ivf = false;         // last search probed IVF lists (nprobe < C)
     bool last_score_pair = false;  // last scoring launch ran as tcgen05 CTA pairs
     bool last_score_ts = false;    // ... with the queries resident in TMEM (TS MMA)
+    bool last_score_pack = false;  // ... on packed pyramid tiles (no pad rows)
     int32_t* cand_slot = nullptr;   // [Bmax][kCandCap]
     float* cand_score = nullptr;    // [Bmax][kCandCap]
     double* cand_exact = nullptr;   // [Bmax][kCandCap]
@@ -173,6 +174,11 @@ struct Ctx {
     CUtensorMap tm_rows{};
     CUtensorMap tm_rows_half{};  // 128-row boxes for the CTA-pair scoring kernel
     CUtensorMap tm_rows_q64{};   // 64-row boxes for the CTA-pair TMEM-A (TS) kernel
+    // packed pyramid tiles (R in {3, 7}: 32 entries x R rows, the pad row skipped): 3-D boxes
+    // (64, R, 32) and (64, R, 16) over the arena viewed as [S][Rp][Dp]
+    CUtensorMap tm_pack{};
+    CUtensorMap tm_pack_half{};
+    bool pack_ok = false;
     CUtensorMap tm_q{};
     bool tc_ok = false;
     int smem_optin = 0;
