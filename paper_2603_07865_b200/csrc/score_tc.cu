@@ -608,19 +608,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 __syncwarp();
             };
             if (PACK && p.experiment != 1 && p.experiment != 2) {
-                // packed tile: entry e's R rows are columns [R e, R e + R); one x8 load per entry
-                // (8 in flight), its max over R columns, one compare
+                // packed tile: entry e's R rows are columns [R e, R e + R); one x8 load per entry,
+                // groups of 4 entries double-buffered (group g + 1 in flight while g is examined),
+                // the max over R columns, one compare
                 const uint32_t tb = lane_base + acc * TBN;
                 const uint32_t vb = __ldg(p.valid_bits + tile);  // 32 entries = one word
-#pragma unroll 1
-                for (int g = 0; g < 32; g += 8) {
-                    uint32_t r[8][8];
-                    __syncwarp();
+                auto exam4 = [&](uint32_t(&r)[4][8], int g) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) ptx::tmem_ld8(tb + RP * (g + u), r[u]);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < 4; ++u) {
                         float m = __uint_as_float(r[u][0]);
 #pragma unroll
                         for (int j = 1; j < RP; ++j) m = fmaxf(m, __uint_as_float(r[u][j]));
@@ -628,8 +623,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (qvalid && ((vb >> (g + u)) & 1u) && m >= theta)
                             emit_one<KL>(m, slot0 + g + u, theta, list, kth, eps2, cnt, slice, p);
                     }
-                }
+                    __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
+                };
+                uint32_t ra[4][8], rb[4][8];
                 __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ptx::tmem_ld8(tb + RP * u, ra[u]);
+                ptx::tmem_ld_wait();
+#pragma unroll 1
+                for (int g = 0; g < 32; g += 8) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) ptx::tmem_ld8(tb + RP * (g + 4 + u), rb[u]);
+                    exam4(ra, g);
+                    ptx::tmem_ld_wait();
+                    if (g + 8 < 32) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) ptx::tmem_ld8(tb + RP * (g + 8 + u), ra[u]);
+                    }
+                    exam4(rb, g + 4);
+                    ptx::tmem_ld_wait();
+                }
             }
             if (!PACK && p.experiment != 1 && p.experiment != 2) {
                 constexpr int NCH = TBN / 32;
