@@ -10,7 +10,7 @@
   config5           BASELINE config 5: Cache Manager trace replay (synth_workload 2000 x 512,
                     1K capacity, IVF 64/8, 64-request lookup batches) vs the reference's own
                     Pipeline::replay on the same trace, same box
-  parity_sample     a sample of the timed batch's choices checked against the C restatement
+  parity_sample     the timed batch's choices (all of them by default) checked against the C restatement
                     (oracle, test infrastructure) on the exported arena
 
 Everything here is measured with CUDA events on the launching stream (device time) or with
@@ -346,9 +346,10 @@ def export_arena(wc):
     return ids, rows, segs
 
 
-def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=64, nthreads=None,
+def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=None, nthreads=None,
                   arena=None):
-    """Checks n_check requests of a timed batch against the C restatement (oracle) over the
+    """Checks n_check requests (default: the whole batch) of a timed batch against the C
+    restatement (oracle) over the
     arena exported from the device (sw_arena_export) — or over `arena` = (ids, rows, segs), the
     union of every rank's exported shard in the sharded run."""
     import oracle
@@ -358,6 +359,7 @@ def parity_sample(wc, q, reqs_np, choices_np, neg, th, ps, n_check=64, nthreads=
     ar = oracle.Arena(ids, np.arange(n + 1, dtype=np.int64) * R, rows, segs["level"],
                       segs["start_s"], segs["length_s"])
     B = q.shape[0]
+    n_check = B if n_check is None else min(n_check, B)
     sel = np.linspace(0, B - 1, n_check).astype(int)
     nt = nthreads or max(1, len(os.sched_getaffinity(0)))
     t = time.perf_counter()
