@@ -311,6 +311,7 @@ __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
         }
         qbase[kMaxCentroids] = a;
         qbase[kMaxCentroids + 1] = b;  // work items (persistent scoring CTAs walk them)
+        qbase[kMaxCentroids + 2] = 0;  // their ticket counter (dynamic item scheduling)
     }
     __syncthreads();
     if (j < kMaxCentroids) qbase[j] = s_nb[j];
@@ -804,7 +805,7 @@ static void build_sorted(Ctx& c) {
         SW_CUDA(cudaMalloc(&c.d_list_tile0, sizeof(int32_t) * kMaxCentroids));
         SW_CUDA(cudaMalloc(&c.d_list_ntiles, sizeof(int32_t) * kMaxCentroids));
         SW_CUDA(cudaMalloc(&c.d_qcnt, sizeof(int32_t) * kMaxCentroids));
-        SW_CUDA(cudaMalloc(&c.d_qbase, sizeof(int32_t) * (kMaxCentroids + 2)));
+        SW_CUDA(cudaMalloc(&c.d_qbase, sizeof(int32_t) * (kMaxCentroids + 3)));
         SW_CUDA(cudaMalloc(&c.d_qlist, sizeof(int32_t) * (size_t)kMaxCentroids * c.Bmax));
     }
     std::vector<uint32_t> vb((size_t)(c.grp_cap_rows / 32 + 16), 0u);

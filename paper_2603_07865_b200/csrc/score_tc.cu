@@ -51,8 +51,6 @@ constexpr int B_HALF = B_STAGE / 2;  // CTA-pair mode: each CTA of the pair stag
 constexpr int EPI_GROUPS = SW_EPI_GROUPS_;
 constexpr int THREADS = 64 + 128 * EPI_GROUPS;
 
-constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
-constexpr uint32_t IDESC_PAIR = ptx::idesc_bf16_f32(2 * BM, BN);
 // TS mode (CTA pairs, A operand in TMEM): 128-column tiles so that 2 x 128 accumulator columns
 // + the 256 columns of the resident bf16 queries fill the 512 TMEM columns exactly.
 constexpr int BN_TS = 128;
@@ -93,6 +91,7 @@ struct TcParams {
     const uint8_t* prank;         // [B][kMaxCentroids] probe rank of each list
     int grp_ch;                   // slice of (query, list l, chunk j) = rank(l) * grp_ch + j
     const int32_t* n_items;       // grouped: device count of real items (persistent CTAs loop)
+    int32_t* ticket;              // grouped, single CTAs: dynamic item tickets (zeroed per search)
     int ivf;                      // IVF mode: only rows of the query's probed lists count
     const int16_t* row_list;      // [rows] list of every stored row
     const uint64_t* pmask;        // [B][4] probed-list bitmask per query
@@ -253,8 +252,48 @@ __global__ void __launch_bounds__(THREADS, 1)
         return !bal || i == first || item_at(i).qrow != item_at(i - istep).qrow;
     };
     const int n_items = p.items ? *p.n_items : bal ? p.n_items_bal : 1;
-    const int item0 = (p.items || bal) ? unit : 0;
-    if (item0 >= n_items || item_at(item0).ntiles == 0) return;  // uniform for the CTA / pair
+    // Grouped IVF on single CTAs takes items from a ticket counter instead of the static
+    // blockIdx.x + k gridDim.x walk: list chunks differ in size by several times, and the static
+    // walk left the first SMs idle at 44% of the kernel (ncu: active cycles 216K-489K). The
+    // producer lane fetches ticket k + 1 once item k's loads are issued and publishes it in a
+    // 4-slot shared ring (full / empty mbarriers); the MMA and epilogue warps read the same
+    // sequence, so every role walks the same items.
+    // (in the dynamic shared memory after the pipeline barriers: the kernel's dynamic size is
+    // set to the opt-in maximum, so it may have no static shared memory)
+    constexpr int kTk = 4;
+    uint64_t* s_tbar = &bars[2 * S + 8];                           // full[kTk] | empty[kTk]
+    int* s_tick = reinterpret_cast<int*>(&bars[2 * S + 8 + 2 * kTk]);  // [kTk]
+    int& s_first = s_tick[kTk];
+    const bool dyn = !PAIR && p.items && p.ticket;
+    int item0 = (p.items || bal) ? unit : 0;
+    if (dyn) {
+        if (threadIdx.x == 0) s_first = atomicAdd(p.ticket, 1);
+        __syncthreads();
+        item0 = s_first;
+        if (item0 >= n_items) return;  // uniform for the CTA
+    } else if (item0 >= n_items || item_at(item0).ntiles == 0) {
+        return;  // uniform for the CTA / pair
+    }
+    // ticket k + 1 (k >= 0); static walk: item0 + (k + 1) istep. -1: no more items.
+    auto prod_next = [&](int k, int ii) {
+        if (!dyn) return ii + istep < n_items ? ii + istep : -1;
+        const int j = k, slot = j % kTk;
+        if (j >= kTk) ptx::mbar_wait(ptx::smem_u32(&s_tbar[kTk + slot]), (uint32_t)(((j / kTk) - 1) & 1));
+        const int t = atomicAdd(p.ticket, 1);
+        const int v = t < n_items ? t : -1;
+        s_tick[slot] = v;
+        ptx::mbar_arrive(ptx::smem_u32(&s_tbar[slot]));
+        return v;
+    };
+    auto cons_next = [&](int k, int ii) {  // all lanes of the calling warp
+        if (!dyn) return ii + istep < n_items ? ii + istep : -1;
+        const int j = k, slot = j % kTk;
+        ptx::mbar_wait(ptx::smem_u32(&s_tbar[slot]), (uint32_t)((j / kTk) & 1));
+        const int v = s_tick[slot];
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(ptx::smem_u32(&s_tbar[kTk + slot]));
+        return v;
+    };
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
     const bool leader = rank == 0;
 
@@ -269,6 +308,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(bar(TFULL + i), 1);
             ptx::mbar_init(bar(TEMPTY + i), PAIR ? 8 : 4);  // one group of 4 warps per acc
         }
+        if (dyn)
+            for (int i = 0; i < kTk; ++i) {
+                ptx::mbar_init(ptx::smem_u32(&s_tbar[i]), 1);  // the producer lane
+                ptx::mbar_init(ptx::smem_u32(&s_tbar[kTk + i]), 1 + 4 * EPI_GROUPS);  // MMA + epilogue warps
+            }
         ptx::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -298,7 +342,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             int s = 0;  // ring stage and its phase, advanced incrementally (no division)
             uint32_t ph = 0;
             int na = 0;  // A loads issued
-            for (int ii = item0; ii < n_items; ii += istep) {
+            int kk = 0;
+            for (int ii = item0; ii >= 0; ii = prod_next(kk++, ii)) {
                 const Item itm = item_at(ii);
                 const int qrow = itm.qrow;
                 const int64_t t0 = itm.t0;
@@ -370,7 +415,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ph = 0;
             int gt = 0;  // tiles across items: accumulator index and phase
             int na = 0;  // A loads consumed
-            for (int ii = item0; ii < n_items; ii += istep) {
+            int kk = 0;
+            for (int ii = item0; ii >= 0;) {
                 const int ntiles = item_at(ii).ntiles;
                 if (loads_a(ii, item0)) {
                     if (TS)
@@ -426,14 +472,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                     __syncwarp();
                 }
                 // the item's MMAs are issued: A may be overwritten once they complete (signalled
-                // only when the next item reloads A; both CTAs of a pair are told)
-                if (ii + istep < n_items && loads_a(ii + istep, item0) && ptx::elect_one()) {
+                // only when the next item reloads A — dynamic tickets: after every item, the next
+                // being unknown here; both CTAs of a pair are told)
+                if ((dyn || (ii + istep < n_items && loads_a(ii + istep, item0))) &&
+                    ptx::elect_one()) {
                     if (PAIR)
                         ptx::mma_commit_pair(bar(AEMPTY));
                     else
                         ptx::mma_commit(bar(AEMPTY));
                 }
                 __syncwarp();
+                ii = cons_next(kk++, ii);
             }
         }
         __syncwarp();
@@ -444,7 +493,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
         const int grp = (warp - 2) >> 2;  // drains accumulator grp: tiles grp, grp + 2, ...
         int gt = 0;  // tiles across items (accumulator index / phase, as the MMA counts them)
-        for (int ii = item0; ii < n_items; ii += istep) {
+        int kk = 0;
+        for (int ii = item0; ii >= 0; ii = cons_next(kk++, ii)) {
         const Item itm = item_at(ii);
         const int qrow = itm.qrow;
         const int64_t t0 = itm.t0;
@@ -900,6 +950,11 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.prank = c.prank;
     p.grp_ch = c.grp_ch;
     p.n_items = c.d_qbase + kMaxCentroids + 1;  // device count written by k_group_plan
+    static const bool dyn_ok = [] {
+        const char* e = getenv("SW_IVF_DYN");
+        return !(e && e[0] == '0');
+    }();
+    p.ticket = (!pair && dyn_ok) ? c.d_qbase + kMaxCentroids + 2 : nullptr;  // zeroed by k_group_plan
     p.n_chunks = std::min(eff_nprobe(c), c.ivf_C) * c.grp_ch;
     SW_REQUIRE(p.n_chunks <= kMaxSlices, "grouped IVF: too many slices per query");
     p.cap_local = (kCandCap / p.n_chunks) & ~3;
