@@ -6,6 +6,7 @@
  * constants, not code) */
 #include "noise_table.h"
 #include "exp_table.h"
+#include "noise_def.h"
 
 #include <math.h>
 #include <pthread.h>
@@ -491,10 +492,13 @@ void so_exp_pair(const double* x, int64_t n, double* ours, double* lib) {
 }
 
 /* ------------------------------------------------------------------ align + noise (ours) */
-void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+/* Philox4x32-R (Salmon et al., SC'11): R rounds of the 4x32 bijection with the Weyl key
+ * schedule. so_philox4x32_10 is Random123's default (pinned by its known-answer vector);
+ * K4's noise uses R = SW_PHILOX_ROUNDS (noise_def.h). */
+void so_philox4x32_r(const uint32_t ctr[4], const uint32_t key[2], int rounds, uint32_t out[4]) {
     uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
     uint32_t k0 = key[0], k1 = key[1];
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < rounds; ++r) {
         uint64_t p0 = (uint64_t)0xD2511F53u * c0;
         uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
         uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
@@ -507,6 +511,10 @@ void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
         k1 += 0xBB67AE85u;
     }
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    so_philox4x32_r(ctr, key, 10, out);
 }
 
 static float as_f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
@@ -538,7 +546,7 @@ void so_philox_normals(uint64_t seed, uint64_t rid, int64_t n, float* out) {
                            (uint32_t)(rid >> 32)};
         uint32_t r[4];
         float z[4];
-        so_philox4x32_10(ctr, key, r);
+        so_philox4x32_r(ctr, key, SW_PHILOX_ROUNDS, r);
         for (int t = 0; t < 4; ++t) z[t] = icdf_normal(r[t]);
         for (int t = 0; t < 4 && i + t < n; ++t) out[i + t] = z[t];
     }

@@ -86,6 +86,7 @@ int so_plan_batch(const so_arena* ar, const float* neg, int B, const float* quer
                   int fixed_arm, int nthreads, so_plan* out, so_hit* hits_out);
 
 /* ---- our align + noise definition (no reference counterpart) ---- */
+void so_philox4x32_r(const uint32_t ctr[4], const uint32_t key[2], int rounds, uint32_t out[4]);
 void so_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 /* glibc 2.39 exp (FMA build), restated op for op (the reference's std::exp). */
 double so_ref_exp(double x);
@@ -95,7 +96,7 @@ double so_ref_log1p(double x);
 void so_log1p_pair(const double* x, int64_t n, double* ours, double* lib);
 /* The normal transform of each 32-bit word. */
 void so_icdf_normals(const uint32_t* words, int64_t n, float* out);
-/* n standard normals for (seed, request_id), element i from philox counter (i/4, rid). */
+/* n standard normals for (seed, request_id), element i from Philox4x32-7 counter (i/4, rid). */
 void so_philox_normals(uint64_t seed, uint64_t request_id, int64_t n, float* out);
 /* x_t[c][t][f] = fmaf(s1, eps, s0 * x0[c][lo + t mod T_seg][f]), t < T_out = llround(L*fps).
  * eps == NULL -> Philox normals (seed, request_id). Returns T_out. */

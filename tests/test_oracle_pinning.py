@@ -185,6 +185,19 @@ def test_philox_known_answer(orc):
     out = (C.c_uint32 * 4)()
     orc.lib.so_philox4x32_10((C.c_uint32 * 4)(0, 0, 0, 0), (C.c_uint32 * 2)(0, 0), out)
     assert list(out) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    # the noise generator is the same round function run 7 times (csrc/noise_def.h): R rounds
+    # are a prefix of R + 1, and 10 rounds through so_philox4x32_r equal the pinned vector
+    r10 = (C.c_uint32 * 4)()
+    orc.lib.so_philox4x32_r((C.c_uint32 * 4)(0, 0, 0, 0), (C.c_uint32 * 2)(0, 0), 10, r10)
+    assert list(r10) == list(out)
+    ctr, key = (C.c_uint32 * 4)(7, 0, 123, 456), (C.c_uint32 * 2)(0x5EED, 1)
+    r7, r8, step = (C.c_uint32 * 4)(), (C.c_uint32 * 4)(), (C.c_uint32 * 4)()
+    orc.lib.so_philox4x32_r(ctr, key, 7, r7)
+    orc.lib.so_philox4x32_r(ctr, key, 8, r8)
+    # round 8 = one round of the bijection on round 7's output with the key bumped 7 times
+    k8 = (C.c_uint32 * 2)((0x5EED + 7 * 0x9E3779B9) & 0xFFFFFFFF, (1 + 7 * 0xBB67AE85) & 0xFFFFFFFF)
+    orc.lib.so_philox4x32_r(r7, k8, 1, step)
+    assert list(step) == list(r8)
     z = orc.philox_normals(1, 2, 1 << 16)
     assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
 
@@ -209,7 +222,7 @@ def test_normal_transform_tracks_erfcinv(orc):
 
 
 def test_noise_distribution(orc):
-    """Philox4x32-10 words through the transform are N(0, 1): moments and the Kolmogorov-Smirnov
+    """Philox4x32-7 words (the noise generator) through the transform are N(0, 1): moments and the Kolmogorov-Smirnov
     distance over 4M draws of one request (KS 1%-critical value 1.63 / sqrt(n) = 8.2e-4)."""
     from scipy.special import ndtr
     n = 1 << 22
