@@ -284,9 +284,20 @@ __global__ void k_group_count(const uint8_t* __restrict__ prank, int C, int np,
 // blocks come in pairs (the odd one padded with an empty block) and one item covers two blocks —
 // a CTA pair (cta_group::2, M = 256) — so the list's tiles stream from HBM once per 256 queries
 // instead of once per 128.
+// SW_IVF_LPT=0: grouped IVF items in list order instead of longest-first (A/B timing)
+static bool ivf_lpt() {
+    static const bool on = [] {
+        const char* e = getenv("SW_IVF_LPT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+constexpr int kMaxTpc = 255;  // tiles per grouped item (SW_IVF_TPC), bucketed by k_group_plan
+
 __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
                              const int32_t* __restrict__ tile0, const int32_t* __restrict__ ntl,
-                             int tpc, int pair, int32_t* __restrict__ qbase,
+                             int tpc, int pair, int sort_items, int32_t* __restrict__ qbase,
                              int4* __restrict__ items) {
     __shared__ int s_nb[kMaxCentroids], s_ni[kMaxCentroids];
     const int j = threadIdx.x;
@@ -315,6 +326,44 @@ __global__ void k_group_plan(const int32_t* __restrict__ qcnt, int C,
     }
     __syncthreads();
     if (j < kMaxCentroids) qbase[j] = s_nb[j];
+    // Item order = the order the persistent CTAs take tickets in. Items are long (a chunk of
+    // ~20 tiles streams ~5 MB at an SM's share of HBM) and each CTA runs only ~2-3 of them, so
+    // the kernel's tail is set by what is left at the end: a list's tiles are split into ch
+    // near-equal chunks (no short remainder chunk), and items are taken largest first
+    // (longest-processing-time order) through shared-memory bucket counters by size (the
+    // order within a size is arbitrary: results do not depend on which CTA scores an item).
+    // The static walk (SW_IVF_DYN=0, pairs) keeps list order and tpc-sized chunks.
+    __shared__ int s_bkt[kMaxTpc + 1];
+    const bool lpt = !pair && sort_items && tpc <= kMaxTpc;
+    if (lpt) {
+        const int nbs = nb / bstep;
+        const int csz = ch > 0 ? ntl[j] / ch : 0, cex = ch > 0 ? ntl[j] % ch : 0;  // sizes
+        if (j <= kMaxTpc) s_bkt[j] = 0;
+        __syncthreads();
+        if (nbs > 0 && cex > 0) atomicAdd(&s_bkt[csz + 1], nbs * cex);
+        if (nbs > 0 && csz > 0) atomicAdd(&s_bkt[csz], nbs * (ch - cex));
+        __syncthreads();
+        if (j == 0) {  // bucket starts, largest chunks first
+            int a = 0;
+            for (int r = kMaxTpc; r >= 1; --r) {
+                const int x = s_bkt[r];
+                s_bkt[r] = a;
+                a += x;
+            }
+        }
+        __syncthreads();
+        int pbig = 0, psmall = 0;
+        if (nbs > 0 && cex > 0) pbig = atomicAdd(&s_bkt[csz + 1], nbs * cex);
+        if (nbs > 0 && csz > 0) psmall = atomicAdd(&s_bkt[csz], nbs * (ch - cex));
+        for (int b = 0; b < nb; b += bstep)
+            for (int jj = 0; jj < ch; ++jj) {
+                const int nt = csz + (jj < cex ? 1 : 0);
+                const int t0 = jj * csz + min(jj, cex);
+                items[jj < cex ? pbig++ : psmall++] =
+                    make_int4((s_nb[j] + b) * 128, tile0[j] + t0, nt, j | (jj << 8));
+            }
+        return;
+    }
     for (int b = 0; b < nb; b += bstep)
         for (int jj = 0; jj < ch; ++jj)
             items[s_ni[j] + b / bstep * ch + jj] =
@@ -776,11 +825,11 @@ static void build_sorted(Ctx& c) {
             sorted[(size_t)pos[(size_t)rl[(size_t)i]]++] = (int32_t)i;
     // chunking: tpc tiles per work item, <= kMaxSlices / nprobe chunks per list
     const int np = std::max(1, std::min(eff_nprobe(c), C));
-    // 16+ tiles per item amortise the per-item pipeline ramp (A load, TMA / MMA fill, drain)
-    // 24 measured best at the reference default (64 lists, nprobe 8, B = 1024, 1M rows):
-    // score 0.285-0.292 ms vs 0.301 (16), 0.308 (28), 0.33 (20, 32), 0.38 (8) — shorter items
-    // pay the per-item ramp (A load, pipeline fill and drain), longer ones balance worse over
-    // the 148 persistent CTAs. SW_IVF_TPC overrides.
+    // 16+ tiles per item amortise the per-item pipeline ramp (A load, TMA / MMA fill, drain).
+    // At the reference default (64 lists, nprobe 8, B = 1024, 1M rows: ~61 tiles per list),
+    // with near-equal chunks taken largest first (k_group_plan): score 0.257 ms at 24 or 28
+    // (3 or 2-3 chunks of ~20-30 tiles per list) vs 0.277 (16, 20) and 0.309 (32: 2 chunks
+    // per list, too few items to balance over 148 CTAs). SW_IVF_TPC overrides.
     static const int tpc_min = [] {
         const char* e = getenv("SW_IVF_TPC");
         return e ? std::max(1, atoi(e)) : 24;
@@ -873,8 +922,8 @@ int64_t ivf_group_prepare(Ctx& c, int B, cudaStream_t st) {
     SW_CUDA(cudaMemsetAsync(c.d_items, 0, sizeof(int4) * max_items, st));
     k_group_count<<<B, kMaxCentroids, 0, st>>>(c.prank, c.ivf_C, np, c.d_qcnt, c.d_qlist, c.Bmax);
     k_group_plan<<<1, kMaxCentroids, 0, st>>>(c.d_qcnt, c.ivf_C, c.d_list_tile0, c.d_list_ntiles,
-                                              c.grp_tpc, c.grp_pair ? 1 : 0, c.d_qbase,
-                                              c.d_items);
+                                              c.grp_tpc, c.grp_pair ? 1 : 0, ivf_lpt() ? 1 : 0,
+                                              c.d_qbase, c.d_items);
     k_group_gather<<<(unsigned)((blocks * 128 + 7) / 8), 256, 0, st>>>(
         c.d_qcnt, c.d_qlist, c.d_qbase, c.ivf_C, c.Bmax, c.q_bf, c.Dp, c.d_qg, c.d_qmap,
         blocks * 128);
