@@ -48,6 +48,7 @@ struct FinishParams {
     int64_t n_slots;
     const int32_t* slice_cnt;
     const int32_t* cand_slot;
+    const int32_t* sorted_slot;  // grouped IVF: emitted slots are list-sorted rows -> arena slot
     const float* cand_score;
     const float* cta_topk;
     const float* q_eps;
@@ -448,7 +449,10 @@ __global__ void __launch_bounds__(FTT, FTT == 64 ? 7 : 1) k_finish(const FinishP
                 for (int u = 0; u < 8; ++u) v[u] = f + u < seg_end ? p.cand_score[src + f + u] : -INFINITY;
 #pragma unroll
                 for (int u = 0; u < 8; ++u)  // (cut may be -inf: keep every real entry)
-                    if (f + u < seg_end && v[u] >= cut) keep(p.cand_slot[src + f + u]);
+                    if (f + u < seg_end && v[u] >= cut) {
+                        const int32_t cs = p.cand_slot[src + f + u];
+                        keep(p.sorted_slot ? __ldg(p.sorted_slot + cs) : cs);
+                    }
             }
             f = seg_end;
         }
@@ -1066,6 +1070,10 @@ int launch_search_fused(Ctx& c, const float* d_q, int B, int k, int rank, const 
     p.n_slots = c.high_water;
     p.slice_cnt = c.slice_cnt;
     p.cand_slot = c.cand_slot;
+    // the grouped scoring emits list-sorted row indices (no lookup on its emission path); the
+    // kept candidates are mapped to arena slots here. The sorted copy is rebuilt only after a
+    // mutation, which first drains in-flight batches (wait_readers), so it is stable here.
+    p.sorted_slot = grp_items > 0 ? c.d_sorted_slot : nullptr;
     p.cand_score = c.cand_score;
     p.cta_topk = c.cta_topk;
     p.q_eps = c.q_eps;

@@ -87,7 +87,6 @@ struct TcParams {
     // list-sorted arena copy. items[b] = {gathered row base, tile0, n_tiles (0: idle), l | j<<8}.
     const int4* items;
     const int32_t* qmap;          // gathered row -> query id (-1: padding)
-    const int32_t* sorted_slot;   // list-sorted row -> arena slot (-1: padding)
     const uint8_t* prank;         // [B][kMaxCentroids] probe rank of each list
     int grp_ch;                   // slice of (query, list l, chunk j) = rank(l) * grp_ch + j
     const int32_t* n_items;       // grouped: device count of real items (persistent CTAs loop)
@@ -128,8 +127,8 @@ __device__ __forceinline__ void emit_chunk(const uint32_t (&r)[32], uint32_t mas
         const float m = fminf(1.0f, fmaxf(-1.0f, t[0]));
         if (m < theta) continue;  // theta may have risen within this chunk
         if (cnt < p.cap_local) {
-            p.cand_slot[slice + cnt] =
-                p.sorted_slot ? p.sorted_slot[slot_c + e] : (int32_t)(slot_c + e);
+            // grouped IVF: the list-sorted row; k_finish maps the kept ones to arena slots
+            p.cand_slot[slice + cnt] = (int32_t)(slot_c + e);
             p.cand_score[slice + cnt] = m;
         }
         ++cnt;
@@ -946,7 +945,6 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.cand_score = c.cand_score;
     p.items = c.d_items;
     p.qmap = c.d_qmap;
-    p.sorted_slot = c.d_sorted_slot;
     p.prank = c.prank;
     p.grp_ch = c.grp_ch;
     p.n_items = c.d_qbase + kMaxCentroids + 1;  // device count written by k_group_plan
@@ -961,7 +959,7 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     c.last_chunks = p.n_chunks;
     c.last_score_pair = pair;
     c.last_score_ts = false;
-    p.experiment = 0;
+    p.experiment = [] { const char* e = getenv("SW_SCORE_EXPERIMENT"); return e ? atoi(e) : 0; }();  // profiling only
     const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * bstg + 512;
     auto kern = [&](auto rp_tag, auto kl_tag) {
         constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
