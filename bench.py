@@ -203,10 +203,10 @@ def reference_sample(n_entries, n_queries, nthreads, seed=1, cache=None, ivf=Non
     return run, idx
 
 
-def ncu_traffic(prefix):
-    """DRAM bytes per launch of a kernel from the committed ncu summary (profiles/), or None."""
+def ncu_traffic(prefix, summary="ncu_latest.json"):
+    """DRAM bytes per launch of a kernel from a committed ncu summary (profiles/), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+        with open(os.path.join(ROOT, "profiles", summary)) as f:
             t = json.load(f)["traffic_bytes"]
         for k, v in t.items():
             if k.startswith(prefix):
@@ -897,6 +897,12 @@ def main():
                     "traffic": None, "traffic_source": "not captured for this configuration",
                     "kernel_ms": round(score_ms, 4),
                     "share_of_step": round(score_ms / total_ms_step, 3)}
+        if (args.ivf or "").replace(" ", "") in ("64,8",):  # the configuration the capture is of
+            tb, tk = ncu_traffic("k_score_tc<1, 8, 0, 0>", "ncu_ivf_latest.json")
+            if tb:
+                roof_ivf["traffic"] = tb
+                roof_ivf["traffic_source"] = ("profiles/ncu_ivf_latest.json (ncu --set full, one "
+                                              "launch of " + tk + ", bench.py --ivf 64,8)")
     value = B * steps / (ms / 1000.0)
     stage_ms = {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items() if v[1]}
 
