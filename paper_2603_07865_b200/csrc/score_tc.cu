@@ -94,6 +94,7 @@ struct TcParams {
     int ivf;                      // IVF mode: only rows of the query's probed lists count
     const int16_t* row_list;      // [rows] list of every stored row
     const uint64_t* pmask;        // [B][4] probed-list bitmask per query
+    int stream_a;    // grouped IVF: queries streamed with every ring stage (no resident A)
     int experiment;  // 0 normal; profiling only (SW_SCORE_EXPERIMENT): 1 = epilogue skipped,
                      // 2 = also no cache TMA (pure MMA rate)
 };
@@ -195,7 +196,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t ID_PAIR = ptx::idesc_bf16_f32(2 * BM, TBN);
     constexpr uint32_t ID_ONE = ptx::idesc_bf16_f32(BM, TBN);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + (TS ? 0 : p.kch * A_CHUNK);
+    // stream_a: [S][A_CHUNK] query chunks, then [S][BSTG]; otherwise the resident A [kch][A_CHUNK]
+    uint8_t* sB = smem + (TS ? 0 : (p.stream_a ? p.n_stages : p.kch) * A_CHUNK);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + p.n_stages * BSTG);
     const int S = p.n_stages;
     // full[S] | empty[S] | a_full | tfull[2] | tempty[2] | a_empty
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int qrow = itm.qrow;
                 const int64_t t0 = itm.t0;
                 const int ntiles = itm.ntiles;
-                const bool lda = loads_a(ii, item0);
+                const bool lda = !p.stream_a && loads_a(ii, item0);
                 if (lda && na > 0) ptx::mbar_wait_sleep(bar(AEMPTY), (uint32_t)((na - 1) & 1));
                 if (lda) ++na;
                 if (!lda) {
@@ -389,6 +391,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                                         ptx::smem_u32(sB + s * BSTG + u * (BSTG / KPS)), &tmE, bar(FULL + s),
                                         (kc + u) * 64, (int32_t)(tile * TBN + rank * (TBN / 2)));
                             }
+                        } else if (!PACK && !TS && p.stream_a) {
+                            // the stage carries the item's query chunk kc with the tile's chunk
+                            ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)(BSTG + A_CHUNK));
+                            ptx::tma_load_2d(ptx::smem_u32(sA + s * A_CHUNK), &tmQ, bar(FULL + s),
+                                             kc * 64, qrow);
+                            ptx::tma_load_2d(ptx::smem_u32(sB + s * BSTG), &tmE, bar(FULL + s),
+                                             kc * 64, (int32_t)(tile * BN));
                         } else {
                             ptx::mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)BSTG);
                             if (PACK)
@@ -417,7 +426,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             int kk = 0;
             for (int ii = item0; ii >= 0;) {
                 const int ntiles = item_at(ii).ntiles;
-                if (loads_a(ii, item0)) {
+                if (!p.stream_a && loads_a(ii, item0)) {
                     if (TS)
                         ptx::mbar_wait_cluster(bar(AFULL), (uint32_t)(na & 1));
                     else
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                              ph ^= (s == 0) ? 1u : 0u) {
                         ptx::mbar_wait_sleep(bar(FULL + s), ph);
                         ptx::tc_fence_after();
-                        const uint64_t ad = adesc0 + (uint64_t)(kc * (A_CHUNK >> 4));
+                        const uint64_t ad = adesc0 + (uint64_t)((p.stream_a ? s : kc) * (A_CHUNK >> 4));
                         const uint64_t bd = bdesc0 + (uint64_t)(s * (BSTG >> 4));
                         if (ptx::elect_one()) {
     #pragma unroll
@@ -473,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // the item's MMAs are issued: A may be overwritten once they complete (signalled
                 // only when the next item reloads A — dynamic tickets: after every item, the next
                 // being unknown here; both CTAs of a pair are told)
-                if ((dyn || (ii + istep < n_items && loads_a(ii + istep, item0))) &&
+                if (!p.stream_a && (dyn || (ii + istep < n_items && loads_a(ii + istep, item0))) &&
                     ptx::elect_one()) {
                     if (PAIR)
                         ptx::mma_commit_pair(bar(AEMPTY));
@@ -926,7 +935,16 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     p.k = k;
     const bool pair = c.grp_pair;
     const int bstg = pair ? B_HALF : B_STAGE;
-    p.n_stages = std::min(8, (budget - p.kch * A_CHUNK) / bstg);
+    // SW_IVF_STREAM_A=0: queries resident per item (128 KB of shared memory: a 3-deep B ring)
+    static const bool stream_a_env = [] {
+        const char* e = getenv("SW_IVF_STREAM_A");
+        return !(e && e[0] == '0');
+    }();
+    p.stream_a = (!pair && stream_a_env) ? 1 : 0;
+    p.n_stages = p.stream_a ? std::min(8, budget / (bstg + A_CHUNK))
+                            : std::min(8, (budget - p.kch * A_CHUNK) / bstg);
+    static const int env_st = [] { const char* e = getenv("SW_IVF_STAGES"); return e ? atoi(e) : 0; }();
+    if (env_st >= 2) p.n_stages = std::min(p.n_stages, env_st);
     SW_REQUIRE(p.n_stages >= 2, "tcgen05 scoring: not enough shared memory for 2 stages");
     p.n_tiles = c.grp_rows / BN;
     p.tiles_per_cta = 1;
@@ -960,7 +978,8 @@ int launch_score_tc_grouped(Ctx& c, int B, int k, int64_t max_items, cudaStream_
     c.last_score_pair = pair;
     c.last_score_ts = false;
     p.experiment = [] { const char* e = getenv("SW_SCORE_EXPERIMENT"); return e ? atoi(e) : 0; }();  // profiling only
-    const size_t smem = 1024 + (size_t)p.kch * A_CHUNK + (size_t)p.n_stages * bstg + 512;
+    const size_t smem = 1024 + (size_t)(p.stream_a ? p.n_stages : p.kch) * A_CHUNK +
+                        (size_t)p.n_stages * bstg + 512;
     auto kern = [&](auto rp_tag, auto kl_tag) {
         constexpr int RPv = decltype(rp_tag)::value, KLv = decltype(kl_tag)::value;
         if (pair) {
